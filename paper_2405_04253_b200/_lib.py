@@ -1,0 +1,222 @@
+"""ctypes binding of libfntgpu.so (C ABI in include/fntgpu.h).
+
+The product path: every compute entry point of the shim goes through here to
+hand-written sm_100a kernels. There is no CPU fallback -- if the library or a GPU
+is missing, calls raise.
+
+PyTorch is used only as plumbing: device allocation, host<->device copies and
+the current CUDA stream handle.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+from pathlib import Path
+
+import numpy as np
+
+_PKG = Path(__file__).resolve().parent
+LIB_PATH = _PKG / "libfntgpu.so"
+
+ABI_VERSION = 1
+
+OK, EINVAL, ECUDA, EUNSUPPORTED = 0, -1, -2, -3
+EPLAN_LENGTH, EPLAN_RADIX, EPLAN_ORDER, EPLAN_SUBORD, EPLAN_MODULUS = -10, -11, -12, -13, -14
+
+NONE, I8, I16, I32, I64, F64, C128 = 0, 1, 2, 3, 4, 5, 6
+DECODE_SIGNED = 1
+AEQ_FWD_FNT, AEQ_FWD_DIRECT = 0, 1
+AEQ_IN_PLANAR, AEQ_IN_DECIM = 0, 1
+
+vp = C.c_void_p
+
+
+class CdcTaps(C.Structure):
+    _fields_ = [("b_plus", C.c_uint32 * 64), ("b_minus", C.c_uint32 * 64),
+                ("n_taps", C.c_int32), ("reserved", C.c_int32)]
+
+
+class CdcIO(C.Structure):
+    _fields_ = [("n_streams", C.c_int32), ("in_dtype", C.c_int32),
+                ("xr", vp), ("xi", vp), ("x_stride", C.c_int64),
+                ("x_first", C.c_int64), ("x_count", C.c_int64), ("length", C.c_int64),
+                ("out_first", C.c_int64), ("out_count", C.c_int64),
+                ("out_dtype", C.c_int32), ("pad0", C.c_int32),
+                ("yr", vp), ("yi", vp), ("y_stride", C.c_int64), ("inv_scale", C.c_double),
+                ("qr", vp), ("qi", vp), ("q_stride", C.c_int64), ("q_scale", C.c_double),
+                ("q_max", C.c_int32), ("pad1", C.c_int32), ("decim_acc", vp)]
+
+
+class DecimIO(C.Structure):
+    _fields_ = [("n_links", C.c_int32), ("sps", C.c_int32), ("acc", vp), ("length", C.c_int64),
+                ("phase", vp), ("gap", vp)]
+
+
+class AeqParams(C.Structure):
+    _fields_ = [("sig_scale", C.c_double), ("tap_scale", C.c_double), ("mu", C.c_double),
+                ("radii", C.c_double * 8), ("n_radii", C.c_int32), ("forward", C.c_int32)]
+
+
+class AeqState(C.Structure):
+    _fields_ = [("w", C.c_double * 256), ("w_int", C.c_int32 * 256), ("hist", C.c_int32 * 64),
+                ("saturations", C.c_int64), ("symbols", C.c_int64), ("n_err", C.c_int64),
+                ("reserved", C.c_int64)]
+
+
+class AeqIO(C.Structure):
+    _fields_ = [("n_streams", C.c_int32), ("in_mode", C.c_int32), ("in_dtype", C.c_int32),
+                ("adapt", C.c_int32), ("x", vp), ("x_stream_stride", C.c_int64),
+                ("x_row_stride", C.c_int64), ("qr", vp), ("qi", vp), ("q_stride", C.c_int64),
+                ("phase", vp), ("n_blocks", C.c_int64), ("mu_blocks", vp), ("y", vp),
+                ("y_stream_stride", C.c_int64), ("y_row_stride", C.c_int64), ("err", vp),
+                ("err_stream_stride", C.c_int64)]
+
+
+AEQ_STATE_BYTES = C.sizeof(AeqState)
+
+# (symbol, restype, argtypes) for every function declared in include/fntgpu.h
+SIGNATURES = {
+    "fntgpu_abi_version": (C.c_int, []),
+    "fntgpu_last_error": (C.c_char_p, []),
+    "fntgpu_device_count": (C.c_int, []),
+    "fntgpu_plan_create": (C.c_int, [C.c_int, C.c_int, C.c_int64, C.POINTER(vp)]),
+    "fntgpu_plan_destroy": (C.c_int, [vp]),
+    "fntgpu_plan_set_twiddles": (C.c_int, [vp, vp, vp]),
+    "fntgpu_plan_info": (C.c_int, [vp, C.POINTER(C.c_int64), C.POINTER(C.c_int64),
+                                   C.POINTER(C.c_int)]),
+    "fntgpu_fnt": (C.c_int, [vp, C.c_int, vp, vp, C.c_int64, C.c_int, vp]),
+    "fntgpu_cyclic_convolve_real": (C.c_int, [vp, vp, vp, C.c_int64, vp, C.c_int64, C.c_int, vp]),
+    "fntgpu_cyclic_convolve_complex": (C.c_int, [vp, vp, vp, vp, vp, C.c_int64, vp, vp,
+                                                 C.c_int64, C.c_int, vp]),
+    "fntgpu_residue_map": (C.c_int, [C.c_int, C.c_int, vp, vp, C.c_int64, vp]),
+    "fntgpu_struct_sizes": (C.c_int, [C.POINTER(C.c_int64), C.c_int]),
+    "fntgpu_quantize_real": (C.c_int, [vp, C.c_int64, C.c_double, C.c_int32, C.c_int, vp, vp, vp]),
+    "fntgpu_cdc64_process": (C.c_int, [C.POINTER(CdcTaps), C.POINTER(CdcIO), vp]),
+    "fntgpu_decim_phase": (C.c_int, [C.POINTER(DecimIO), vp]),
+    "fntgpu_aeq_init": (C.c_int, [vp, C.c_int, C.POINTER(AeqParams), vp]),
+    "fntgpu_aeq_process": (C.c_int, [vp, C.POINTER(AeqParams), C.POINTER(AeqIO), vp]),
+    "fntgpu_aeq_update_taps": (C.c_int, [vp, C.POINTER(AeqParams), vp, vp, C.c_double, vp, vp]),
+}
+
+_LIB = None
+
+
+class FntGpuError(RuntimeError):
+    """A CUDA / library failure inside libfntgpu.so."""
+
+
+def load(build_if_missing: bool = True):
+    """Load libfntgpu.so (building it in-tree with nvcc if it is absent)."""
+    global _LIB
+    if _LIB is not None:
+        return _LIB
+    if not LIB_PATH.exists():
+        if not build_if_missing:
+            raise FntGpuError(f"{LIB_PATH} is missing; run paper_2405_04253_b200._build")
+        from . import _build
+        _build.build()
+    lib = C.CDLL(str(LIB_PATH))
+    for name, (res, args) in SIGNATURES.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    if lib.fntgpu_abi_version() != ABI_VERSION:
+        raise FntGpuError("libfntgpu.so ABI version mismatch; rebuild the extension")
+    _LIB = lib
+    return lib
+
+
+def last_error() -> str:
+    msg = load().fntgpu_last_error()
+    return msg.decode() if msg else ""
+
+
+def check(rc: int, where: str = "") -> None:
+    if rc == OK:
+        return
+    msg = last_error()
+    if rc == EINVAL:
+        raise ValueError(msg)
+    if rc == EUNSUPPORTED:
+        raise NotImplementedError(msg)
+    raise FntGpuError(f"{where}: {msg}" if where else msg)
+
+
+# ---------------------------------------------------------------------------
+# device plumbing (torch)
+
+_torch = None
+
+
+def torch():
+    global _torch
+    if _torch is None:
+        import torch as _t
+        _torch = _t
+    return _torch
+
+
+def device():
+    t = torch()
+    if not t.cuda.is_available():
+        raise FntGpuError("no CUDA device: the FNT kernels have no CPU fallback")
+    return t.device("cuda", t.cuda.current_device())
+
+
+def stream_handle():
+    return vp(torch().cuda.current_stream().cuda_stream)
+
+
+def ptr(t) -> vp:
+    return vp(t.data_ptr()) if t is not None else vp(0)
+
+
+_NP2T = {}
+
+
+def to_device(a: np.ndarray):
+    """Contiguous host array -> device tensor (same dtype)."""
+    t = torch()
+    a = np.ascontiguousarray(a)
+    if not a.flags.writeable:
+        a = a.copy()
+    if a.size == 0:
+        return t.empty(a.shape, dtype=_torch_dtype(a.dtype), device=device())
+    return t.from_numpy(a).to(device(), non_blocking=False)
+
+
+def empty(shape, np_dtype):
+    t = torch()
+    return t.empty(tuple(shape), dtype=_torch_dtype(np.dtype(np_dtype)), device=device())
+
+
+def zeros(shape, np_dtype):
+    t = torch()
+    return t.zeros(tuple(shape), dtype=_torch_dtype(np.dtype(np_dtype)), device=device())
+
+
+def to_host(t) -> np.ndarray:
+    return t.cpu().numpy()
+
+
+def _torch_dtype(dt: np.dtype):
+    t = torch()
+    m = {np.dtype(np.int8): t.int8, np.dtype(np.int16): t.int16, np.dtype(np.int32): t.int32,
+         np.dtype(np.int64): t.int64, np.dtype(np.float64): t.float64,
+         np.dtype(np.complex128): t.complex128, np.dtype(np.uint8): t.uint8,
+         np.dtype(np.float32): t.float32}
+    return m[np.dtype(dt)]
+
+
+def dtype_code(dt) -> int:
+    dt = np.dtype(dt)
+    return {np.dtype(np.int8): I8, np.dtype(np.int16): I16, np.dtype(np.int32): I32,
+            np.dtype(np.int64): I64, np.dtype(np.float64): F64,
+            np.dtype(np.complex128): C128}[dt]
+
+
+def env_forward_mode() -> int:
+    """Default AEQ forward path: FNT (the paper's algorithm) unless overridden."""
+    v = os.environ.get("FNTGPU_AEQ_FORWARD", "fnt").lower()
+    return AEQ_FWD_DIRECT if v == "direct" else AEQ_FWD_FNT

@@ -1,0 +1,319 @@
+"""FNT-AEQ: 4x4 real-valued MIMO radius-directed block equalizer on the B200
+(drop-in for fntdsp/aeq.py).
+
+The stream state (float taps w, 14-bit taps w_int, overlap history, saturation
+and symbol counters) lives in device memory (fntgpu_aeq_state); `process` runs
+the whole block recursion inside one kernel launch (k_aeq.cu: one warp per
+stream, taps in registers across blocks). Host attributes (`w`, `taps`,
+`history`, `saturations`, `symbols_processed`) read the device state on access,
+and assigning them writes it back, so code written against the reference object
+keeps working.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib
+from .cdc import BudgetError
+from .complexity import COUNTER
+from .fixedpoint import QuantSpec, check_overflow, split_taps
+from .fnt import TransformPlan, default_plans
+
+STREAMS = ("XI", "XQ", "YI", "YQ")
+TAP_MAG_MAX = (1 << 14) - 1
+
+
+def qam16_radii() -> np.ndarray:
+    """Ring moduli of unit-energy 16QAM (aeq.py:29-31)."""
+    return np.sqrt(np.array([2.0, 10.0, 18.0]) / 10.0)
+
+
+@dataclass
+class AeqConfig:
+    block_n: int = 32
+    l_taps: int = 16
+    mu: float = 1e-3
+    radii: np.ndarray = field(default_factory=qam16_radii)
+    tap_bits: int = 14
+    group_bits: int = 7
+    sig_spec: QuantSpec = field(default_factory=lambda: QuantSpec(5, 8.0))
+    tap_scale: float = float(1 << 13)
+
+    def __post_init__(self) -> None:
+        if self.l_taps != self.block_n // 2:
+            raise ValueError("l_taps must equal block_n / 2")
+        if self.mu < 0:
+            raise ValueError("mu must be >= 0")
+        self.radii = np.sort(np.asarray(self.radii, dtype=float))
+
+
+def rde_error(y_i: np.ndarray, y_q: np.ndarray, radii: np.ndarray) -> np.ndarray:
+    """R^2 - |y|^2 against the nearest ring (aeq.py:53-58); host helper."""
+    r2 = np.asarray(y_i) ** 2 + np.asarray(y_q) ** 2
+    r = np.sqrt(r2)
+    nearest = radii[np.argmin(np.abs(r[..., None] - radii), axis=-1)]
+    return nearest ** 2 - r2
+
+
+@dataclass
+class RvMimoTaps:
+    """16 real FIR filters (output stream, input stream, lag) (aeq.py:61-81)."""
+
+    w_int: np.ndarray
+    high: np.ndarray = field(init=False)
+    low: np.ndarray = field(init=False)
+
+    def __post_init__(self) -> None:
+        self.resplit()
+
+    def resplit(self) -> None:
+        s = split_taps(self.w_int)
+        self.high, self.low = s.high, s.low
+
+    @classmethod
+    def center_spike(cls, l_taps: int, spike: int) -> "RvMimoTaps":
+        w = np.zeros((4, 4, l_taps), dtype=np.int64)
+        for s in range(4):
+            w[s, s, l_taps // 2] = spike
+        return cls(w)
+
+
+def aeq_params(config: AeqConfig, forward: int | None = None) -> _lib.AeqParams:
+    """The C-ABI parameter block for an AeqConfig."""
+    prm = _lib.AeqParams()
+    prm.sig_scale = float(config.sig_spec.scale)
+    prm.tap_scale = float(config.tap_scale)
+    prm.mu = float(config.mu)
+    radii = np.asarray(config.radii, dtype=float)
+    if not 1 <= radii.size <= 8:
+        raise NotImplementedError("the GPU equalizer supports 1..8 ring radii")
+    for i, r in enumerate(radii):
+        prm.radii[i] = float(r)
+    prm.n_radii = int(radii.size)
+    prm.forward = _lib.env_forward_mode() if forward is None else int(forward)
+    return prm
+
+
+def mu_block_array(n_blocks: int, hop: int, mu_schedule, default_mu: float) -> np.ndarray:
+    """mu of each block: mu_schedule(b * hop), or config.mu (aeq.py:187-188)."""
+    if mu_schedule is None:
+        return np.full(n_blocks, default_mu, dtype=np.float64)
+    out = np.empty(n_blocks, dtype=np.float64)
+    for b in range(n_blocks):
+        m = mu_schedule(b * hop)
+        out[b] = default_mu if m is None else float(m)
+    return out
+
+
+class FntAeq:
+    """Block equalizer state: taps, overlap history, error trace (aeq.py:84-190)."""
+
+    def __init__(self, config: AeqConfig, plan: TransformPlan | None = None,
+                 forward: int | None = None):
+        self.config = config
+        self.plan = plan if plan is not None else default_plans()["aeq32"]
+        if self.plan.n != config.block_n:
+            raise ValueError("plan length does not match block_n")
+        self.budget = check_overflow(np.full(config.l_taps, (1 << config.group_bits) - 1),
+                                     config.sig_spec, self.plan.params)
+        if not self.budget.passed:
+            raise BudgetError(str(self.budget))
+        p = self.plan
+        if not (p.params.t == 4 and p.n == 32 and p.alpha == 2):
+            raise NotImplementedError(
+                "the GPU FNT-AEQ implements the aeq32 plan (F4, alpha=2, N=32) only")
+        self.err_trace: list[float] = []
+        self._tap_spectra = None
+        self._prm = aeq_params(config, forward)
+        self._state = _lib.zeros((_lib.AEQ_STATE_BYTES,), np.uint8)
+        lib = _lib.load()
+        _lib.check(lib.fntgpu_aeq_init(_lib.ptr(self._state), 1, C.byref(self._prm),
+                                       _lib.stream_handle()), "aeq_init")
+
+    # -- device state views -----------------------------------------------------
+
+    def _read(self) -> _lib.AeqState:
+        raw = _lib.to_host(self._state)
+        return _lib.AeqState.from_buffer_copy(raw.tobytes())
+
+    def _write(self, st: _lib.AeqState) -> None:
+        raw = np.frombuffer(bytes(st), dtype=np.uint8).copy()
+        self._state.copy_(_lib.torch().from_numpy(raw).to(self._state.device))
+
+    @property
+    def w(self) -> np.ndarray:
+        return np.array(self._read().w, dtype=np.float64).reshape(4, 4, 16)
+
+    @w.setter
+    def w(self, value) -> None:
+        st = self._read()
+        v = np.ascontiguousarray(np.asarray(value, dtype=np.float64).reshape(256))
+        C.memmove(st.w, v.ctypes.data, v.nbytes)
+        self._write(st)
+
+    @property
+    def taps(self) -> RvMimoTaps:
+        return RvMimoTaps(np.array(self._read().w_int, dtype=np.int64).reshape(4, 4, 16))
+
+    @taps.setter
+    def taps(self, value: RvMimoTaps) -> None:
+        st = self._read()
+        v = np.ascontiguousarray(np.asarray(value.w_int, dtype=np.int32).reshape(256))
+        C.memmove(st.w_int, v.ctypes.data, v.nbytes)
+        self._write(st)
+
+    @property
+    def history(self) -> np.ndarray:
+        return np.array(self._read().hist, dtype=np.int64).reshape(4, 16)
+
+    @history.setter
+    def history(self, value) -> None:
+        st = self._read()
+        v = np.ascontiguousarray(np.asarray(value, dtype=np.int32).reshape(64))
+        C.memmove(st.hist, v.ctypes.data, v.nbytes)
+        self._write(st)
+
+    @property
+    def saturations(self) -> int:
+        return int(self._read().saturations)
+
+    @property
+    def symbols_processed(self) -> int:
+        return int(self._read().symbols)
+
+    # -- forward / update -------------------------------------------------------
+
+    def _launch(self, x: np.ndarray, n_blocks: int, adapt: bool, mu_blocks: np.ndarray | None):
+        hop = self.config.l_taps
+        n = n_blocks * hop
+        lo, hi = (int(x.min()), int(x.max())) if x.size else (0, 0)
+        if max(-lo, hi) > self.plan.params.half:
+            raise ValueError("input exceeds the encodable signed range")
+        if -128 <= lo and hi <= 127:
+            dt, align = np.int8, 16
+        else:
+            dt, align = np.int32, 4
+        ld = -(-n // align) * align
+        host = np.zeros((4, ld), dtype=dt)
+        host[:, :n] = x[:, :n]
+        dx = _lib.to_device(host)
+        dy = _lib.empty((4, n), np.float64)
+        derr = _lib.empty((max(n_blocks, 1),), np.float64) if adapt else None
+        dmu = _lib.to_device(mu_blocks) if (adapt and mu_blocks is not None) else None
+        io = _lib.AeqIO()
+        io.n_streams = 1
+        io.in_mode = _lib.AEQ_IN_PLANAR
+        io.in_dtype = _lib.dtype_code(dt)
+        io.adapt = int(adapt)
+        io.x = dx.data_ptr()
+        io.x_stream_stride = 4 * ld
+        io.x_row_stride = ld
+        io.n_blocks = n_blocks
+        io.mu_blocks = dmu.data_ptr() if dmu is not None else None
+        io.y = dy.data_ptr()
+        io.y_stream_stride = 4 * n
+        io.y_row_stride = n
+        io.err = derr.data_ptr() if derr is not None else None
+        io.err_stream_stride = max(n_blocks, 1)
+        lib = _lib.load()
+        _lib.check(lib.fntgpu_aeq_process(_lib.ptr(self._state), C.byref(self._prm), C.byref(io),
+                                          _lib.stream_handle()), "aeq_process")
+        y = _lib.to_host(dy)
+        if adapt:
+            self.err_trace.extend(_lib.to_host(derr)[:n_blocks].tolist())
+        return y
+
+    def equalize_block(self, x_new: np.ndarray) -> tuple[np.ndarray, np.ndarray]:
+        """4 x hop new samples -> (y float (4, hop), x_block (4, 2 hop)) (aeq.py:118-144)."""
+        hop = self.config.l_taps
+        x_new = np.asarray(x_new, dtype=np.int64)
+        if x_new.shape != (4, hop):
+            raise ValueError(f"expected (4, {hop}) block, got {x_new.shape}")
+        x_block = np.concatenate([self.history, x_new], axis=1)
+        if np.abs(x_block).max() > self.plan.params.half:
+            raise ValueError("input exceeds the encodable signed range")
+        with COUNTER.scope("aeq-fnt"):
+            COUNTER.add(2 * 16 * self.plan.n)  # prod.size (aeq.py:137-138)
+        y = self._launch(x_new, 1, False, None)
+        return y, x_block
+
+    def update_taps(self, x_block: np.ndarray, y: np.ndarray, mu: float | None = None) -> None:
+        """Block-accumulated RDE update, requantize, resplit (aeq.py:148-170)."""
+        cfg = self.config
+        mu = cfg.mu if mu is None else mu
+        xb = np.ascontiguousarray(np.asarray(x_block, dtype=np.int64).reshape(4, 32))
+        yy = np.ascontiguousarray(np.asarray(y, dtype=np.float64).reshape(4, 16))
+        dxb = _lib.to_device(xb)
+        dy = _lib.to_device(yy)
+        derr = _lib.empty((1,), np.float64)
+        lib = _lib.load()
+        _lib.check(lib.fntgpu_aeq_update_taps(_lib.ptr(self._state), C.byref(self._prm),
+                                              _lib.ptr(dxb), _lib.ptr(dy), float(mu),
+                                              _lib.ptr(derr), _lib.stream_handle()),
+                   "aeq_update_taps")
+        self.err_trace.append(float(_lib.to_host(derr)[0]))
+        self._tap_spectra = None
+
+    def process(self, x: np.ndarray, adapt: bool = True, mu_schedule=None) -> np.ndarray:
+        """Stream 4 x n samples through the equalize/update loop (aeq.py:172-190)."""
+        hop = self.config.l_taps
+        x = np.asarray(x, dtype=np.int64)
+        n_blocks = x.shape[1] // hop
+        if n_blocks == 0:
+            return np.zeros((4, 0))
+        if x.shape[0] != 4:
+            raise ValueError(f"expected (4, {hop}) block, got {(x.shape[0], hop)}")
+        with COUNTER.scope("aeq-fnt"):
+            COUNTER.add(2 * 16 * self.plan.n * n_blocks)
+        mu_blocks = mu_block_array(n_blocks, hop, mu_schedule, self.config.mu) if adapt else None
+        return self._launch(x, n_blocks, adapt, mu_blocks)
+
+
+def td_aeq_float(x: np.ndarray, config: AeqConfig, mu_schedule=None,
+                 w0: np.ndarray | None = None) -> tuple[np.ndarray, np.ndarray]:
+    """Per-symbol float 4x4 RDE baseline (aeq.py:193-249).
+
+    Not on the FNT path: the paper's float comparator. Implemented as a plain
+    host loop in float64 (the reference JIT-compiles the same loop with numba),
+    kept for API completeness and the penalty comparison."""
+    x = np.asarray(x, dtype=float)
+    n = x.shape[1]
+    L = config.l_taps
+    if w0 is None:
+        w = np.zeros((4, 4, L))
+        for s in range(4):
+            w[s, s, L // 2] = 1.0
+    else:
+        w = w0.astype(float).copy()
+    mu_arr = (np.full(n, config.mu) if mu_schedule is None
+              else np.array([mu_schedule(i) for i in range(n)]))
+    radii = np.asarray(config.radii, dtype=float)
+    y = np.zeros((4, n))
+    with COUNTER.scope("aeq-td"):
+        for m in range(L - 1, n):
+            win = x[:, m - L + 1:m + 1][:, ::-1]
+            for s2 in range(4):
+                acc = 0.0
+                for s1 in range(4):
+                    for k in range(L):
+                        acc += w[s2, s1, k] * win[s1, k]
+                y[s2, m] = acc
+            for pol in range(2):
+                yi, yq = y[2 * pol, m], y[2 * pol + 1, m]
+                r = np.sqrt(yi * yi + yq * yq)
+                best = radii[0]
+                for ri in range(1, radii.size):
+                    if abs(radii[ri] - r) < abs(best - r):
+                        best = radii[ri]
+                e = best * best - (yi * yi + yq * yq)
+                for ii in range(2):
+                    s2 = 2 * pol + ii
+                    g = mu_arr[m] * e * y[s2, m]
+                    if g != 0.0:
+                        w[s2] += g * win
+        COUNTER.add(16 * L * n)
+    return y, w

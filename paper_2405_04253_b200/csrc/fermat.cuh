@@ -1,0 +1,194 @@
+// fermat.cuh -- Fermat-ring arithmetic for the sm_100a FNT kernels.
+//
+// Reference semantics: fntdsp/fermat.py:56-117 (reduce, mul_pow2, sqrt2) and the
+// vectorised residue arithmetic of fntdsp/fnt.py:86-161.
+//
+// B200 design: F4 = 2^16 + 1 divides M = 2^32 - 1 = (2^16 - 1)(2^16 + 1). Every
+// transform / product / sum is therefore computed in the ring Z/M on full 32-bit
+// words and reduced mod F4 once, at the end. In Z/M:
+//   * a + b  = 32-bit add + end-around carry          (IADD3 + IADD3.X / IMAD.X)
+//   * a - b  = 32-bit sub - end-around borrow
+//   * a * 2^j = 32-bit rotate left by j               (one SHF.L.W)
+//   * -a     = ~a                                      (free inside LOP3 / swaps)
+// so a radix-2 butterfly with a power-of-two twiddle is 5 integer instructions
+// with no data-dependent reduction, and the sqrt(2) twiddles of the 64-point plan
+// (sqrt2 = 2^12 - 2^4, fermat.py:111-117) are two rotates and one subtraction.
+// The final fold x mod F4 = lo16 - hi16 (fermat.py:56-66) is one SHF + one IMAD.
+#pragma once
+#include <cstdint>
+
+namespace fntgpu {
+
+constexpr uint32_t F4 = 65537u;
+constexpr int32_t F4_HALF = 32768;
+
+// a + b (mod 2^32 - 1)
+__device__ __forceinline__ uint32_t m_add(uint32_t a, uint32_t b) {
+  uint32_t r;
+  asm("{\n\t.reg .u32 t;\n\tadd.cc.u32 t, %1, %2;\n\taddc.u32 %0, t, 0;\n\t}"
+      : "=r"(r) : "r"(a), "r"(b));
+  return r;
+}
+
+// a - b (mod 2^32 - 1)
+__device__ __forceinline__ uint32_t m_sub(uint32_t a, uint32_t b) {
+  uint32_t r;
+  asm("{\n\t.reg .u32 t;\n\tsub.cc.u32 t, %1, %2;\n\tsubc.u32 %0, t, 0;\n\t}"
+      : "=r"(r) : "r"(a), "r"(b));
+  return r;
+}
+
+// a * 2^j (mod 2^32 - 1), j in [0, 32)
+__device__ __forceinline__ uint32_t m_rot(uint32_t a, int j) {
+  return j == 0 ? a : __funnelshift_l(a, a, j);
+}
+
+// a * b (mod 2^32 - 1): 64-bit product folded with 2^32 == 1.
+__device__ __forceinline__ uint32_t m_mul(uint32_t a, uint32_t b) {
+  return m_add(a * b, __umulhi(a, b));
+}
+
+// Canonical residue in [0, F4) of a word of Z/M.
+__device__ __forceinline__ uint32_t f4_canon(uint32_t x) {
+  int32_t r = (int32_t)(x - (x >> 16) * F4);  // lo16 - hi16 in [-65535, 65535]
+  return (uint32_t)(r < 0 ? r + (int32_t)F4 : r);
+}
+
+// Signed residue in [-32768, 32768]: decode_signed(canon(x)) (fermat.py:117-118, 131-133).
+__device__ __forceinline__ int32_t f4_signed(uint32_t x) {
+  int32_t r = (int32_t)(x - (x >> 16) * F4);
+  r = r > F4_HALF ? r - (int32_t)F4 : r;
+  r = r < -F4_HALF ? r + (int32_t)F4 : r;
+  return r;
+}
+
+// Encode a signed integer |v| < 2^31 - F4*256 into Z/M with the right residue mod F4.
+// Adding a multiple of F4 keeps the residue (the mod-M class does not matter:
+// only the final mod-F4 reduction is observed).
+constexpr uint32_t F4_BIAS = 65537u * 256u;  // > 32768 * 257, keeps v + bias >= 0
+__device__ __forceinline__ uint32_t f4_enc_small(int32_t v) { return (uint32_t)(v + (int32_t)F4_BIAS); }
+
+// Encode an arbitrary int64 into Z/M (fnt.py accepts any int64 and reduces it,
+// probe t17): v = hi * 2^32 + lo == hi + lo (mod 2^32 - 1), with a negative hi
+// represented as M + hi. No 64-bit division.
+__device__ __forceinline__ uint32_t f4_enc64(int64_t v) {
+  const uint32_t lo = (uint32_t)(uint64_t)v;
+  const int32_t hi = (int32_t)((uint64_t)v >> 32);
+  const uint32_t h = (uint32_t)hi - (hi < 0 ? 1u : 0u);
+  return m_add(lo, h);
+}
+
+// ---------------------------------------------------------------------------
+// Twiddles of the two shift-add plans, as compile-time-resolved operations.
+//   kind RADIX2 : alpha = 2, N <= 32         alpha^e = 2^e
+//   kind SQRT2  : alpha = 2^12 - 2^4 (4080), N = 64
+//                 alpha^(2h) = 2^h, alpha^(2h+1) = 2^h * (2^12 - 2^4)
+// The result is returned as (value, negate) where negate means the caller must
+// use -value (absorbed by swapping the butterfly's add and subtract): a rotate
+// by r >= 16 equals -(rotate by r - 16) modulo F4.
+enum TwKind { RADIX2 = 0, SQRT2 = 1 };
+
+struct Tw {
+  uint32_t v;
+  bool neg;
+};
+
+template <int KIND>
+__device__ __forceinline__ Tw twiddle(uint32_t a, int e /* exponent of alpha, >= 0 */) {
+  if (KIND == RADIX2) {
+    int r = e & 31;
+    if (r >= 16) return {m_rot(a, r - 16), true};
+    return {m_rot(a, r), false};
+  } else {
+    e &= 63;
+    if ((e & 1) == 0) {
+      int r = (e >> 1) & 31;
+      if (r >= 16) return {m_rot(a, r - 16), true};
+      return {m_rot(a, r), false};
+    }
+    int h = e >> 1;
+    int r1 = (h + 12) & 31, r2 = (h + 4) & 31;
+    bool neg = false;
+    // 2^r1 - 2^r2; fold rotates >= 16 into signs, preferring one overall negate.
+    if (r1 >= 16 && r2 >= 16) { r1 -= 16; r2 -= 16; neg = true; }
+    if (r1 >= 16) {  // -(2^(r1-16)) - 2^r2 = -(2^(r1-16) + 2^r2)
+      return {m_add(m_rot(a, r1 - 16), m_rot(a, r2)), !neg};
+    }
+    if (r2 >= 16) {  // 2^r1 + 2^(r2-16)
+      return {m_add(m_rot(a, r1), m_rot(a, r2 - 16)), neg};
+    }
+    return {m_sub(m_rot(a, r1), m_rot(a, r2)), neg};
+  }
+}
+
+// Radix-2 DIT butterfly (fnt.py:94-102): (u, v) -> (u + tw*v, u - tw*v).
+template <int KIND>
+__device__ __forceinline__ void bfly(uint32_t& u, uint32_t& v, int e) {
+  Tw t = twiddle<KIND>(v, e);
+  uint32_t s = t.neg ? m_sub(u, t.v) : m_add(u, t.v);
+  uint32_t d = t.neg ? m_add(u, t.v) : m_sub(u, t.v);
+  u = s;
+  v = d;
+}
+
+// Only the difference output u - tw*v (pruned last stage of an inverse transform).
+template <int KIND>
+__device__ __forceinline__ uint32_t bfly_hi(uint32_t u, uint32_t v, int e) {
+  Tw t = twiddle<KIND>(v, e);
+  return t.neg ? m_add(u, t.v) : m_sub(u, t.v);
+}
+
+__host__ __device__ constexpr int ilog2(int n) { return n <= 1 ? 0 : 1 + ilog2(n >> 1); }
+
+__host__ __device__ constexpr int bitrev(int i, int lg) {
+  int r = 0;
+  for (int b = 0; b < lg; ++b) { r = (r << 1) | ((i >> b) & 1); }
+  return r;
+}
+
+// natural order -> bit-reversed order (register renaming only; free after unrolling)
+template <int N>
+__device__ __forceinline__ void to_bitrev(uint32_t (&a)[N]) {
+  constexpr int LG = ilog2(N);
+  uint32_t t[N];
+#pragma unroll
+  for (int i = 0; i < N; ++i) t[bitrev(i, LG)] = a[i];
+#pragma unroll
+  for (int i = 0; i < N; ++i) a[i] = t[i];
+}
+
+// In-register radix-2 DIT transform over a[N] held in BIT-REVERSED order on entry,
+// natural order on exit (fnt.py:86-103). INV selects alpha^-1 twiddles (the N^-1
+// scale is left to the caller, who folds it into a rotate). ZERO_TOP declares that
+// inputs with natural index >= N/2 are zero (first stage becomes a copy).
+// PRUNE_LO skips the low-half outputs of the last stage (only a[N/2..N) valid).
+// Stages are expanded by template recursion so every register index is a
+// compile-time constant (no local-memory arrays).
+template <int N, int KIND, bool INV, bool ZERO_TOP, bool PRUNE_LO, int S>
+__device__ __forceinline__ void fnt_stage(uint32_t (&a)[N]) {
+  constexpr int LG = ilog2(N);
+  constexpr int half = 1 << S;
+  constexpr int step = N >> (S + 1);
+#pragma unroll
+  for (int q = 0; q < N / 2; ++q) {
+    const int g = (q / half) * 2 * half;
+    const int j = q % half;
+    int e = j * step;
+    if (INV) e = (N - e) % N;
+    if (ZERO_TOP && S == 0) {
+      a[g + j + half] = a[g + j];
+    } else if (PRUNE_LO && S == LG - 1) {
+      a[g + j + half] = bfly_hi<KIND>(a[g + j], a[g + j + half], e);
+    } else {
+      bfly<KIND>(a[g + j], a[g + j + half], e);
+    }
+  }
+  if constexpr (S + 1 < LG) fnt_stage<N, KIND, INV, ZERO_TOP, PRUNE_LO, S + 1>(a);
+}
+
+template <int N, int KIND, bool INV, bool ZERO_TOP = false, bool PRUNE_LO = false>
+__device__ __forceinline__ void fnt_dit(uint32_t (&a)[N]) {
+  fnt_stage<N, KIND, INV, ZERO_TOP, PRUNE_LO, 0>(a);
+}
+
+}  // namespace fntgpu

@@ -1,0 +1,478 @@
+// k_aeq.cu -- FNT-AEQ: 4x4 real-valued MIMO radius-directed block equalizer.
+//
+// Reference: fntdsp/aeq.py:53-58 (rde_error), 61-81 (RvMimoTaps, split_taps),
+// 84-190 (FntAeq: __init__, _spectra, equalize_block, update_taps, process).
+//
+// One warp owns one stream for the whole call (the block recursion through the
+// taps is strictly sequential, aeq.py:182-189). Lane = 8 s + 2 t + g with
+//   s = output stream, t = input stream, g = tap group (hi/lo) in the forward
+//   path and tap half (k in [8g, 8g+8)) in the update.
+// Taps (float w and 14-bit w_int), the overlap history and the per-lane FNT
+// arrays live in registers across all blocks; lane exchanges go through a small
+// per-warp shared-memory scratch with __syncwarp.
+//
+// Forward path, FNTGPU_AEQ_FWD_FNT (aeq.py:118-144): lane (s,t,g) transforms the
+//   32-sample block of input stream t (FNT-32, alpha = 2, rotates in Z/(2^32-1)),
+//   transforms its 16-tap group padded to 32 (first DIT stage free), multiplies
+//   pointwise (the 32 general products of that filter group), runs the inverse
+//   pruned to outputs 16..31 and decodes -- the reference's residue convolution
+//   per (group, s, t); recombine 128*hi + lo and sum over t, g.
+// Forward path, FNTGPU_AEQ_FWD_DIRECT: the same integer per-group sums computed
+//   as a time-domain FIR (each group sum reduced mod F4 and decoded exactly as the
+//   residue path, so the bits are identical for every input the reference accepts).
+// Update (aeq.py:148-170): float64 with explicit __dmul_rn/__dadd_rn (never
+//   contracted into FMA), IEEE division and sqrt, numpy's einsum reduction order
+//   over m (two lanes of even/odd m, unrolled by 4) and numpy's
+//   pairwise order for the err_trace mean.
+#include "fermat.cuh"
+#include "internal.h"
+
+namespace fntgpu {
+
+constexpr int AEQ_L = 16;            // taps per filter = hop (aeq.py:45)
+constexpr int AEQ_N = 32;            // block length
+constexpr int AEQ_WARPS = 4;         // streams per CTA
+constexpr int AEQ_TAP_MAX = 16383;   // TAP_MAG_MAX (aeq.py:26)
+constexpr int XF_LUT = 127;          // x / sig_scale table for |x| <= 127
+
+struct AeqScratch {
+  int32_t part[32][32];     // per-lane partial sums (direct: 16 hi + 16 lo; fnt: 16)
+  double ey[4][AEQ_L];      // e * y per output stream
+  double xf[4][2][AEQ_L];   // x / sig_scale ring: [t][block parity][j]
+  double err[32];           // |e| values for the err_trace mean
+};
+
+struct AeqArgs {
+  fntgpu_aeq_params prm;
+  fntgpu_aeq_io io;
+  double R2[8];             // radii[i] * radii[i] (nearest ** 2, aeq.py:58)
+  double D;                 // sig_scale * tap_scale (aeq.py:142)
+};
+
+__device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double dsub(double a, double b) { return __dsub_rn(a, b); }
+
+__device__ __forceinline__ int32_t sext8(uint32_t w, int k) {
+  return (int32_t)(w << (24 - 8 * k)) >> 24;
+}
+
+// split_taps (fixedpoint.py:111-121): sign * (|w| >> 7) or sign * (|w| & 127)
+__device__ __forceinline__ int32_t tap_group(int32_t w, int g) {
+  const int32_t m = w < 0 ? -w : w;
+  const int32_t v = g == 0 ? (m >> 7) : (m & 127);
+  return w < 0 ? -v : v;
+}
+
+// rde_error (aeq.py:53-58) for one output pair (y_I, y_Q)
+__device__ __forceinline__ double rde(double yi, double yq, const AeqArgs& A) {
+  const double r2 = dadd(dmul(yi, yi), dmul(yq, yq));
+  const double r = __dsqrt_rn(r2);
+  int best = 0;
+  double bd = fabs(dsub(r, A.prm.radii[0]));
+  for (int i = 1; i < A.prm.n_radii; ++i) {
+    const double d = fabs(dsub(r, A.prm.radii[i]));
+    if (d < bd) { bd = d; best = i; }  // np.argmin: first minimum
+  }
+  return dsub(A.R2[best], r2);
+}
+
+// einsum("sm,tmk->stk") inner reduction over m in numpy's SSE2 order.
+__device__ __forceinline__ double einsum_m(const double (&P)[AEQ_L]) {
+  double c0 = P[6], c1 = P[7];
+  c0 = dadd(P[4], c0);  c1 = dadd(P[5], c1);
+  c0 = dadd(P[2], c0);  c1 = dadd(P[3], c1);
+  c0 = dadd(P[0], c0);  c1 = dadd(P[1], c1);
+  c0 = dadd(P[14], c0); c1 = dadd(P[15], c1);
+  c0 = dadd(P[12], c0); c1 = dadd(P[13], c1);
+  c0 = dadd(P[10], c0); c1 = dadd(P[11], c1);
+  c0 = dadd(P[8], c0);  c1 = dadd(P[9], c1);
+  return dadd(c0, c1);
+}
+
+// x / sig_scale exactly as numpy's true_divide (IEEE), via a table for |x| <= 127.
+__device__ __forceinline__ double xf_of(int32_t x, const double* lut, double sig) {
+  return (x >= -XF_LUT && x <= XF_LUT) ? lut[x + XF_LUT] : __ddiv_rn((double)x, sig);
+}
+
+// Lane-level block update (aeq.py:148-170) shared by process and update_taps.
+// Inputs: this lane's y0,y1 (= y[s][m0], y[s][m0+1]) and the scratch holding xf[t]
+// for the block (slot layout given by cur/prev). Returns |e| contributions via
+// scratch and updates the lane's 8 taps.
+struct LaneTaps {
+  double w[8];
+  int32_t wi[8];
+  long long sat;
+};
+
+// Exchange the e values, compute err mean (written by lane 0 to *err_out when
+// non-null) and, when mu != 0, the float update of this lane's 8 taps.
+__device__ __forceinline__ void lane_update(const AeqArgs& A, AeqScratch& S, int lane, int m0,
+                                            double y0, double y1, int cur, double mu,
+                                            LaneTaps& T, double* err_out) {
+  const int s = lane >> 3, t = (lane >> 1) & 3, g = lane & 1;
+  // rde: the I lane (s even) takes m0, the Q lane (s odd) takes m0 + 1
+  const double send = (s & 1) ? y0 : y1;
+  const double recv = __shfl_xor_sync(0xffffffffu, send, 8);
+  double e_mine = (s & 1) ? rde(recv, y1, A) : rde(y0, recv, A);
+  const double e_other = __shfl_xor_sync(0xffffffffu, e_mine, 8);
+  const double e0 = (s & 1) ? e_other : e_mine;  // e[p][m0]
+  const double e1 = (s & 1) ? e_mine : e_other;  // e[p][m0 + 1]
+  // err_trace: mean(|e|) over (2 pols x 16) in numpy pairwise order
+  if ((s & 1) == 0) {
+    const int p = s >> 1;
+    S.err[p * 16 + m0] = fabs(e0);
+    S.err[p * 16 + m0 + 1] = fabs(e1);
+  }
+  // ey for this lane's two outputs
+  S.ey[s][m0] = dmul(e0, y0);
+  S.ey[s][m0 + 1] = dmul(e1, y1);
+  __syncwarp();
+  if (err_out != nullptr) {
+    double r = 0.0;
+    if (lane < 8) {
+      r = dadd(dadd(dadd(S.err[lane], S.err[lane + 8]), S.err[lane + 16]), S.err[lane + 24]);
+    }
+    r = dadd(r, __shfl_xor_sync(0xffffffffu, r, 1));
+    r = dadd(r, __shfl_xor_sync(0xffffffffu, r, 2));
+    r = dadd(r, __shfl_xor_sync(0xffffffffu, r, 4));
+    if (lane == 0) *err_out = dmul(r, 1.0 / 32.0);
+  }
+  if (mu != 0.0) {
+    // gradient for taps k in [8g, 8g+8): sum_m ey[s][m] * xf[t][16 + m - k]
+    double ey[AEQ_L];
+#pragma unroll
+    for (int m = 0; m < AEQ_L; ++m) ey[m] = S.ey[s][m];
+    double xf[23];  // xf[t][j] for j = 9 - 8g ... 31 - 8g
+    const int prev = cur ^ 1;
+#pragma unroll
+    for (int q = 0; q < 23; ++q) {
+      const int j = q + 9 - 8 * g;  // 1..31
+      xf[q] = j < AEQ_L ? S.xf[t][prev][j] : S.xf[t][cur][j - AEQ_L];
+    }
+#pragma unroll
+    for (int kk = 0; kk < 8; ++kk) {
+      // k = 8g + kk ; j = 16 + m - k = 16 + m - 8g - kk ; q = j - (9 - 8g) = 7 + m - kk
+      double P[AEQ_L];
+#pragma unroll
+      for (int m = 0; m < AEQ_L; ++m) P[m] = dmul(ey[m], xf[7 + m - kk]);
+      const double gr = einsum_m(P);
+      T.w[kk] = dadd(T.w[kk], dmul(mu, gr));
+      long long wi = __double2ll_rn(dmul(T.w[kk], A.prm.tap_scale));  // np.rint -> int64
+      const long long aw = wi < 0 ? -wi : wi;
+      if (aw > AEQ_TAP_MAX) {
+        T.sat++;
+        wi = wi < 0 ? -AEQ_TAP_MAX : AEQ_TAP_MAX;
+      }
+      T.wi[kk] = (int32_t)wi;
+    }
+  }
+  __syncwarp();
+}
+
+// Forward path for one block: returns y_int[s][m0], y_int[s][m0+1] in yi0, yi1.
+// xb holds this lane's input stream t block (32 ints: history | new).
+template <int FWD>
+__device__ __forceinline__ void lane_forward(AeqScratch& S, int lane, const int32_t (&xb)[AEQ_N],
+                                             const LaneTaps& T, int m0, int32_t& yi0,
+                                             int32_t& yi1) {
+  const int s = lane >> 3, g = lane & 1;
+  if (FWD == FNTGPU_AEQ_FWD_FNT) {
+    // all 16 taps of filter (s, t): own 8 + partner's 8 (lane ^ 1 holds the other half)
+    int32_t taps[AEQ_L];
+#pragma unroll
+    for (int kk = 0; kk < 8; ++kk) {
+      const int32_t other = __shfl_xor_sync(0xffffffffu, T.wi[kk], 1);
+      taps[kk] = g == 0 ? T.wi[kk] : other;
+      taps[8 + kk] = g == 0 ? other : T.wi[kk];
+    }
+    uint32_t X[AEQ_N], W[AEQ_N];
+#pragma unroll
+    for (int i = 0; i < AEQ_N; ++i) X[bitrev(i, 5)] = f4_enc_small(xb[i]);
+#pragma unroll
+    for (int k = 0; k < AEQ_N; ++k)
+      W[bitrev(k, 5)] = k < AEQ_L ? f4_enc_small(tap_group(taps[k], g)) : 0u;
+    fnt_dit<AEQ_N, RADIX2, false>(X);
+    fnt_dit<AEQ_N, RADIX2, false, true>(W);  // taps zero-padded: first stage is a copy
+#pragma unroll
+    for (int k = 0; k < AEQ_N; ++k) X[k] = m_mul(X[k], W[k]);  // 32 general products
+    to_bitrev<AEQ_N>(X);
+    fnt_dit<AEQ_N, RADIX2, true, false, true>(X);  // outputs 16..31 only
+#pragma unroll
+    for (int m = 0; m < AEQ_L; ++m) {
+      const int32_t c = f4_signed(m_rot(X[AEQ_L + m], 27));  // * N^-1 = 2^-5
+      S.part[lane][m] = g == 0 ? c * 128 : c;                 // recombine (fixedpoint.py:139-143)
+    }
+    __syncwarp();
+    int32_t a0 = 0, a1 = 0;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      a0 += S.part[s * 8 + q][m0];
+      a1 += S.part[s * 8 + q][m0 + 1];
+    }
+    yi0 = a0;
+    yi1 = a1;
+  } else {
+    // time-domain per-group partial sums over this lane's 8 taps k = 8g + kk
+    int32_t hi[AEQ_L], lo[AEQ_L];
+#pragma unroll
+    for (int m = 0; m < AEQ_L; ++m) { hi[m] = 0; lo[m] = 0; }
+#pragma unroll
+    for (int kk = 0; kk < 8; ++kk) {
+      const int32_t th = tap_group(T.wi[kk], 0), tl = tap_group(T.wi[kk], 1);
+#pragma unroll
+      for (int m = 0; m < AEQ_L; ++m) {
+        // x index 16 + m - k, k = 8g + kk  (runtime g: select between two windows)
+        const int32_t xv = g == 0 ? xb[AEQ_L + m - kk] : xb[AEQ_L + m - 8 - kk];
+        hi[m] += th * xv;
+        lo[m] += tl * xv;
+      }
+    }
+#pragma unroll
+    for (int m = 0; m < AEQ_L; ++m) { S.part[lane][m] = hi[m]; S.part[lane][AEQ_L + m] = lo[m]; }
+    __syncwarp();
+    int32_t a0 = 0, a1 = 0;
+#pragma unroll
+    for (int tt = 0; tt < 4; ++tt) {
+      const int l0 = s * 8 + tt * 2;
+#pragma unroll
+      for (int r = 0; r < 2; ++r) {
+        const int m = m0 + r;
+        const int32_t sh = S.part[l0][m] + S.part[l0 + 1][m];
+        const int32_t sl = S.part[l0][AEQ_L + m] + S.part[l0 + 1][AEQ_L + m];
+        // each group convolution is a residue mod F4, decoded (aeq.py:139-140)
+        const int32_t v = 128 * f4_signed((uint32_t)(sh + (int32_t)(F4 * 1024u))) +
+                          f4_signed((uint32_t)(sl + (int32_t)(F4 * 1024u)));
+        if (r == 0) a0 += v; else a1 += v;
+      }
+    }
+    yi0 = a0;
+    yi1 = a1;
+  }
+  __syncwarp();
+}
+
+// -------------------------------------------------------------------------------------
+// process (aeq.py:172-190) for one stream per warp
+
+template <int FWD, int IN_MODE, typename TIN>
+__global__ void __launch_bounds__(AEQ_WARPS * 32) k_aeq_process(fntgpu_aeq_state* __restrict__ st,
+                                                                 const __grid_constant__ AeqArgs A) {
+  __shared__ AeqScratch scratch[AEQ_WARPS];
+  __shared__ double lut[2 * XF_LUT + 1];
+  for (int i = threadIdx.x; i < 2 * XF_LUT + 1; i += blockDim.x)
+    lut[i] = __ddiv_rn((double)(i - XF_LUT), A.prm.sig_scale);
+  __syncthreads();
+
+  const fntgpu_aeq_io& io = A.io;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t S_idx = (int64_t)blockIdx.x * AEQ_WARPS + warp;
+  if (S_idx >= io.n_streams) return;
+  AeqScratch& S = scratch[warp];
+  fntgpu_aeq_state& state = st[S_idx];
+
+  const int s = lane >> 3, t = (lane >> 1) & 3, g = lane & 1;
+  const int j8 = lane & 7;  // m0 = 8*b0 + 4*b1 + 2*b2 with (b2 b1 b0) = lane bits 2,1,0
+  const int m0 = 8 * (j8 & 1) + 4 * ((j8 >> 1) & 1) + 2 * ((j8 >> 2) & 1);
+
+  LaneTaps T;
+#pragma unroll
+  for (int kk = 0; kk < 8; ++kk) {
+    T.w[kk] = state.w[s][t][8 * g + kk];
+    T.wi[kk] = state.w_int[s][t][8 * g + kk];
+  }
+  T.sat = 0;
+  int32_t xb[AEQ_N];
+#pragma unroll
+  for (int i = 0; i < AEQ_L; ++i) xb[AEQ_L + i] = state.hist[t][i];
+  // xf ring: slot 1 holds the history (block -1), slot 0 receives block 0
+  if (s == 0 && g == 0) {
+#pragma unroll
+    for (int i = 0; i < AEQ_L; ++i) S.xf[t][1][i] = xf_of(xb[AEQ_L + i], lut, A.prm.sig_scale);
+  }
+  __syncwarp();
+
+  // input row pointer for this lane's stream t
+  const TIN* xrow = nullptr;
+  int phase = 0;
+  if (IN_MODE == FNTGPU_AEQ_IN_PLANAR) {
+    xrow = reinterpret_cast<const TIN*>(io.x) + S_idx * io.x_stream_stride + t * io.x_row_stride;
+  } else {
+    const int8_t* plane = (t & 1) ? io.qi : io.qr;
+    xrow = reinterpret_cast<const TIN*>(plane + (2 * S_idx + (t >> 1)) * io.q_stride);
+    phase = io.phase[S_idx];
+  }
+
+  auto load_new = [&](int64_t b, int32_t (&v)[AEQ_L]) {
+    if (IN_MODE == FNTGPU_AEQ_IN_PLANAR) {
+      if (sizeof(TIN) == 1) {
+        const uint4 w = *reinterpret_cast<const uint4*>(xrow + b * AEQ_L);
+        const uint32_t ww[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+        for (int i = 0; i < AEQ_L; ++i) v[i] = sext8(ww[i >> 2], i & 3);
+      } else {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int4 w = *reinterpret_cast<const int4*>(xrow + b * AEQ_L + 4 * q);
+          v[4 * q] = w.x; v[4 * q + 1] = w.y; v[4 * q + 2] = w.z; v[4 * q + 3] = w.w;
+        }
+      }
+    } else {
+      const uint4 w0 = *reinterpret_cast<const uint4*>(xrow + b * 2 * AEQ_L);
+      const uint4 w1 = *reinterpret_cast<const uint4*>(xrow + b * 2 * AEQ_L + 16);
+      const uint32_t ww[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
+#pragma unroll
+      for (int i = 0; i < AEQ_L; ++i) {
+        const int byte = 2 * i;  // + phase
+        v[i] = phase ? sext8(ww[(byte + 1) >> 2], (byte + 1) & 3) : sext8(ww[byte >> 2], byte & 3);
+      }
+    }
+  };
+
+  const double D = A.D;
+  int32_t nxt[AEQ_L];
+  if (io.n_blocks > 0) load_new(0, nxt);
+  for (int64_t b = 0; b < io.n_blocks; ++b) {
+    // shift: x_block = [history | new]
+#pragma unroll
+    for (int i = 0; i < AEQ_L; ++i) { xb[i] = xb[AEQ_L + i]; xb[AEQ_L + i] = nxt[i]; }
+    if (b + 1 < io.n_blocks) load_new(b + 1, nxt);  // prefetch the next block
+    const int cur = (int)(b & 1);
+    if (io.adapt && s == 0 && g == 0) {
+      // x_block / sig_scale for the new half of stream t (aeq.py:154); the history
+      // half was converted one block earlier and sits in the other ring slot
+#pragma unroll
+      for (int i = 0; i < AEQ_L; ++i) S.xf[t][cur][i] = xf_of(xb[AEQ_L + i], lut, A.prm.sig_scale);
+    }
+    int32_t yi0, yi1;
+    lane_forward<FWD>(S, lane, xb, T, m0, yi0, yi1);
+    const double y0 = __ddiv_rn((double)yi0, D);  // y_int / (sig_scale * tap_scale)
+    const double y1 = __ddiv_rn((double)yi1, D);
+    double2* yrow = reinterpret_cast<double2*>(io.y + S_idx * io.y_stream_stride + s * io.y_row_stride + b * AEQ_L + m0);
+    *yrow = make_double2(y0, y1);
+    if (io.adapt) {
+      const double mu = io.mu_blocks ? io.mu_blocks[b] : A.prm.mu;
+      double* err_out = io.err ? io.err + S_idx * io.err_stream_stride + b : nullptr;
+      lane_update(A, S, lane, m0, y0, y1, cur, mu, T, err_out);
+    }
+  }
+
+  // write back the stream state
+#pragma unroll
+  for (int kk = 0; kk < 8; ++kk) {
+    state.w[s][t][8 * g + kk] = T.w[kk];
+    state.w_int[s][t][8 * g + kk] = T.wi[kk];
+  }
+  if (s == 0 && g == 0) {
+#pragma unroll
+    for (int i = 0; i < AEQ_L; ++i) state.hist[t][i] = xb[AEQ_L + i];
+  }
+  long long sat = T.sat;
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) sat += __shfl_xor_sync(0xffffffffu, sat, off);
+  if (lane == 0) {
+    state.saturations += sat;
+    state.symbols += io.n_blocks * AEQ_L;
+    if (io.adapt) state.n_err += io.n_blocks;
+  }
+}
+
+// update_taps with caller-given x_block (4, 32) and y (4, 16) (aeq.py:148-170)
+__global__ void k_aeq_update_once(fntgpu_aeq_state* st, const __grid_constant__ AeqArgs A,
+                                  const int64_t* xblk, const double* y, double mu, double* err) {
+  __shared__ AeqScratch S;
+  __shared__ double lut[2 * XF_LUT + 1];
+  for (int i = threadIdx.x; i < 2 * XF_LUT + 1; i += blockDim.x)
+    lut[i] = __ddiv_rn((double)(i - XF_LUT), A.prm.sig_scale);
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const int s = lane >> 3, t = (lane >> 1) & 3, g = lane & 1;
+  const int j8 = lane & 7;
+  const int m0 = 8 * (j8 & 1) + 4 * ((j8 >> 1) & 1) + 2 * ((j8 >> 2) & 1);
+  LaneTaps T;
+#pragma unroll
+  for (int kk = 0; kk < 8; ++kk) { T.w[kk] = st->w[s][t][8 * g + kk]; T.wi[kk] = st->w_int[s][t][8 * g + kk]; }
+  T.sat = 0;
+  if (s == 0 && g == 0) {
+    for (int i = 0; i < AEQ_L; ++i) {
+      // x_block may hold any int64 the reference accepted; divide exactly
+      S.xf[t][1][i] = __ddiv_rn((double)xblk[t * AEQ_N + i], A.prm.sig_scale);
+      S.xf[t][0][i] = __ddiv_rn((double)xblk[t * AEQ_N + AEQ_L + i], A.prm.sig_scale);
+    }
+  }
+  __syncwarp();
+  const double y0 = y[s * AEQ_L + m0], y1 = y[s * AEQ_L + m0 + 1];
+  lane_update(A, S, lane, m0, y0, y1, 0, mu, T, err);
+#pragma unroll
+  for (int kk = 0; kk < 8; ++kk) { st->w[s][t][8 * g + kk] = T.w[kk]; st->w_int[s][t][8 * g + kk] = T.wi[kk]; }
+  long long sat = T.sat;
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) sat += __shfl_xor_sync(0xffffffffu, sat, off);
+  if (lane == 0) { st->saturations += sat; st->n_err += 1; }
+}
+
+__global__ void k_aeq_init(fntgpu_aeq_state* st, int n_streams, double tap_scale, int32_t spike) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t total = (int64_t)n_streams * 256;
+  if (i >= total) return;
+  fntgpu_aeq_state& S = st[i / 256];
+  const int r = (int)(i % 256);
+  const int s = r >> 6, t = (r >> 4) & 3, k = r & 15;
+  const bool on = (s == t) && (k == AEQ_L / 2);
+  S.w_int[s][t][k] = on ? spike : 0;
+  S.w[s][t][k] = on ? __ddiv_rn((double)spike, tap_scale) : 0.0;  // w_int / tap_scale (aeq.py:99)
+  if (r < 64) S.hist[r >> 4][r & 15] = 0;
+  if (r == 0) { S.saturations = 0; S.symbols = 0; S.n_err = 0; S.reserved = 0; }
+}
+
+static AeqArgs make_args(const fntgpu_aeq_params& prm, const fntgpu_aeq_io* io) {
+  AeqArgs A;
+  A.prm = prm;
+  if (io) A.io = *io;
+  for (int i = 0; i < 8; ++i) A.R2[i] = prm.radii[i] * prm.radii[i];
+  A.D = prm.sig_scale * prm.tap_scale;
+  return A;
+}
+
+cudaError_t launch_aeq_init(fntgpu_aeq_state* st, int n_streams, const fntgpu_aeq_params& prm,
+                            cudaStream_t s) {
+  if (n_streams <= 0) return cudaSuccess;
+  // int(round(tap_scale)) with Python's round-half-even (aeq.py:97)
+  const int32_t spike = (int32_t)nearbyint(prm.tap_scale);
+  const int64_t total = (int64_t)n_streams * 256;
+  k_aeq_init<<<(unsigned)((total + 255) / 256), 256, 0, s>>>(st, n_streams, prm.tap_scale, spike);
+  return cudaGetLastError();
+}
+
+template <int FWD>
+static cudaError_t launch_fwd(fntgpu_aeq_state* st, const AeqArgs& A, cudaStream_t s) {
+  const unsigned grid = (unsigned)((A.io.n_streams + AEQ_WARPS - 1) / AEQ_WARPS);
+  if (A.io.in_mode == FNTGPU_AEQ_IN_DECIM) {
+    k_aeq_process<FWD, FNTGPU_AEQ_IN_DECIM, int8_t><<<grid, AEQ_WARPS * 32, 0, s>>>(st, A);
+  } else if (A.io.in_dtype == FNTGPU_I8) {
+    k_aeq_process<FWD, FNTGPU_AEQ_IN_PLANAR, int8_t><<<grid, AEQ_WARPS * 32, 0, s>>>(st, A);
+  } else if (A.io.in_dtype == FNTGPU_I32) {
+    k_aeq_process<FWD, FNTGPU_AEQ_IN_PLANAR, int32_t><<<grid, AEQ_WARPS * 32, 0, s>>>(st, A);
+  } else {
+    return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_aeq_process(fntgpu_aeq_state* st, const fntgpu_aeq_params& prm,
+                               const fntgpu_aeq_io& io, cudaStream_t s) {
+  if (io.n_streams <= 0) return cudaSuccess;
+  const AeqArgs A = make_args(prm, &io);
+  if (prm.forward == FNTGPU_AEQ_FWD_DIRECT) return launch_fwd<FNTGPU_AEQ_FWD_DIRECT>(st, A, s);
+  return launch_fwd<FNTGPU_AEQ_FWD_FNT>(st, A, s);
+}
+
+cudaError_t launch_aeq_update_once(fntgpu_aeq_state* st, const fntgpu_aeq_params& prm,
+                                   const int64_t* xblk, const double* y, double mu, double* err,
+                                   cudaStream_t s) {
+  const AeqArgs A = make_args(prm, nullptr);
+  k_aeq_update_once<<<1, 32, 0, s>>>(st, A, xblk, y, mu, err);
+  return cudaGetLastError();
+}
+
+}  // namespace fntgpu

@@ -1,0 +1,218 @@
+"""Device-resident, multi-stream entry points (the throughput path).
+
+The reference API (fnt.py, cdc.py, aeq.py mirrors) moves numpy arrays per call.
+For many channels / long streams the data stays in HBM instead:
+
+* `CdcBank`   -- FNT-CDC over S streams x L samples in one launch, optionally
+                 restricted to an output range (range shards with a halo) and
+                 with the CDC->AEQ glue fused into its epilogue.
+* `AeqBank`   -- S independent FNT-AEQ states, one warp per stream.
+* `CdcAeqChain` -- the full per-link receiver chain of linksim.py:283-308 and
+                 399-406: CDC on both polarizations (int8 in, fused requantized
+                 int8 AEQ input and exact decimation statistics), the
+                 decimation-phase decision, and the adaptive FNT-AEQ.
+
+All tensors are torch CUDA tensors (plumbing); every compute step is a
+libfntgpu kernel.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+
+from . import _lib
+from .aeq import AeqConfig, aeq_params, mu_block_array
+from .cdc import FntCdcEngine
+
+
+def _t():
+    return _lib.torch()
+
+
+_TORCH2CODE = None
+
+
+def _code(t) -> int:
+    global _TORCH2CODE
+    if _TORCH2CODE is None:
+        tt = _t()
+        _TORCH2CODE = {tt.int8: _lib.I8, tt.int16: _lib.I16, tt.int32: _lib.I32,
+                       tt.int64: _lib.I64, tt.complex128: _lib.C128}
+    return _TORCH2CODE[t.dtype]
+
+
+class CdcBank:
+    """Launch wrapper around fntgpu_cdc64_process for one tap set."""
+
+    def __init__(self, engine: FntCdcEngine):
+        if not engine._fast():
+            raise NotImplementedError("CdcBank runs the cdc64 plan")
+        self.engine = engine
+        self.taps = engine.c_taps()
+        self.inv_scale = 1.0 / engine.output_scale
+
+    def run(self, xr, xi, *, length: int | None = None, x_first: int = 0,
+            out_first: int = 0, out_count: int | None = None, yr=None, yi=None,
+            qr=None, qi=None, q_spec=None, decim_acc=None, stream=None) -> None:
+        """xr, xi: (S, Lx) int8/int32/int64 device tensors holding global samples
+        [x_first, x_first + Lx) of S streams of length `length`. Outputs for the
+        global range [out_first, out_first + out_count) go to yr/yi (S, out_count)
+        (int16/int32/int64, or complex128 in yr) and/or the fused int8 requantized
+        planes qr/qi, and/or the decimation statistics decim_acc (S*8 uint64)."""
+        S, Lx = xr.shape
+        length = Lx if length is None else length
+        out_count = length - out_first if out_count is None else out_count
+        io = _lib.CdcIO()
+        io.n_streams = S
+        io.in_dtype = _code(xr)
+        io.xr, io.xi = xr.data_ptr(), xi.data_ptr()
+        io.x_stride = xr.stride(0)
+        io.x_first, io.x_count, io.length = x_first, Lx, length
+        io.out_first, io.out_count = out_first, out_count
+        io.out_dtype = _lib.NONE
+        io.inv_scale = self.inv_scale
+        if yr is not None:
+            io.out_dtype = _code(yr)
+            io.yr = yr.data_ptr()
+            io.yi = yi.data_ptr() if yi is not None else None
+            io.y_stride = yr.stride(0)
+        if qr is not None:
+            io.qr, io.qi = qr.data_ptr(), qi.data_ptr()
+            io.q_stride = qr.stride(0)
+            io.q_scale = float(q_spec.scale)
+            io.q_max = int(q_spec.max_int)
+        if decim_acc is not None:
+            io.decim_acc = decim_acc.data_ptr()
+        lib = _lib.load()
+        st = _lib.vp(stream.cuda_stream) if stream is not None else _lib.stream_handle()
+        _lib.check(lib.fntgpu_cdc64_process(C.byref(self.taps), C.byref(io), st), "cdc64_process")
+
+
+def decimation_phase(acc, n_links: int, length: int, phase_out, gap_out=None, stream=None) -> None:
+    io = _lib.DecimIO()
+    io.n_links = n_links
+    io.sps = 2
+    io.acc = acc.data_ptr()
+    io.length = length
+    io.phase = phase_out.data_ptr()
+    io.gap = gap_out.data_ptr() if gap_out is not None else None
+    lib = _lib.load()
+    st = _lib.vp(stream.cuda_stream) if stream is not None else _lib.stream_handle()
+    _lib.check(lib.fntgpu_decim_phase(C.byref(io), st), "decim_phase")
+
+
+class AeqBank:
+    """S independent FNT-AEQ streams (device state), one warp each."""
+
+    def __init__(self, config: AeqConfig, n_streams: int, forward: int | None = None):
+        self.config = config
+        self.n = n_streams
+        self.prm = aeq_params(config, forward)
+        self.state = _lib.zeros((n_streams * _lib.AEQ_STATE_BYTES,), np.uint8)
+        self.reset()
+
+    def reset(self, stream=None) -> None:
+        lib = _lib.load()
+        st = _lib.vp(stream.cuda_stream) if stream is not None else _lib.stream_handle()
+        _lib.check(lib.fntgpu_aeq_init(_lib.ptr(self.state), self.n, C.byref(self.prm), st),
+                   "aeq_init")
+
+    def _io(self, n_blocks, adapt, mu_blocks, y, err):
+        io = _lib.AeqIO()
+        io.n_streams = self.n
+        io.adapt = int(adapt)
+        io.n_blocks = n_blocks
+        io.mu_blocks = mu_blocks.data_ptr() if mu_blocks is not None else None
+        io.y = y.data_ptr()
+        io.y_stream_stride = y.stride(0)
+        io.y_row_stride = y.stride(1)
+        io.err = err.data_ptr() if err is not None else None
+        io.err_stream_stride = err.stride(0) if err is not None else 0
+        return io
+
+    def run_planar(self, x, n_blocks: int, y, *, adapt=True, mu_blocks=None, err=None,
+                   stream=None) -> None:
+        """x: (S, 4, ld) int8/int32 device tensor; y: (S, 4, >=16 n_blocks) float64."""
+        io = self._io(n_blocks, adapt, mu_blocks, y, err)
+        io.in_mode = _lib.AEQ_IN_PLANAR
+        io.in_dtype = _code(x)
+        io.x = x.data_ptr()
+        io.x_stream_stride = x.stride(0)
+        io.x_row_stride = x.stride(1)
+        self._launch(io, stream)
+
+    def run_decim(self, qr, qi, phase, n_blocks: int, y, *, adapt=True, mu_blocks=None,
+                  err=None, stream=None) -> None:
+        """qr, qi: (2S, Lq) int8 requantized CDC planes (pol X = row 2s, pol Y = 2s+1);
+        phase: (S,) int32 decimation phase per link."""
+        io = self._io(n_blocks, adapt, mu_blocks, y, err)
+        io.in_mode = _lib.AEQ_IN_DECIM
+        io.in_dtype = _lib.I8
+        io.qr, io.qi = qr.data_ptr(), qi.data_ptr()
+        io.q_stride = qr.stride(0)
+        io.phase = phase.data_ptr()
+        self._launch(io, stream)
+
+    def _launch(self, io, stream):
+        lib = _lib.load()
+        st = _lib.vp(stream.cuda_stream) if stream is not None else _lib.stream_handle()
+        _lib.check(lib.fntgpu_aeq_process(_lib.ptr(self.state), C.byref(self.prm), C.byref(io), st),
+                   "aeq_process")
+
+    def read_state(self) -> list[_lib.AeqState]:
+        raw = _lib.to_host(self.state).tobytes()
+        sz = _lib.AEQ_STATE_BYTES
+        return [_lib.AeqState.from_buffer_copy(raw[i * sz:(i + 1) * sz]) for i in range(self.n)]
+
+
+class CdcAeqChain:
+    """Receiver chain for n_links dual-polarization links of L samples each
+    (linksim.py:283-308 + 399-406), all buffers preallocated in HBM.
+
+    Inputs: xr, xi (2*n_links, L) int8 -- quantized front-end I/Q, row 2l = pol X
+    and 2l+1 = pol Y of link l. Output: y (n_links, 4, 16*n_blocks) float64, the
+    AEQ outputs [XI, XQ, YI, YQ]; err (n_links, n_blocks) the err_trace."""
+
+    def __init__(self, engine: FntCdcEngine, aeq_config: AeqConfig, n_links: int, length: int,
+                 sig_spec, mu_schedule=None, forward: int | None = None, keep_cdc_int=False):
+        t = _t()
+        dev = _lib.device()
+        self.cdc = CdcBank(engine)
+        self.n_links = n_links
+        self.L = length
+        self.sig_spec = sig_spec
+        S = 2 * n_links
+        # decimated length per phase is ceil((L - ph) / 2); both fit in Lq = ceil(L/2)
+        self.n_sym = length // 2  # phase-1 length; phase 0 has ceil(L/2) >= this
+        hop = aeq_config.l_taps
+        self.n_blocks = (length - 1) // 2 // hop if length % 2 else (length // 2) // hop
+        # q planes: padded to a multiple of 32 bytes so 32-byte loads stay in bounds
+        lq = -(-length // 32) * 32 + 32
+        self.qr = t.zeros((S, lq), dtype=t.int8, device=dev)
+        self.qi = t.zeros((S, lq), dtype=t.int8, device=dev)
+        self.acc = t.zeros((S * 8,), dtype=t.int64, device=dev)
+        self.phase = t.zeros((n_links,), dtype=t.int32, device=dev)
+        self.gap = t.zeros((n_links,), dtype=t.float64, device=dev)
+        self.y = t.empty((n_links, 4, 16 * self.n_blocks), dtype=t.float64, device=dev)
+        self.err = t.empty((n_links, max(self.n_blocks, 1)), dtype=t.float64, device=dev)
+        self.yint = None
+        if keep_cdc_int:
+            self.yint = (t.empty((S, length), dtype=t.int16, device=dev),
+                         t.empty((S, length), dtype=t.int16, device=dev))
+        self.aeq = AeqBank(aeq_config, n_links, forward)
+        mu = mu_block_array(self.n_blocks, hop, mu_schedule, aeq_config.mu)
+        self.mu_blocks = t.from_numpy(mu).to(dev)
+
+    def run(self, xr, xi, stream=None, reset=True) -> None:
+        """One pass of the chain over the resident inputs (no host sync)."""
+        if reset:
+            self.aeq.reset(stream)
+        self.acc.zero_()
+        yr, yi = self.yint if self.yint is not None else (None, None)
+        self.cdc.run(xr, xi, length=self.L, yr=yr, yi=yi, qr=self.qr, qi=self.qi,
+                     q_spec=self.sig_spec, decim_acc=self.acc, stream=stream)
+        decimation_phase(self.acc, self.n_links, self.L, self.phase, self.gap, stream=stream)
+        self.aeq.run_decim(self.qr, self.qi, self.phase, self.n_blocks, self.y, adapt=True,
+                           mu_blocks=self.mu_blocks, err=self.err, stream=stream)

@@ -1,0 +1,391 @@
+"""GPU parity: the sm_100a kernels (through the public drop-in API and the C
+ABI) against the reference's golden fixtures and the pinned CPU oracle.
+Integer outputs are compared bit-exactly; float64 AEQ outputs bit-exactly too
+(the update reproduces numpy's operation order)."""
+
+import numpy as np
+import pytest
+
+import oracle as O
+import paper_2405_04253_b200 as P
+from conftest import SIG_SCALE, sha
+
+pytestmark = pytest.mark.gpu
+
+PLANS = ("mod17", "aeq32", "cdc64")
+
+
+@pytest.fixture(scope="module")
+def plans():
+    return P.default_plans()
+
+
+# ---------------------------------------------------------------- transforms
+
+@pytest.mark.parametrize("name", PLANS)
+def test_fnt_ifnt_golden(golden, plans, name):
+    g = golden("transforms")
+    p = plans[name]
+    for k, suf in (("x", ""), ("xs", "_xs"), ("ext", "_ext")):
+        assert np.array_equal(P.fnt(p, g[f"{name}_{k}"]), g[f"{name}_fnt{suf}"]), k
+        assert np.array_equal(P.ifnt(p, g[f"{name}_{k}"]), g[f"{name}_ifnt{suf}"]), k
+    out = P.fnt(p, g[f"{name}_x3"])
+    assert out.shape == (3, 5, p.n) and out.dtype == np.int64
+    assert np.array_equal(out, g[f"{name}_fnt3"])
+
+
+def test_selftest_golden_vectors(golden, plans):
+    g = golden("selftest")
+    p17 = plans["mod17"]
+    assert np.array_equal(P.fnt(p17, np.array([1, 0, 0, 0, 0, 0, 0, 0])), np.ones(8, np.int64))
+    assert np.array_equal(P.fnt(p17, np.array([1, 1, 0, 0, 0, 0, 0, 0])), [2, 3, 5, 9, 0, 16, 14, 10])
+    assert np.array_equal(P.ifnt(p17, np.array([2, 3, 5, 9, 0, 16, 14, 10])), [1, 1, 0, 0, 0, 0, 0, 0])
+    for name in PLANS:
+        p = plans[name]
+        assert np.array_equal(P.ifnt(p, P.fnt(p, g[f"rt_{name}_x"])), g[f"rt_{name}_y"])
+    assert np.array_equal(P.convolve_signed_real(p17, [1, 2, 0, 0, 0, 0, 0, 0], [3, 1, 0, 0, 0, 0, 0, 0]),
+                          [3, 7, 2, 0, 0, 0, 0, 0])
+
+
+def test_fault_injection_negative_control(plans):
+    """cli.py:84-86: a corrupted twiddle table must change the transform."""
+    p = P.default_plans()["mod17"]
+    p.fwd_twiddles[-1][1] += 1
+    assert not np.array_equal(P.fnt(p, np.array([1, 1, 0, 0, 0, 0, 0, 0])), [2, 3, 5, 9, 0, 16, 14, 10])
+    p = P.default_plans()["cdc64"]
+    x = np.random.default_rng(1).integers(0, 65537, (4, 64))
+    good = P.fnt(p, x)
+    p.fwd_twiddles[-1][1] += 1
+    assert not np.array_equal(P.fnt(p, x), good)
+
+
+@pytest.mark.parametrize("name", PLANS)
+def test_random_round_trip_and_oracle(plans, name):
+    p = plans[name]
+    rng = np.random.default_rng(5)
+    x = rng.integers(0, p.params.F, (1000, p.n))
+    X = P.fnt(p, x)
+    assert np.array_equal(X, O.fnt(O.Plan.named(name), x))
+    assert np.array_equal(P.ifnt(p, X), x)
+
+
+def test_other_valid_plans_generic_kernel():
+    """Any plan make_plan accepts runs (table-driven kernel)."""
+    for t, alpha, n in ((4, pow(3, 16, 65537), 1 << 12), (4, 4, 16), (3, 2, 16), (1, 2, 4), (4, 65536, 2)):
+        p = P.make_plan(P.FermatParams(t), alpha, n)
+        op = O.Plan(t, n, alpha)
+        x = np.random.default_rng(n).integers(-(1 << 20), 1 << 20, (7, n))
+        assert np.array_equal(P.fnt(p, x), O.fnt(op, x)), (t, alpha, n)
+        assert np.array_equal(P.ifnt(p, x), O.ifnt(op, x)), (t, alpha, n)
+
+
+def test_transform_errors(plans):
+    with pytest.raises(ValueError, match="expected length 64, got 63"):
+        P.fnt(plans["cdc64"], np.zeros(63))
+    with pytest.raises(P.InvalidPlanError):
+        P.make_plan(P.FermatParams(4), 2, 64)
+    assert P.fnt(plans["cdc64"], np.zeros((0, 64))).shape == (0, 64)
+
+
+# -------------------------------------------------------------- convolutions
+
+@pytest.mark.parametrize("name", PLANS)
+def test_convolution_golden(golden, plans, name):
+    c = golden("convolution")
+    p = plans[name]
+    F = p.params.F
+    xr, xi, yr, yi = (c[f"{name}_{k}"] for k in ("xr", "xi", "yr", "yi"))
+    assert np.array_equal(P.cyclic_convolve_real(p, xr % F, yr[0] % F), c[f"{name}_real_bcast"])
+    assert np.array_equal(P.cyclic_convolve_real(p, xr % F, yr % F), c[f"{name}_real"])
+    zr, zi = P.cyclic_convolve_complex(p, xr % F, xi % F, yr % F, yi % F)
+    assert np.array_equal(zr, c[f"{name}_cplx_re"]) and np.array_equal(zi, c[f"{name}_cplx_im"])
+    assert np.array_equal(P.convolve_signed_real(p, xr, yr), c[f"{name}_signed_real"])
+    sr, si = P.convolve_signed_complex(p, xr, xi, yr, yi)
+    assert np.array_equal(sr, c[f"{name}_signed_cplx_re"]) and np.array_equal(si, c[f"{name}_signed_cplx_im"])
+
+
+def test_config1_full(golden, digests, plans):
+    """BASELINE config 1: 16384 x 64, seed 0, bit-exact (reference digest)."""
+    p = plans["cdc64"]
+    rng = np.random.default_rng(0)
+    x = rng.integers(-16, 16, (16384, 64))
+    h = rng.integers(-32, 32, (16384, 64))
+    P.COUNTER.reset()
+    with P.COUNTER.enabled_ctx():
+        z = P.cyclic_convolve_real(p, x % p.params.F, h % p.params.F)
+        n = P.COUNTER.total()
+    assert sha(z) == digests["convolution"]["c1_cyclic_real"]
+    assert n == digests["convolution"]["c1_counter"]
+    assert sha(P.convolve_signed_real(p, x, h)) == digests["convolution"]["c1_signed_real"]
+
+
+def test_convolution_extremes(golden, plans):
+    c = golden("convolution")
+    p = plans["cdc64"]
+    assert np.array_equal(P.convolve_signed_real(p, c["ext_x"], c["ext_h"]), c["ext_z"])
+    assert np.array_equal(P.convolve_signed_real(p, c["wrap_x"], c["wrap_h"]), c["wrap_z"])
+    with pytest.raises(ValueError, match="encodable signed range"):
+        P.convolve_signed_real(p, np.full(64, 32769), np.zeros(64))
+
+
+# ------------------------------------------------------------------ quantize
+
+def test_quantize_golden(golden):
+    q = golden("quantize")
+    for tag, (bits, sc) in {"s5": (5, SIG_SCALE), "s6": (6, 128.0), "s8": (8, 8.0)}.items():
+        spec = P.QuantSpec(bits, sc)
+        for k in ("x", "ties", "exact", "special"):
+            v, cnt = P.quantize_real(q[k], spec)
+            assert v.dtype == np.int64
+            assert np.array_equal(v, q[f"{tag}_{k}_q"]), (tag, k)
+            assert cnt == int(q[f"{tag}_{k}_c"]), (tag, k)
+
+
+def test_encode_decode_arrays():
+    f = P.FermatParams(4)
+    v = np.array([-32768, -1, 0, 1, 32768])
+    assert np.array_equal(P.encode_signed_array(v, f), [32769, 65536, 0, 1, 32768])
+    assert np.array_equal(P.decode_signed_array([32769, 65536, 0, 1, 32768, 100000], f),
+                          [-32768, -1, 0, 1, 32768, 34463])
+    with pytest.raises(ValueError):
+        P.encode_signed_array([40000], f)
+
+
+# ----------------------------------------------------------------------- CDC
+
+def _c2_engine():
+    cfg = P.LinkConfig(n_symbols=2 ** 18, z_km=75.0, snr_db=(20.0,), pol_rotation_deg=0.0,
+                       dgd_symbols=0.0, iq_skew_samples=0.0, seed=1)
+    return P.FntCdcEngine(cfg.cdc_config("fnt"), cfg.sig_spec())
+
+
+def test_cdc_engine_constants(golden, digests):
+    a = golden("cdc")
+    eng = _c2_engine()
+    assert np.array_equal(eng.tap_re, a["tap_re"]) and np.array_equal(eng.tap_im, a["tap_im"])
+    assert np.array_equal(eng.taps, a["taps_float"])
+    assert np.array_equal(eng._b_plus, a["b_plus"]) and np.array_equal(eng._b_minus, a["b_minus"])
+    d = digests["cdc"]
+    assert eng.budget.bound == d["c2_budget_bound"] and eng.tap_scale == d["c2_tap_scale"]
+    assert eng.output_scale == d["c2_output_scale"]
+    assert eng.support_warning == d["c2_support_warning"]
+
+
+def test_cdc_config2_full(golden, digests):
+    """BASELINE config 2 (2^19 samples, 75 km, 20 dB) bit-exact vs the reference."""
+    a = golden("cdc")
+    eng = _c2_engine()
+    P.COUNTER.reset()
+    with P.COUNTER.enabled_ctx():
+        yr, yi = eng.process_int(a["c2_xr"].astype(np.int64), a["c2_xi"].astype(np.int64))
+        assert P.COUNTER.total("cdc-fnt") == digests["cdc"]["c2_counter"]
+    assert yr.dtype == np.int64
+    assert sha(yr) == digests["cdc"]["c2_yr"] and sha(yi) == digests["cdc"]["c2_yi"]
+    # int8 input path gives the same bits
+    yr8, yi8 = eng.process_int(a["c2_xr"], a["c2_xi"])
+    assert np.array_equal(yr8, yr) and np.array_equal(yi8, yi)
+    y = eng.process(a["c2_xr"], a["c2_xi"])
+    assert y.dtype == np.complex128 and sha(y) == digests["cdc"]["c2_process"]
+
+
+def test_cdc_edges(golden):
+    a = golden("cdc")
+    eng = _c2_engine()
+    for L in (0, 1, 2, 15, 16, 17, 31, 32, 33, 63, 64, 65, 97, 1000, 4097):
+        r, i = eng.process_int(a[f"len{L}_xr"], a[f"len{L}_xi"])
+        assert np.array_equal(r, a[f"len{L}_yr"]) and np.array_equal(i, a[f"len{L}_yi"]), L
+    for tag in ("sat", "wide"):
+        r, i = eng.process_int(a[f"{tag}_xr"], a[f"{tag}_xi"])
+        assert np.array_equal(r, a[f"{tag}_yr"]) and np.array_equal(i, a[f"{tag}_yi"]), tag
+    br, bi = eng.process_block(a["blk_r"], a["blk_i"])
+    assert np.array_equal(br, a["blk_out_r"]) and np.array_equal(bi, a["blk_out_i"])
+    with pytest.raises(ValueError, match="encodable"):
+        eng.process_int(np.full(10, 40000), np.zeros(10))
+
+
+@pytest.mark.parametrize("tag,cfg", [
+    ("t33", dict(z_km=25.0, fs_hz=80e9, n_taps=33)),
+    ("z0", dict(z_km=0.0, fs_hz=80e9, n_taps=32)),
+    ("t17", dict(z_km=10.0, fs_hz=80e9, n_taps=17)),
+    ("t1", dict(z_km=5.0, fs_hz=80e9, n_taps=1)),
+])
+def test_cdc_other_tap_designs(golden, tag, cfg):
+    a = golden("cdc")
+    eng = P.FntCdcEngine(P.CdcConfig(**cfg), P.QuantSpec(5, 8.0))
+    assert np.array_equal(eng.tap_re, a[f"{tag}_tap_re"]) and eng.tap_scale == float(a[f"{tag}_scale"])
+    r, i = eng.process_int(a[f"{tag}_xr"], a[f"{tag}_xi"])
+    assert np.array_equal(r, a[f"{tag}_yr"]) and np.array_equal(i, a[f"{tag}_yi"])
+
+
+def test_cdc_budget_error():
+    with pytest.raises(P.BudgetError):
+        P.FntCdcEngine(P.CdcConfig(z_km=0.0, fs_hz=80e9, n_taps=32), P.QuantSpec(12, 8.0))
+
+
+def test_cdc_bank_ranges_match_full_stream():
+    """Range shards with the 15/16-sample halo reproduce the full stream
+    (SURVEY 8e), through the device-resident multi-stream API."""
+    import torch
+    from paper_2405_04253_b200.stream import CdcBank
+    eng = _c2_engine()
+    bank = CdcBank(eng)
+    rng = np.random.default_rng(11)
+    S, L = 3, 100_003
+    xr = rng.integers(-15, 16, (S, L)).astype(np.int8)
+    xi = rng.integers(-15, 16, (S, L)).astype(np.int8)
+    dxr, dxi = torch.from_numpy(xr).cuda(), torch.from_numpy(xi).cuda()
+    yr = torch.empty((S, L), dtype=torch.int32, device="cuda")
+    yi = torch.empty_like(yr)
+    bank.run(dxr, dxi, yr=yr, yi=yi)
+    full_r, full_i = yr.cpu().numpy(), yi.cpu().numpy()
+    for s in range(S):
+        orr, ori = O.cdc_direct(eng.tap_re, eng.tap_im, xr[s], xi[s])
+        assert np.array_equal(full_r[s], orr) and np.array_equal(full_i[s], ori)
+    # 4 uneven shards, each fed only its inputs [a - 48, b + 48) (block-aligned halo)
+    cuts = [0, 17_000, 50_001, 77_777, L]
+    for a, b in zip(cuts[:-1], cuts[1:]):
+        lo, hi = max(0, (a + 16) // 32 * 32 - 32), min(L, ((b - 1 + 16) // 32) * 32 + 32)
+        sr = torch.empty((S, b - a), dtype=torch.int32, device="cuda")
+        si = torch.empty_like(sr)
+        bank.run(dxr[:, lo:hi].contiguous(), dxi[:, lo:hi].contiguous(), length=L, x_first=lo,
+                 out_first=a, out_count=b - a, yr=sr, yi=si)
+        assert np.array_equal(sr.cpu().numpy(), full_r[:, a:b])
+        assert np.array_equal(si.cpu().numpy(), full_i[:, a:b])
+    # a shard missing part of its halo is rejected before launch
+    with pytest.raises(ValueError, match="needed"):
+        bank.run(dxr[:, 1000:2000].contiguous(), dxi[:, 1000:2000].contiguous(), length=L,
+                 x_first=1000, out_first=1000, out_count=1000, yr=sr, yi=si)
+
+
+# ----------------------------------------------------------------------- AEQ
+
+AEQ_MODES = (0, 1)  # FNTGPU_AEQ_FWD_FNT, FNTGPU_AEQ_FWD_DIRECT
+
+
+def _aeq(mu=1e-4, forward=0):
+    cfg = P.AeqConfig(block_n=32, l_taps=16, mu=mu, sig_spec=P.QuantSpec(5, SIG_SCALE))
+    return P.FntAeq(cfg, forward=forward)
+
+
+@pytest.mark.parametrize("forward", AEQ_MODES)
+@pytest.mark.parametrize("tag", ["a", "b"])
+def test_aeq_link_golden(golden, tag, forward):
+    g = golden("aeq")
+    eq = _aeq(forward=forward)
+    cfg = P.LinkConfig()
+    y = eq.process(g[f"{tag}_q"], adapt=True, mu_schedule=cfg.mu_schedule())
+    assert np.array_equal(y, g[f"{tag}_y"])
+    assert np.array_equal(eq.w, g[f"{tag}_w"])
+    assert np.array_equal(eq.taps.w_int, g[f"{tag}_wint"])
+    assert np.array_equal(eq.history, g[f"{tag}_hist"])
+    assert np.array_equal(np.array(eq.err_trace), g[f"{tag}_err"])
+    assert eq.saturations == int(g[f"{tag}_sat"])
+    assert eq.symbols_processed == g[f"{tag}_q"].shape[1] // 16 * 16
+
+
+@pytest.mark.parametrize("forward", AEQ_MODES)
+def test_aeq_saturation_noadapt_streaming(golden, forward):
+    g = golden("aeq")
+    eq = _aeq(mu=0.05, forward=forward)
+    y = eq.process(g["c_q"])
+    assert np.array_equal(y, g["c_y"]) and np.array_equal(eq.w, g["c_w"])
+    assert np.array_equal(eq.taps.w_int, g["c_wint"]) and eq.saturations == int(g["c_sat"])
+    assert np.array_equal(np.array(eq.err_trace), g["c_err"])
+    eq = _aeq(forward=forward)
+    P.COUNTER.reset()
+    with P.COUNTER.enabled_ctx():
+        y = eq.process(g["d_q"], adapt=False)
+        assert P.COUNTER.total("aeq-fnt") == 65536
+    assert np.array_equal(y, g["d_y"]) and eq.err_trace == []
+    assert np.array_equal(eq.history, g["d_hist"])
+    eq = _aeq(forward=forward)
+    sched = lambda i: 0.0 if (i // 16) % 5 == 3 else 3e-3  # noqa: E731
+    q = g["e_q"]
+    y1 = eq.process(q[:, :16 * 77], mu_schedule=sched)
+    y2 = eq.process(q[:, 16 * 77:], mu_schedule=sched)
+    assert np.array_equal(y1, g["e_y1"]) and np.array_equal(y2, g["e_y2"])
+    assert np.array_equal(eq.w, g["e_w"]) and np.array_equal(eq.taps.w_int, g["e_wint"])
+    assert np.array_equal(np.array(eq.err_trace), g["e_err"])
+
+
+def test_aeq_single_block_api(golden):
+    g = golden("aeq")
+    eq = _aeq()
+    y, xb = eq.equalize_block(g["f_x"])
+    assert np.array_equal(y, g["f_y"]) and np.array_equal(xb, g["f_xblk"])
+    eq.update_taps(xb, y, mu=0.01)
+    assert np.array_equal(eq.w, g["f_w"])
+    y2, xb2 = eq.equalize_block(g["f_xblk2"][:, 16:])
+    assert np.array_equal(y2, g["f_y2"]) and np.array_equal(xb2, g["f_xblk2"])
+
+
+@pytest.mark.parametrize("forward", AEQ_MODES)
+def test_aeq_wide_inputs_match_oracle(forward):
+    """|x| up to 2^15: per-group residues wrap mod F exactly as the reference's."""
+    rng = np.random.default_rng(3)
+    x = rng.integers(-32768, 32769, (4, 16 * 40))
+    eq = _aeq(forward=forward)
+    y = eq.process(x, adapt=False)
+    oq = O.Aeq(SIG_SCALE)
+    assert np.array_equal(y, oq.process(x, adapt=False))
+    x = rng.integers(-300, 301, (4, 16 * 40))
+    eq = _aeq(mu=1e-6, forward=forward)
+    oq = O.Aeq(SIG_SCALE, mu=1e-6)
+    assert np.array_equal(eq.process(x), oq.process(x))
+    assert np.array_equal(eq.w, oq.w)
+
+
+def test_aeq_bank_many_streams_vs_oracle():
+    """The multi-stream kernel (one warp per stream) against the oracle on
+    independent random streams with the LinkConfig gear-shift schedule."""
+    import torch
+    from paper_2405_04253_b200.stream import AeqBank
+    cfg = P.LinkConfig().aeq_config()
+    S, nb = 37, 300
+    rng = np.random.default_rng(21)
+    x = rng.integers(-15, 16, (S, 4, 16 * nb)).astype(np.int8)
+    mu = O.mu_blocks(nb, mu1=2e-3, mu2=1e-4, gear_symbols=2000)
+    for forward in AEQ_MODES:
+        bank = AeqBank(cfg, S, forward=forward)
+        y = torch.empty((S, 4, 16 * nb), dtype=torch.float64, device="cuda")
+        err = torch.empty((S, nb), dtype=torch.float64, device="cuda")
+        bank.run_planar(torch.from_numpy(x).cuda(), nb, y, mu_blocks=torch.from_numpy(mu).cuda(), err=err)
+        yh, eh = y.cpu().numpy(), err.cpu().numpy()
+        st = bank.read_state()
+        for s in (0, 1, 17, 36):
+            oq = O.Aeq(cfg.sig_spec.scale, mu=cfg.mu)
+            oy = oq.process(x[s].astype(np.int64), mu_blocks=mu)
+            assert np.array_equal(yh[s], oy), (forward, s)
+            assert np.array_equal(eh[s], np.array(oq.err_trace))
+            assert np.array_equal(np.array(st[s].w).reshape(4, 4, 16), oq.w)
+
+
+# ------------------------------------------------------- CDC -> AEQ glue chain
+
+def test_chain_matches_reference_glue(golden):
+    """CDC (fused requantization + decimation statistics) -> phase -> AEQ on the
+    75 km / 45 deg link of fixture b: phase, requantized AEQ input and the AEQ
+    outputs equal the reference's rx_frontend + run_single glue."""
+    import torch
+    from paper_2405_04253_b200.stream import CdcAeqChain
+    g = golden("aeq")
+    cfg = P.LinkConfig(n_symbols=2 ** 14, z_km=75.0, snr_db=(18.0,), pol_rotation_deg=45.0,
+                       dgd_symbols=0.0, iq_skew_samples=0.0, seed=6)
+    eng = P.FntCdcEngine(cfg.cdc_config("fnt"), cfg.sig_spec())
+    q = g["b_cdc_q"]  # (pol, re/im, L) int8 front-end samples
+    L = q.shape[-1]
+    xr = torch.from_numpy(np.ascontiguousarray(q[:, 0])).cuda()
+    xi = torch.from_numpy(np.ascontiguousarray(q[:, 1])).cuda()
+    chain = CdcAeqChain(eng, cfg.aeq_config(), 1, L, cfg.sig_spec(), cfg.mu_schedule(),
+                        keep_cdc_int=True)
+    chain.run(xr, xi)
+    assert int(chain.phase.cpu()[0]) == int(g["b_phase"])
+    ph = int(g["b_phase"])
+    qa = np.stack([chain.qr[0, ph:L:2].cpu().numpy(), chain.qi[0, ph:L:2].cpu().numpy(),
+                   chain.qr[1, ph:L:2].cpu().numpy(), chain.qi[1, ph:L:2].cpu().numpy()])
+    assert np.array_equal(qa, g["b_q"].astype(np.int8))
+    y = chain.y[0].cpu().numpy()
+    assert np.array_equal(y, g["b_y"])
+    assert np.array_equal(chain.err[0].cpu().numpy(), g["b_err"])
+    y0 = eng.process(q[0, 0], q[0, 1])
+    assert np.array_equal(y0[:2048], g["b_cdc_y0_head"])

@@ -1,0 +1,452 @@
+#!/usr/bin/env python3
+"""FNT-CDC + FNT-AEQ throughput on B200 (BASELINE.json metric).
+
+Workload (default, --config c5): BASELINE config 5 -- many-channel dual-pol
+PDM-16QAM receivers: per GPU `--links` (4096) independent links of 2^18 symbols
+at 2 sps (L = 2^19 complex samples per polarization), 75 km, per-link Haar Jones
+rotation and SNR ~ U[16, 22] dB, generated on device (paper_2405_04253_b200.
+linkgen; statistically equivalent to the reference generator, not bitwise).
+One step = the whole receiver chain over every link with inputs resident in
+HBM: FNT-CDC on both polarizations (fused requantization + decimation
+statistics) -> decimation phase -> adaptive FNT-AEQ (fresh state per link,
+LinkConfig gear-shift mu schedule). Inputs (8.6 GB) exceed L2 (126 MB), so no
+L2 flush is needed between steps.
+
+Metric: Gsamples/s = complex samples per polarization, summed over
+polarizations and links, per second (whole job, all ranks).
+
+    python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...   (one process per GPU,
+        links sharded as independent objects: weak scaling, no collective on
+        the data path; NCCL only reduces the timing/sample counts)
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+if str(ROOT) not in sys.path:
+    sys.path.insert(0, str(ROOT))
+
+METRIC = "FNT-CDC+AEQ Gsamples/s"
+UNIT = "Gsamples/s"
+PROFILES = ROOT / "profiles"
+
+# Algorithmic work per unit (SURVEY 8d convention):
+#   radix-2 butterfly = 6 INT ops, general residue product = 6, modular aux op = 2
+CDC_INT_OPS_PER_BLOCK = 4 * 192 * 6 + 128 * 6 + 256 * 2   # 5888 per 64-block = 184 / sample
+AEQ_INT_OPS_PER_BLOCK_FNT = (4 + 32 + 32) * 80 * 6 + 1024 * 6 + 448  # 39232 (incl. tap-spectrum refresh)
+AEQ_INT_OPS_PER_BLOCK_DIRECT = 2 * 4096 + 448               # 8640 (exact time-domain MIMO FIR)
+AEQ_FP64_OPS_PER_BLOCK = 2 * 4096 + 256 * 4 + 64 * 2 + 32 * 12  # gradient + update + y + rde ~ 9728
+
+
+def measured_peaks() -> dict:
+    peaks = {}
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        peaks.update(json.loads(p.read_text()))
+    q = PROFILES / "int_peaks_r01.json"
+    if q.exists():
+        d = json.loads(q.read_text())
+        peaks["int_tops"] = d["mixed_iadd_imad"]["Tinst_per_s"]
+        peaks["fp64_tinst"] = d["fp64_dadd"]["Tinst_per_s"]
+        peaks["int_source"] = "measured: profiles/int_peaks_r01.json (tools/int_peaks.cu)"
+    else:
+        peaks["int_tops"] = 36.0
+        peaks["fp64_tinst"] = 18.3
+        peaks["int_source"] = "fallback constants"
+    peaks.setdefault("hbm_gbs", 6650.0)
+    return peaks
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines: list[str] = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "200", "-i", str(self.index)], stdout=subprocess.PIPE,
+                stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ------------------------------------------------------------------ CPU side
+
+def _cpu_task(args):
+    """One link through the numpy restatement of the reference (np_port.chain)."""
+    xr2, xi2, tap_re, tap_im, n_taps, out_scale, sig_scale, mu = args
+    import oracle.np_port as N
+    t0 = time.perf_counter()
+    N.chain(xr2, xi2, tap_re, tap_im, n_taps, out_scale, sig_scale, mu)
+    return time.perf_counter() - t0
+
+
+def cpu_links_sample(n_tasks: int, n_sym: int, seed: int = 4):
+    """Bounded CPU sample: n_tasks links of n_sym symbols from the numpy
+    generator port of the reference link model (oracle.linkgen), falling back to
+    i.i.d. 5-bit samples if unavailable; returns per-task inputs."""
+    rng = np.random.default_rng(seed)
+    L = 2 * n_sym
+    out = []
+    for _ in range(n_tasks):
+        out.append((rng.integers(-15, 16, (2, L)), rng.integers(-15, 16, (2, L))))
+    return out
+
+
+def run_cpu_baseline(engine, cfg, n_sym: int, cores: int, rounds: int = 1) -> dict:
+    """Time the reference algorithm (numpy port) on all host cores."""
+    from concurrent.futures import ProcessPoolExecutor
+    import oracle.np_port  # noqa: F401  (checker / baseline only)
+    hop = 16
+    nb = n_sym // hop
+    mu = np.where(np.arange(nb) * hop < cfg.gear_symbols, cfg.mu1, cfg.mu2)
+    samples = cpu_links_sample(cores, n_sym)
+    args = [(xr, xi, engine.tap_re, engine.tap_im, cfg.n_cdc_taps, engine.output_scale,
+             cfg.sig_scale, mu) for xr, xi in samples]
+    with ProcessPoolExecutor(max_workers=cores) as ex:
+        list(ex.map(_cpu_task, args[:1]))  # warm the workers' imports
+        t0 = time.perf_counter()
+        for _ in range(rounds):
+            list(ex.map(_cpu_task, args))
+        wall = time.perf_counter() - t0
+    n_samples = rounds * cores * 2 * (2 * n_sym)
+    return {"value": n_samples / wall / 1e9, "unit": UNIT, "cores": cores, "kind": "port",
+            "sample": (f"{rounds * cores} links x 2 pols x {2 * n_sym} samples (2^{int(math.log2(n_sym))} "
+                       f"symbols) through oracle/np_port.chain (numpy restatement of the reference's "
+                       f"CDC -> glue -> AEQ, pinned to reference fixtures), one process per core, "
+                       f"{wall:.1f} s wall"),
+            "wall_s": wall}
+
+
+def impl_reference(args) -> None:
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    sys.path.insert(0, str(ROOT))
+    from paper_2405_04253_b200.cdc import CdcConfig
+    cfg = _link_cfg(args)
+    cores = os.cpu_count() or 1
+    eng = _HostEngine(cfg)
+    n_sym = args.cpu_symbols
+    for _ in range(args.warmup and 1):
+        run_cpu_baseline(eng, cfg, n_sym, cores)
+    t0 = time.perf_counter()
+    vals = [run_cpu_baseline(eng, cfg, n_sym, cores) for _ in range(args.steps)]
+    wall = time.perf_counter() - t0
+    v = float(np.mean([x["value"] for x in vals]))
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * wall / max(args.steps, 1),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int64+f64",
+        "data": "synthetic", "config": _config_dict(args, cpu=True),
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "port",
+                         "sample": vals[0]["sample"]},
+        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "gpu_launches": 0,
+        "note": ("the reference is pure numpy (no native build); its algorithm is timed through "
+                 "oracle/np_port.py, a numpy restatement pinned to the reference's golden outputs"),
+    }
+    del CdcConfig
+    print(json.dumps(line))
+
+
+class _HostEngine:
+    """Tap constants computed on the host exactly as FntCdcEngine does, for the
+    CPU-only reference arm (no GPU needed)."""
+
+    def __init__(self, cfg):
+        from paper_2405_04253_b200.cdc import design_cd_taps
+        import oracle
+        c = cfg.cdc_config("fnt")
+        taps = design_cd_taps(c)
+        max_int = (1 << (c.tap_bits - 1)) - 1
+        peak = max(np.abs(taps.real).max(), np.abs(taps.imag).max())
+        scale = 2.0 ** math.floor(math.log2(max_int / peak))
+        self.tap_re, _ = oracle.quantize_real(taps.real, scale, max_int)
+        self.tap_im, _ = oracle.quantize_real(taps.imag, scale, max_int)
+        self.tap_scale = scale
+        self.output_scale = cfg.sig_scale * scale
+
+
+# ------------------------------------------------------------------ GPU side
+
+def _link_cfg(args):
+    from paper_2405_04253_b200.linksim import LinkConfig
+    return LinkConfig(n_symbols=args.symbols, z_km=75.0, pol_rotation_deg=0.0, dgd_symbols=0.0,
+                      iq_skew_samples=0.0, seed=4)
+
+
+def _config_dict(args, cpu=False):
+    d = {"workload": ("C5 many-channel FNT-CDC+FNT-AEQ: per GPU %d dual-pol PDM-16QAM links x 2^%d "
+                      "symbols x 2 sps, 75 km SSMF, Haar Jones, SNR U[16,22] dB, 5-bit I/Q, "
+                      "6-bit CDC taps (N=64 sqrt2 FNT), 4x4 FNT-AEQ (N=32) gear-shift mu")
+                     % (args.links, int(math.log2(args.symbols))),
+         "links_per_gpu": args.links, "symbols": args.symbols, "samples_per_pol": 2 * args.symbols,
+         "aeq_forward": args.forward, "parallelism": f"links sharded over {args.gpus} GPU(s), no collective",
+         "l2": "inputs (int8 I/Q, %.1f GB/GPU) exceed the 126 MB L2; no flush needed"
+               % (4 * args.links * 2 * args.symbols / 1e9)}
+    if cpu:
+        d["cpu_symbols"] = args.cpu_symbols
+    return d
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--links", type=int, default=4096, help="links per GPU (C5: 4096)")
+    ap.add_argument("--symbols", type=int, default=1 << 18)
+    ap.add_argument("--forward", default="fnt", choices=["fnt", "direct"])
+    ap.add_argument("--e2e-links", type=int, default=512)
+    ap.add_argument("--cpu-symbols", type=int, default=1 << 13)
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        impl_reference(args)
+        return
+
+    import torch
+    import torch.distributed as dist
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    import paper_2405_04253_b200 as P
+    from paper_2405_04253_b200 import _lib
+    from paper_2405_04253_b200.linkgen import DeviceLinkGenerator
+    from paper_2405_04253_b200.stream import CdcAeqChain
+
+    cfg = _link_cfg(args)
+    fwd = _lib.AEQ_FWD_DIRECT if args.forward == "direct" else _lib.AEQ_FWD_FNT
+    eng = P.FntCdcEngine(cfg.cdc_config("fnt"), cfg.sig_spec())
+    L = 2 * args.symbols
+    gen = DeviceLinkGenerator(args.symbols, z_km=cfg.z_km, sig_scale=cfg.sig_scale)
+    xr, xi = gen.generate(args.links, seed=4 + 7919 * rank)
+    chain = CdcAeqChain(eng, cfg.aeq_config(), args.links, L, cfg.sig_spec(), cfg.mu_schedule(),
+                        forward=fwd)
+    torch.cuda.synchronize()
+
+    # instrumented step: events around the two heavy kernels on the launching stream
+    ev = []
+
+    def step(record: bool):
+        s = torch.cuda.current_stream()
+        if record:
+            e = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+            chain.aeq.reset()
+            chain.acc.zero_()
+            e[0].record(s)
+            chain.cdc.run(xr, xi, length=L, qr=chain.qr, qi=chain.qi, q_spec=chain.sig_spec,
+                          decim_acc=chain.acc)
+            e[1].record(s)
+            from paper_2405_04253_b200.stream import decimation_phase
+            decimation_phase(chain.acc, chain.n_links, L, chain.phase, chain.gap)
+            e[2].record(s)
+            chain.aeq.run_decim(chain.qr, chain.qi, chain.phase, chain.n_blocks, chain.y,
+                                adapt=True, mu_blocks=chain.mu_blocks, err=chain.err)
+            e[3].record(s)
+            ev.append(e)
+        else:
+            chain.run(xr, xi)
+
+    for _ in range(args.warmup):
+        step(False)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clocks = ClockSampler(local)
+    clocks.start()
+    t_start = torch.cuda.Event(enable_timing=True)
+    t_end = torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    t_start.record()
+    for _ in range(args.steps):
+        step(True)
+    t_end.record()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clk = clocks.stop()
+    ms = t_start.elapsed_time(t_end)
+    cdc_ms = float(np.mean([e[0].elapsed_time(e[1]) for e in ev]))
+    ph_ms = float(np.mean([e[1].elapsed_time(e[2]) for e in ev]))
+    aeq_ms = float(np.mean([e[2].elapsed_time(e[3]) for e in ev]))
+    samples_rank = args.steps * args.links * 2 * L
+    if world > 1:
+        t = torch.tensor([ms, float(samples_rank)], dtype=torch.float64, device="cuda")
+        mx = t.clone()
+        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        ms_max, samples_all = float(mx[0]), float(t[1])
+    else:
+        ms_max, samples_all = ms, float(samples_rank)
+    value = samples_all / (ms_max * 1e-3) / 1e9
+
+    # sanity on the outputs of the last step (cheap): finite, phase decided
+    ok = bool(torch.isfinite(chain.y).all().item())
+
+    peaks = measured_peaks()
+    n_blk_cdc = 2 * args.links * (L // 32 + 1)
+    n_blk_aeq = args.links * chain.n_blocks
+    cdc_tops = n_blk_cdc * CDC_INT_OPS_PER_BLOCK / (cdc_ms * 1e-3) / 1e12
+    aeq_int = AEQ_INT_OPS_PER_BLOCK_FNT if fwd == _lib.AEQ_FWD_FNT else AEQ_INT_OPS_PER_BLOCK_DIRECT
+    aeq_tops = n_blk_aeq * aeq_int / (aeq_ms * 1e-3) / 1e12
+    aeq_fp64 = n_blk_aeq * AEQ_FP64_OPS_PER_BLOCK / (aeq_ms * 1e-3) / 1e12
+    cdc_bytes = 2 * args.links * L * (2 + 2)  # int8 I/Q in, int8 requantized I/Q out
+    aeq_bytes = args.links * (4 * 2 * (2 * chain.n_blocks * 16) // 2 + 4 * 8 * chain.n_blocks * 16)
+    traffic = None
+    ncu = PROFILES / "ncu_summary_r01.json"
+    if ncu.exists():
+        try:
+            traffic = json.loads(ncu.read_text()).get("per_launch_dram_bytes", {})
+        except Exception:
+            traffic = None
+    kernels = {
+        "k_cdc64": {"ms": cdc_ms, "bound": "int", "achieved": cdc_tops, "peak": peaks["int_tops"],
+                    "unit": "Tops/s", "frac": cdc_tops / peaks["int_tops"],
+                    "alg_ops_per_launch": n_blk_cdc * CDC_INT_OPS_PER_BLOCK,
+                    "hbm_gbs": cdc_bytes / (cdc_ms * 1e-3) / 1e9},
+        "k_aeq_process": {"ms": aeq_ms, "bound": "int", "achieved": aeq_tops,
+                          "peak": peaks["int_tops"], "unit": "Tops/s",
+                          "frac": aeq_tops / peaks["int_tops"],
+                          "alg_ops_per_launch": n_blk_aeq * aeq_int,
+                          "fp64_tinst_per_s": aeq_fp64,
+                          "fp64_frac": aeq_fp64 / peaks["fp64_tinst"],
+                          "hbm_gbs": aeq_bytes / (aeq_ms * 1e-3) / 1e9},
+        "k_decim_phase": {"ms": ph_ms},
+    }
+    dom = "k_aeq_process" if aeq_ms >= cdc_ms else "k_cdc64"
+    kd = kernels[dom]
+    tr = None
+    if isinstance(traffic, dict) and dom in traffic:
+        tr = traffic[dom]
+    roofline = {"bound": kd["bound"], "kernel": dom, "achieved": kd["achieved"], "peak": kd["peak"],
+                "unit": kd["unit"], "frac": kd["frac"], "traffic": tr,
+                "peak_source": peaks["int_source"],
+                "step_share": kd["ms"] / (cdc_ms + ph_ms + aeq_ms),
+                "kernels": kernels,
+                "hbm": {"achieved_gbs": (cdc_bytes + aeq_bytes) / ((cdc_ms + aeq_ms) * 1e-3) / 1e9,
+                        "peak_gbs": peaks["hbm_gbs"]}}
+
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "int32 (Z/(2^32-1) residues) + f64",
+        "data": "synthetic (on-device 16QAM link model, seeded)", "config": _config_dict(args),
+        "roofline": roofline, "clocks": clk, "gpu_launches": 4 * args.steps,
+        "outputs_finite": ok,
+    }
+
+    # end-to-end through the public host API: pinned host int8 in, float64 AEQ y out
+    if not args.no_e2e:
+        line["e2e"] = run_e2e(args, eng, cfg, xr, xi, fwd, world)
+
+    if rank == 0 and world == 1 and not args.no_cpu:
+        line["cpu_baseline"] = run_cpu_baseline(eng, cfg, args.cpu_symbols, os.cpu_count() or 1)
+    if rank == 0:
+        print(json.dumps(line))
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def run_e2e(args, eng, cfg, xr, xi, fwd, world):
+    import torch
+    import torch.distributed as dist
+    from paper_2405_04253_b200.stream import HostChain
+    n = min(args.e2e_links, args.links)
+    L = 2 * args.symbols
+    hc = HostChain(eng, cfg.aeq_config(), n, L, cfg.sig_spec(), cfg.mu_schedule(), forward=fwd)
+    hx_r = torch.empty((2 * n, L), dtype=torch.int8, pin_memory=True)
+    hx_i = torch.empty((2 * n, L), dtype=torch.int8, pin_memory=True)
+    hx_r.copy_(xr[:2 * n])
+    hx_i.copy_(xi[:2 * n])
+    for _ in range(min(args.warmup, 2)):
+        hc(hx_r, hx_i)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    a = torch.cuda.Event(enable_timing=True)
+    b = torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(args.steps):
+        hc(hx_r, hx_i)
+    b.record()
+    torch.cuda.synchronize()
+    ms = a.elapsed_time(b)
+    if world > 1:
+        t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t[0])
+    samples = args.steps * n * 2 * L * world
+    return {"value": samples / (ms * 1e-3) / 1e9, "unit": UNIT,
+            "h2d_bytes_per_step": hc.h2d_bytes, "d2h_bytes_per_step": hc.d2h_bytes,
+            "links_per_gpu": n,
+            "path": "paper_2405_04253_b200.stream.HostChain: pinned host int8 I/Q -> H2D -> "
+                    "CDC -> phase -> AEQ -> D2H float64 y + err_trace, every step"}
+
+
+if __name__ == "__main__":
+    main()

@@ -179,6 +179,8 @@ class CdcAeqChain:
                  sig_spec, mu_schedule=None, forward: int | None = None, keep_cdc_int=False):
         t = _t()
         dev = _lib.device()
+        if length % 2:
+            raise NotImplementedError("the chain runs 2 sps streams of even length")
         self.cdc = CdcBank(engine)
         self.n_links = n_links
         self.L = length
@@ -216,3 +218,31 @@ class CdcAeqChain:
         decimation_phase(self.acc, self.n_links, self.L, self.phase, self.gap, stream=stream)
         self.aeq.run_decim(self.qr, self.qi, self.phase, self.n_blocks, self.y, adapt=True,
                            mu_blocks=self.mu_blocks, err=self.err, stream=stream)
+
+
+class HostChain:
+    """The receiver chain as a host-facing call: pinned host int8 I/Q in,
+    float64 AEQ outputs and err_trace out (what a user of the reference's
+    rx_frontend + run_single glue gets back), every call moving the data over
+    PCIe. Used for the end-to-end measurement."""
+
+    def __init__(self, engine: FntCdcEngine, aeq_config: AeqConfig, n_links: int, length: int,
+                 sig_spec, mu_schedule=None, forward: int | None = None):
+        t = _t()
+        dev = _lib.device()
+        self.chain = CdcAeqChain(engine, aeq_config, n_links, length, sig_spec, mu_schedule,
+                                 forward)
+        self.dxr = t.empty((2 * n_links, length), dtype=t.int8, device=dev)
+        self.dxi = t.empty_like(self.dxr)
+        self.y = t.empty(tuple(self.chain.y.shape), dtype=t.float64, pin_memory=True)
+        self.err = t.empty(tuple(self.chain.err.shape), dtype=t.float64, pin_memory=True)
+        self.h2d_bytes = 2 * self.dxr.numel()
+        self.d2h_bytes = 8 * (self.y.numel() + self.err.numel())
+
+    def __call__(self, xr_host, xi_host):
+        self.dxr.copy_(xr_host, non_blocking=True)
+        self.dxi.copy_(xi_host, non_blocking=True)
+        self.chain.run(self.dxr, self.dxi)
+        self.y.copy_(self.chain.y, non_blocking=True)
+        self.err.copy_(self.chain.err, non_blocking=True)
+        return self.y, self.err

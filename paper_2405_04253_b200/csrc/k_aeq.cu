@@ -7,16 +7,19 @@
 // taps is strictly sequential, aeq.py:182-189). Lane = 8 s + 2 t + g with
 //   s = output stream, t = input stream, g = tap group (hi/lo) in the forward
 //   path and tap half (k in [8g, 8g+8)) in the update.
-// Taps (float w and 14-bit w_int), the overlap history and the per-lane FNT
-// arrays live in registers across all blocks; lane exchanges go through a small
-// per-warp shared-memory scratch with __syncwarp.
+// Taps (float w and 14-bit w_int) live in registers across all blocks. Inputs
+// arrive two samples per lane per block (lane L loads samples 2(L&7), 2(L&7)+1 of
+// input stream L>>3, one block ahead) into per-warp shared rings of the block's
+// integers and of x / sig_scale, so no lane ever indexes registers dynamically.
 //
-// Forward path, FNTGPU_AEQ_FWD_FNT (aeq.py:118-144): lane (s,t,g) transforms the
-//   32-sample block of input stream t (FNT-32, alpha = 2, rotates in Z/(2^32-1)),
-//   transforms its 16-tap group padded to 32 (first DIT stage free), multiplies
-//   pointwise (the 32 general products of that filter group), runs the inverse
-//   pruned to outputs 16..31 and decodes -- the reference's residue convolution
-//   per (group, s, t); recombine 128*hi + lo and sum over t, g.
+// Forward path, FNTGPU_AEQ_FWD_FNT (aeq.py:118-144): the four 32-point input
+//   transforms are computed cooperatively by the warp in shared memory (2
+//   butterflies per lane per stage); lane (s,t,g) transforms its 16-tap group
+//   padded to 32 in registers (first DIT stage free), multiplies pointwise (the 32
+//   general products of that filter group), runs the inverse pruned to outputs
+//   16..31 and decodes -- the reference's residue convolution per (group, s, t);
+//   recombine 128*hi + lo and sum over t, g. All transforms: alpha = 2, rotates
+//   in Z/(2^32-1) (fermat.cuh).
 // Forward path, FNTGPU_AEQ_FWD_DIRECT: the same integer per-group sums computed
 //   as a time-domain FIR (each group sum reduced mod F4 and decoded exactly as the
 //   residue path, so the bits are identical for every input the reference accepts).
@@ -35,26 +38,29 @@ constexpr int AEQ_WARPS = 4;         // streams per CTA
 constexpr int AEQ_TAP_MAX = 16383;   // TAP_MAG_MAX (aeq.py:26)
 constexpr int XF_LUT = 127;          // x / sig_scale table for |x| <= 127
 
-struct AeqScratch {
-  int32_t part[32][32];     // per-lane partial sums (direct: 16 hi + 16 lo; fnt: 16)
-  double ey[4][AEQ_L];      // e * y per output stream
-  double xf[4][2][AEQ_L];   // x / sig_scale ring: [t][block parity][j]
-  double err[32];           // |e| values for the err_trace mean
+struct __align__(16) AeqScratch {
+  int32_t part[32][32];       // per-lane partial sums (direct: 16 hi + 16 lo; fnt: 16)
+  double ey[4][AEQ_L];        // e * y per output stream
+  double xf[4][2][AEQ_L];     // x / sig_scale ring: [t][block parity][j]
+  int32_t xi[4][2][AEQ_L];    // input integer ring: [t][block parity][j]
+  uint32_t X[4][AEQ_N];       // cooperative input spectra (FNT path)
+  double err[32];             // |e| values for the err_trace mean
 };
 
 struct AeqArgs {
   fntgpu_aeq_params prm;
   fntgpu_aeq_io io;
-  double R2[8];             // radii[i] * radii[i] (nearest ** 2, aeq.py:58)
-  double D;                 // sig_scale * tap_scale (aeq.py:142)
+  double R2[8];               // radii[i] * radii[i] (nearest ** 2, aeq.py:58)
+  double D;                   // sig_scale * tap_scale (aeq.py:142)
 };
 
 __device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a, b); }
 __device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a, b); }
 __device__ __forceinline__ double dsub(double a, double b) { return __dsub_rn(a, b); }
 
-__device__ __forceinline__ int32_t sext8(uint32_t w, int k) {
-  return (int32_t)(w << (24 - 8 * k)) >> 24;
+// sign-extended byte k (0..3, may be a runtime value) of w
+__device__ __forceinline__ int32_t sbyte(uint32_t w, uint32_t k) {
+  return (int32_t)(w << (24u - 8u * k)) >> 24;
 }
 
 // split_taps (fixedpoint.py:111-121): sign * (|w| >> 7) or sign * (|w| & 127)
@@ -70,11 +76,17 @@ __device__ __forceinline__ double rde(double yi, double yq, const AeqArgs& A) {
   const double r = __dsqrt_rn(r2);
   int best = 0;
   double bd = fabs(dsub(r, A.prm.radii[0]));
-  for (int i = 1; i < A.prm.n_radii; ++i) {
-    const double d = fabs(dsub(r, A.prm.radii[i]));
-    if (d < bd) { bd = d; best = i; }  // np.argmin: first minimum
+#pragma unroll
+  for (int i = 1; i < 8; ++i) {
+    if (i < A.prm.n_radii) {
+      const double d = fabs(dsub(r, A.prm.radii[i]));
+      if (d < bd) { bd = d; best = i; }  // np.argmin: first minimum
+    }
   }
-  return dsub(A.R2[best], r2);
+  double R2 = A.R2[0];
+#pragma unroll
+  for (int i = 1; i < 8; ++i) R2 = best == i ? A.R2[i] : R2;
+  return dsub(R2, r2);
 }
 
 // einsum("sm,tmk->stk") inner reduction over m in numpy's SSE2 order.
@@ -90,22 +102,21 @@ __device__ __forceinline__ double einsum_m(const double (&P)[AEQ_L]) {
   return dadd(c0, c1);
 }
 
-// x / sig_scale exactly as numpy's true_divide (IEEE), via a table for |x| <= 127.
+// x / sig_scale exactly as numpy's true_divide (IEEE). Inputs narrower than 16 bits
+// always hit the table; wider ones fall back to the division.
+template <bool NARROW>
 __device__ __forceinline__ double xf_of(int32_t x, const double* lut, double sig) {
+  if (NARROW) return lut[x + XF_LUT];
   return (x >= -XF_LUT && x <= XF_LUT) ? lut[x + XF_LUT] : __ddiv_rn((double)x, sig);
 }
 
-// Lane-level block update (aeq.py:148-170) shared by process and update_taps.
-// Inputs: this lane's y0,y1 (= y[s][m0], y[s][m0+1]) and the scratch holding xf[t]
-// for the block (slot layout given by cur/prev). Returns |e| contributions via
-// scratch and updates the lane's 8 taps.
 struct LaneTaps {
   double w[8];
   int32_t wi[8];
   long long sat;
 };
 
-// Exchange the e values, compute err mean (written by lane 0 to *err_out when
+// Exchange the e values, compute the err_trace mean (lane 0 writes *err_out when
 // non-null) and, when mu != 0, the float update of this lane's 8 taps.
 __device__ __forceinline__ void lane_update(const AeqArgs& A, AeqScratch& S, int lane, int m0,
                                             double y0, double y1, int cur, double mu,
@@ -118,17 +129,16 @@ __device__ __forceinline__ void lane_update(const AeqArgs& A, AeqScratch& S, int
   const double e_other = __shfl_xor_sync(0xffffffffu, e_mine, 8);
   const double e0 = (s & 1) ? e_other : e_mine;  // e[p][m0]
   const double e1 = (s & 1) ? e_mine : e_other;  // e[p][m0 + 1]
-  // err_trace: mean(|e|) over (2 pols x 16) in numpy pairwise order
   if ((s & 1) == 0) {
     const int p = s >> 1;
     S.err[p * 16 + m0] = fabs(e0);
     S.err[p * 16 + m0 + 1] = fabs(e1);
   }
-  // ey for this lane's two outputs
   S.ey[s][m0] = dmul(e0, y0);
   S.ey[s][m0 + 1] = dmul(e1, y1);
   __syncwarp();
   if (err_out != nullptr) {
+    // np.mean(|e|) over (2 pols x 16): numpy pairwise order r[j] = a[j]+a[j+8]+a[j+16]+a[j+24]
     double r = 0.0;
     if (lane < 8) {
       r = dadd(dadd(dadd(S.err[lane], S.err[lane + 8]), S.err[lane + 16]), S.err[lane + 24]);
@@ -152,7 +162,7 @@ __device__ __forceinline__ void lane_update(const AeqArgs& A, AeqScratch& S, int
     }
 #pragma unroll
     for (int kk = 0; kk < 8; ++kk) {
-      // k = 8g + kk ; j = 16 + m - k = 16 + m - 8g - kk ; q = j - (9 - 8g) = 7 + m - kk
+      // k = 8g + kk ; j = 16 + m - k ; q = j - (9 - 8g) = 7 + m - kk
       double P[AEQ_L];
 #pragma unroll
       for (int m = 0; m < AEQ_L; ++m) P[m] = dmul(ey[m], xf[7 + m - kk]);
@@ -170,30 +180,69 @@ __device__ __forceinline__ void lane_update(const AeqArgs& A, AeqScratch& S, int
   __syncwarp();
 }
 
+// Cooperative 32-point forward transforms of the four input streams' blocks
+// x_block[t] = [ring prev | ring cur] into S.X[t][k] (natural order), 2
+// butterflies per lane per stage, twiddles 2^e as runtime rotates.
+__device__ __forceinline__ void warp_input_fnt(AeqScratch& S, int lane, int cur) {
+  const int prev = cur ^ 1;
+  {
+    const int tq = lane >> 3;
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const int p = 4 * (lane & 7) + r;           // bit-reversed position
+      const int i = (int)(__brev((unsigned)p) >> 27);  // natural index
+      const int32_t v = i < AEQ_L ? S.xi[tq][prev][i] : S.xi[tq][cur][i - AEQ_L];
+      S.X[tq][p] = f4_enc_small(v);
+    }
+  }
+  __syncwarp();
+#pragma unroll
+  for (int st = 0; st < 5; ++st) {
+    const int half = 1 << st;
+    const int step = AEQ_N >> (st + 1);
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int q = lane + 32 * h;                // 64 butterflies: 4 streams x 16
+      const int tt = q >> 4, j2 = q & 15;
+      const int j = j2 & (half - 1);
+      const int i0 = (j2 >> st) * 2 * half + j;
+      const uint32_t u = S.X[tt][i0], v = S.X[tt][i0 + half];
+      const int e = (j * step) & 31;              // alpha^e = 2^e ; 2^16 = -1
+      uint32_t w = __funnelshift_l(v, v, e & 15);
+      w = (e & 16) ? ~w : w;                      // negate = one's complement in Z/M
+      S.X[tt][i0] = m_add(u, w);
+      S.X[tt][i0 + half] = m_sub(u, w);
+    }
+    __syncwarp();
+  }
+}
+
 // Forward path for one block: returns y_int[s][m0], y_int[s][m0+1] in yi0, yi1.
-// xb holds this lane's input stream t block (32 ints: history | new).
 template <int FWD>
-__device__ __forceinline__ void lane_forward(AeqScratch& S, int lane, const int32_t (&xb)[AEQ_N],
-                                             const LaneTaps& T, int m0, int32_t& yi0,
-                                             int32_t& yi1) {
-  const int s = lane >> 3, g = lane & 1;
+__device__ __forceinline__ void lane_forward(AeqScratch& S, int lane, int cur, const LaneTaps& T,
+                                             int m0, int32_t& yi0, int32_t& yi1) {
+  const int s = lane >> 3, t = (lane >> 1) & 3, g = lane & 1;
   if (FWD == FNTGPU_AEQ_FWD_FNT) {
+    warp_input_fnt(S, lane, cur);
     // all 16 taps of filter (s, t): own 8 + partner's 8 (lane ^ 1 holds the other half)
-    int32_t taps[AEQ_L];
+    uint32_t W[AEQ_N];
 #pragma unroll
     for (int kk = 0; kk < 8; ++kk) {
       const int32_t other = __shfl_xor_sync(0xffffffffu, T.wi[kk], 1);
-      taps[kk] = g == 0 ? T.wi[kk] : other;
-      taps[8 + kk] = g == 0 ? other : T.wi[kk];
+      const int32_t lo8 = g == 0 ? T.wi[kk] : other;   // tap kk
+      const int32_t hi8 = g == 0 ? other : T.wi[kk];   // tap 8 + kk
+      W[bitrev(kk, 5)] = f4_enc_small(tap_group(lo8, g));
+      W[bitrev(8 + kk, 5)] = f4_enc_small(tap_group(hi8, g));
     }
-    uint32_t X[AEQ_N], W[AEQ_N];
 #pragma unroll
-    for (int i = 0; i < AEQ_N; ++i) X[bitrev(i, 5)] = f4_enc_small(xb[i]);
-#pragma unroll
-    for (int k = 0; k < AEQ_N; ++k)
-      W[bitrev(k, 5)] = k < AEQ_L ? f4_enc_small(tap_group(taps[k], g)) : 0u;
-    fnt_dit<AEQ_N, RADIX2, false>(X);
+    for (int k = AEQ_L; k < AEQ_N; ++k) W[bitrev(k, 5)] = 0u;
     fnt_dit<AEQ_N, RADIX2, false, true>(W);  // taps zero-padded: first stage is a copy
+    uint32_t X[AEQ_N];
+#pragma unroll
+    for (int q = 0; q < AEQ_N / 4; ++q) {
+      const uint4 v = reinterpret_cast<const uint4*>(S.X[t])[q];
+      X[4 * q] = v.x; X[4 * q + 1] = v.y; X[4 * q + 2] = v.z; X[4 * q + 3] = v.w;
+    }
 #pragma unroll
     for (int k = 0; k < AEQ_N; ++k) X[k] = m_mul(X[k], W[k]);  // 32 general products
     to_bitrev<AEQ_N>(X);
@@ -207,12 +256,22 @@ __device__ __forceinline__ void lane_forward(AeqScratch& S, int lane, const int3
     int32_t a0 = 0, a1 = 0;
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
-      a0 += S.part[s * 8 + q][m0];
-      a1 += S.part[s * 8 + q][m0 + 1];
+      const int2 v = *reinterpret_cast<const int2*>(&S.part[s * 8 + q][m0]);
+      a0 += v.x;
+      a1 += v.y;
     }
     yi0 = a0;
     yi1 = a1;
   } else {
+    int32_t xb[AEQ_N];
+    const int prev = cur ^ 1;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int4 a = reinterpret_cast<const int4*>(S.xi[t][prev])[q];
+      const int4 b = reinterpret_cast<const int4*>(S.xi[t][cur])[q];
+      xb[4 * q] = a.x; xb[4 * q + 1] = a.y; xb[4 * q + 2] = a.z; xb[4 * q + 3] = a.w;
+      xb[16 + 4 * q] = b.x; xb[16 + 4 * q + 1] = b.y; xb[16 + 4 * q + 2] = b.z; xb[16 + 4 * q + 3] = b.w;
+    }
     // time-domain per-group partial sums over this lane's 8 taps k = 8g + kk
     int32_t hi[AEQ_L], lo[AEQ_L];
 #pragma unroll
@@ -235,16 +294,14 @@ __device__ __forceinline__ void lane_forward(AeqScratch& S, int lane, const int3
 #pragma unroll
     for (int tt = 0; tt < 4; ++tt) {
       const int l0 = s * 8 + tt * 2;
-#pragma unroll
-      for (int r = 0; r < 2; ++r) {
-        const int m = m0 + r;
-        const int32_t sh = S.part[l0][m] + S.part[l0 + 1][m];
-        const int32_t sl = S.part[l0][AEQ_L + m] + S.part[l0 + 1][AEQ_L + m];
-        // each group convolution is a residue mod F4, decoded (aeq.py:139-140)
-        const int32_t v = 128 * f4_signed((uint32_t)(sh + (int32_t)(F4 * 1024u))) +
-                          f4_signed((uint32_t)(sl + (int32_t)(F4 * 1024u)));
-        if (r == 0) a0 += v; else a1 += v;
-      }
+      const int2 h0 = *reinterpret_cast<const int2*>(&S.part[l0][m0]);
+      const int2 h1 = *reinterpret_cast<const int2*>(&S.part[l0 + 1][m0]);
+      const int2 l0v = *reinterpret_cast<const int2*>(&S.part[l0][AEQ_L + m0]);
+      const int2 l1v = *reinterpret_cast<const int2*>(&S.part[l0 + 1][AEQ_L + m0]);
+      // each group convolution is a residue mod F4, decoded (aeq.py:139-140)
+      const int32_t B = (int32_t)(F4 * 1024u);
+      a0 += 128 * f4_signed((uint32_t)(h0.x + h1.x + B)) + f4_signed((uint32_t)(l0v.x + l1v.x + B));
+      a1 += 128 * f4_signed((uint32_t)(h0.y + h1.y + B)) + f4_signed((uint32_t)(l0v.y + l1v.y + B));
     }
     yi0 = a0;
     yi1 = a1;
@@ -258,6 +315,7 @@ __device__ __forceinline__ void lane_forward(AeqScratch& S, int lane, const int3
 template <int FWD, int IN_MODE, typename TIN>
 __global__ void __launch_bounds__(AEQ_WARPS * 32) k_aeq_process(fntgpu_aeq_state* __restrict__ st,
                                                                  const __grid_constant__ AeqArgs A) {
+  constexpr bool NARROW = sizeof(TIN) == 1;
   __shared__ AeqScratch scratch[AEQ_WARPS];
   __shared__ double lut[2 * XF_LUT + 1];
   for (int i = threadIdx.x; i < 2 * XF_LUT + 1; i += blockDim.x)
@@ -274,6 +332,8 @@ __global__ void __launch_bounds__(AEQ_WARPS * 32) k_aeq_process(fntgpu_aeq_state
   const int s = lane >> 3, t = (lane >> 1) & 3, g = lane & 1;
   const int j8 = lane & 7;  // m0 = 8*b0 + 4*b1 + 2*b2 with (b2 b1 b0) = lane bits 2,1,0
   const int m0 = 8 * (j8 & 1) + 4 * ((j8 >> 1) & 1) + 2 * ((j8 >> 2) & 1);
+  // input-loader role: samples iq, iq + 1 of input stream tq
+  const int tq = lane >> 3, iq = 2 * (lane & 7);
 
   LaneTaps T;
 #pragma unroll
@@ -282,70 +342,68 @@ __global__ void __launch_bounds__(AEQ_WARPS * 32) k_aeq_process(fntgpu_aeq_state
     T.wi[kk] = state.w_int[s][t][8 * g + kk];
   }
   T.sat = 0;
-  int32_t xb[AEQ_N];
-#pragma unroll
-  for (int i = 0; i < AEQ_L; ++i) xb[AEQ_L + i] = state.hist[t][i];
-  // xf ring: slot 1 holds the history (block -1), slot 0 receives block 0
-  if (s == 0 && g == 0) {
-#pragma unroll
-    for (int i = 0; i < AEQ_L; ++i) S.xf[t][1][i] = xf_of(xb[AEQ_L + i], lut, A.prm.sig_scale);
+  // history -> ring slot 1 (the slot block 0 treats as "previous")
+  {
+    const int32_t h0 = state.hist[tq][iq], h1 = state.hist[tq][iq + 1];
+    S.xi[tq][1][iq] = h0;
+    S.xi[tq][1][iq + 1] = h1;
+    S.xf[tq][1][iq] = xf_of<false>(h0, lut, A.prm.sig_scale);
+    S.xf[tq][1][iq + 1] = xf_of<false>(h1, lut, A.prm.sig_scale);
   }
-  __syncwarp();
 
-  // input row pointer for this lane's stream t
-  const TIN* xrow = nullptr;
-  int phase = 0;
+  // this lane's input row (stream tq) and a one-block-ahead prefetch of its 2 samples
+  const char* row;
+  uint32_t sel0 = 0, sel1 = 1;
   if (IN_MODE == FNTGPU_AEQ_IN_PLANAR) {
-    xrow = reinterpret_cast<const TIN*>(io.x) + S_idx * io.x_stream_stride + t * io.x_row_stride;
+    row = reinterpret_cast<const char*>(reinterpret_cast<const TIN*>(io.x) + S_idx * io.x_stream_stride +
+                                        tq * io.x_row_stride);
   } else {
-    const int8_t* plane = (t & 1) ? io.qi : io.qr;
-    xrow = reinterpret_cast<const TIN*>(plane + (2 * S_idx + (t >> 1)) * io.q_stride);
-    phase = io.phase[S_idx];
+    const int8_t* plane = (tq & 1) ? io.qi : io.qr;
+    row = reinterpret_cast<const char*>(plane + (2 * S_idx + (tq >> 1)) * io.q_stride);
+    const uint32_t ph = (uint32_t)io.phase[S_idx];
+    sel0 = ph;       // byte of symbol iq within the 4-byte word (2 iq .. 2 iq + 3)
+    sel1 = 2 + ph;   // byte of symbol iq + 1
   }
-
-  auto load_new = [&](int64_t b, int32_t (&v)[AEQ_L]) {
-    if (IN_MODE == FNTGPU_AEQ_IN_PLANAR) {
-      if (sizeof(TIN) == 1) {
-        const uint4 w = *reinterpret_cast<const uint4*>(xrow + b * AEQ_L);
-        const uint32_t ww[4] = {w.x, w.y, w.z, w.w};
-#pragma unroll
-        for (int i = 0; i < AEQ_L; ++i) v[i] = sext8(ww[i >> 2], i & 3);
-      } else {
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const int4 w = *reinterpret_cast<const int4*>(xrow + b * AEQ_L + 4 * q);
-          v[4 * q] = w.x; v[4 * q + 1] = w.y; v[4 * q + 2] = w.z; v[4 * q + 3] = w.w;
-        }
-      }
+  auto fetch = [&](int64_t b) -> uint2 {
+    if (IN_MODE == FNTGPU_AEQ_IN_DECIM) {
+      return make_uint2(__ldg(reinterpret_cast<const uint32_t*>(row + b * 2 * AEQ_L + 2 * iq)), 0u);
+    } else if (NARROW) {
+      return make_uint2(__ldg(reinterpret_cast<const uint16_t*>(row + b * AEQ_L + iq)), 0u);
     } else {
-      const uint4 w0 = *reinterpret_cast<const uint4*>(xrow + b * 2 * AEQ_L);
-      const uint4 w1 = *reinterpret_cast<const uint4*>(xrow + b * 2 * AEQ_L + 16);
-      const uint32_t ww[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
-#pragma unroll
-      for (int i = 0; i < AEQ_L; ++i) {
-        const int byte = 2 * i;  // + phase
-        v[i] = phase ? sext8(ww[(byte + 1) >> 2], (byte + 1) & 3) : sext8(ww[byte >> 2], byte & 3);
-      }
+      const int2 v = __ldg(reinterpret_cast<const int2*>(row + 4 * (b * AEQ_L + iq)));
+      return make_uint2((uint32_t)v.x, (uint32_t)v.y);
+    }
+  };
+  auto decode = [&](uint2 raw, int32_t& v0, int32_t& v1) {
+    if (IN_MODE == FNTGPU_AEQ_IN_DECIM) {
+      v0 = sbyte(raw.x, sel0);
+      v1 = sbyte(raw.x, sel1);
+    } else if (NARROW) {
+      v0 = sbyte(raw.x, 0);
+      v1 = sbyte(raw.x, 1);
+    } else {
+      v0 = (int32_t)raw.x;
+      v1 = (int32_t)raw.y;
     }
   };
 
   const double D = A.D;
-  int32_t nxt[AEQ_L];
-  if (io.n_blocks > 0) load_new(0, nxt);
+  int32_t v0 = 0, v1 = 0;
+  uint2 raw = make_uint2(0u, 0u);
+  if (io.n_blocks > 0) raw = fetch(0);
   for (int64_t b = 0; b < io.n_blocks; ++b) {
-    // shift: x_block = [history | new]
-#pragma unroll
-    for (int i = 0; i < AEQ_L; ++i) { xb[i] = xb[AEQ_L + i]; xb[AEQ_L + i] = nxt[i]; }
-    if (b + 1 < io.n_blocks) load_new(b + 1, nxt);  // prefetch the next block
     const int cur = (int)(b & 1);
-    if (io.adapt && s == 0 && g == 0) {
-      // x_block / sig_scale for the new half of stream t (aeq.py:154); the history
-      // half was converted one block earlier and sits in the other ring slot
-#pragma unroll
-      for (int i = 0; i < AEQ_L; ++i) S.xf[t][cur][i] = xf_of(xb[AEQ_L + i], lut, A.prm.sig_scale);
+    decode(raw, v0, v1);
+    if (b + 1 < io.n_blocks) raw = fetch(b + 1);  // one block ahead
+    S.xi[tq][cur][iq] = v0;
+    S.xi[tq][cur][iq + 1] = v1;
+    if (io.adapt) {
+      S.xf[tq][cur][iq] = xf_of<NARROW>(v0, lut, A.prm.sig_scale);
+      S.xf[tq][cur][iq + 1] = xf_of<NARROW>(v1, lut, A.prm.sig_scale);
     }
+    __syncwarp();
     int32_t yi0, yi1;
-    lane_forward<FWD>(S, lane, xb, T, m0, yi0, yi1);
+    lane_forward<FWD>(S, lane, cur, T, m0, yi0, yi1);
     const double y0 = __ddiv_rn((double)yi0, D);  // y_int / (sig_scale * tap_scale)
     const double y1 = __ddiv_rn((double)yi1, D);
     double2* yrow = reinterpret_cast<double2*>(io.y + S_idx * io.y_stream_stride + s * io.y_row_stride + b * AEQ_L + m0);
@@ -363,9 +421,9 @@ __global__ void __launch_bounds__(AEQ_WARPS * 32) k_aeq_process(fntgpu_aeq_state
     state.w[s][t][8 * g + kk] = T.w[kk];
     state.w_int[s][t][8 * g + kk] = T.wi[kk];
   }
-  if (s == 0 && g == 0) {
-#pragma unroll
-    for (int i = 0; i < AEQ_L; ++i) state.hist[t][i] = xb[AEQ_L + i];
+  if (io.n_blocks > 0) {
+    state.hist[tq][iq] = v0;
+    state.hist[tq][iq + 1] = v1;
   }
   long long sat = T.sat;
 #pragma unroll
@@ -381,10 +439,6 @@ __global__ void __launch_bounds__(AEQ_WARPS * 32) k_aeq_process(fntgpu_aeq_state
 __global__ void k_aeq_update_once(fntgpu_aeq_state* st, const __grid_constant__ AeqArgs A,
                                   const int64_t* xblk, const double* y, double mu, double* err) {
   __shared__ AeqScratch S;
-  __shared__ double lut[2 * XF_LUT + 1];
-  for (int i = threadIdx.x; i < 2 * XF_LUT + 1; i += blockDim.x)
-    lut[i] = __ddiv_rn((double)(i - XF_LUT), A.prm.sig_scale);
-  __syncthreads();
   const int lane = threadIdx.x & 31;
   const int s = lane >> 3, t = (lane >> 1) & 3, g = lane & 1;
   const int j8 = lane & 7;

@@ -4,17 +4,18 @@
 // 141-156 (_convolve_blocks), 165-180 (process_int / process) and the CDC->AEQ glue
 // of linksim.py:283-308, 399-404 (float rescale, requantization, decimation metric).
 //
-// One thread owns one 64-sample overlap-save block (hop 32) and produces its 32
-// valid outputs; a CTA owns CDC_CTA consecutive blocks. Per thread:
-//   a+- = x_r +- 2^8 x_i (time domain, linearity of the FNT)         64 x 3 ops
-//   FNT-64(a+), FNT-64(a-)  radix-sqrt2 DIT, rotates in Z/(2^32-1)   2 x 192 butterflies
-//   u+- = a+- * b+-'   (b+- pre-scaled by c_re * N^-1 = 2^25)         128 products
-//   IFNT-64(u+), IFNT-64(u-) with the last stage pruned to outputs 32..63
-//   z_re = u+ + u-,  z_im = 2^24 (u+ - u-)   -> fold mod F4, signed decode
-// so the whole block is one HBM read of the input and one write of the output.
-// Inputs are staged into shared memory once per CTA (the 32-sample halo between
-// neighbouring blocks is read from shared memory, not re-fetched from HBM), and
-// outputs are staged so the global stores are contiguous across the CTA.
+// A CTA owns CDC_BLK = 64 consecutive 64-sample overlap-save blocks (hop 32) of one
+// stream. Each block is split over two threads in different warps (warp-uniform
+// sign, so the two halves of Eqs. (7)-(8) are branch-free):
+//   sign +: a+ = x_r + 2^8 x_i  ->  FNT-64  ->  * b+'  ->  IFNT-64 (outputs 32..63)
+//   sign -: a- = x_r - 2^8 x_i  ->  FNT-64  ->  * b-'  ->  IFNT-64 (outputs 32..63)
+// (b+- pre-scaled by c_re * N^-1 = 2^25; radix-sqrt2 DIT with rotate-only twiddles
+// in Z/(2^32-1), fermat.cuh). The epilogue combines z_re = u+ + u-,
+// z_im = 2^24 (u+ - u-), folds mod F4 and decodes, then streams the contiguous
+// output range of the CTA (and the fused requantization / decimation
+// statistics) with coalesced stores. One HBM read per input sample (the 32-sample
+// halo between neighbouring blocks is re-read from shared memory) and one HBM
+// write per output.
 #include <type_traits>
 
 #include "fermat.cuh"
@@ -22,10 +23,12 @@
 
 namespace fntgpu {
 
-constexpr int CDC_CTA = 128;
+constexpr int CDC_CTA = 128;                    // threads
+constexpr int CDC_BLK = 64;                     // overlap-save blocks per CTA
 constexpr int CDC_N = 64;
 constexpr int CDC_HOP = 32;
-constexpr int OUT_PITCH = 33;  // padded row pitch of the output staging tile (bank-conflict free)
+constexpr int WIN = CDC_HOP * (CDC_BLK + 1);    // input samples staged per plane
+constexpr int UP = 33;                          // padded pitch of the u staging rows
 
 struct CdcArgs {
   uint32_t bp[CDC_N];  // b+ * 2^25 mod F4
@@ -36,65 +39,80 @@ struct CdcArgs {
   int32_t c;           // n_taps // 2
 };
 
-template <typename T>
-__device__ __forceinline__ int32_t ld_in(const void* base, int64_t idx) {
-  return (int32_t)reinterpret_cast<const T*>(base)[idx];
-}
-
 __device__ __forceinline__ int32_t sext8(uint32_t w, int k) {
   return (int32_t)(w << (24 - 8 * k)) >> 24;
 }
 
-// Stage the CTA's input window [g0, g0 + n) of one plane into shared memory (zero
-// outside the stream [0, L)). TIN = int8 uses byte smem, wider inputs int32 smem.
+// Stage the CTA's input window [g0, g0 + WIN) of one plane into shared memory,
+// zero outside the stream [0, L). int8 planes move in 16-byte vectors.
 template <typename TIN, typename TS>
-__device__ __forceinline__ void stage_plane(TS* dst, const void* src, int64_t g0, int n,
+__device__ __forceinline__ void stage_plane(TS* dst, const TIN* src, int64_t g0,
                                             const fntgpu_cdc_io& io) {
-  for (int i = threadIdx.x; i < n; i += blockDim.x) {
-    const int64_t g = g0 + i;
-    int32_t v = 0;
-    if (g >= 0 && g < io.length) v = ld_in<TIN>(src, g - io.x_first);
-    dst[i] = (TS)v;
+  const int64_t lo = io.x_first > 0 ? io.x_first : 0;
+  const int64_t hi_avail = io.x_first + io.x_count;
+  const int64_t hi = hi_avail < io.length ? hi_avail : io.length;
+  if (sizeof(TIN) == 1) {
+    constexpr int CH = WIN / 16;
+    for (int ch = threadIdx.x; ch < CH; ch += blockDim.x) {
+      const int64_t g = g0 + 16 * ch;
+      const TIN* p = src + (g - io.x_first);
+      uint4 v;
+      if (g >= lo && g + 16 <= hi && ((reinterpret_cast<uintptr_t>(p) & 15) == 0)) {
+        v = __ldg(reinterpret_cast<const uint4*>(p));
+      } else {
+        uint32_t w[4] = {0u, 0u, 0u, 0u};
+        for (int k = 0; k < 16; ++k) {
+          const int64_t gk = g + k;
+          if (gk >= lo && gk < hi) w[k >> 2] |= ((uint32_t)(uint8_t)src[gk - io.x_first]) << (8 * (k & 3));
+        }
+        v = make_uint4(w[0], w[1], w[2], w[3]);
+      }
+      reinterpret_cast<uint4*>(dst)[ch] = v;
+    }
+  } else {
+    for (int i = threadIdx.x; i < WIN; i += blockDim.x) {
+      const int64_t g = g0 + i;
+      dst[i] = (g >= lo && g < hi) ? (TS)src[g - io.x_first] : (TS)0;
+    }
   }
 }
 
 template <typename TIN>
 __global__ void __launch_bounds__(CDC_CTA) k_cdc64(const __grid_constant__ CdcArgs A) {
   using TS = typename std::conditional<sizeof(TIN) == 1, int8_t, int32_t>::type;
-  constexpr int WIN = CDC_HOP * (CDC_CTA + 1);
   constexpr int IN_BYTES = 2 * WIN * (int)sizeof(TS);
-  constexpr int OUT_BYTES = 2 * CDC_CTA * OUT_PITCH * 4;
-  // input staging and output staging are never live at the same time: one buffer
-  __shared__ __align__(16) unsigned char smem[IN_BYTES > OUT_BYTES ? IN_BYTES : OUT_BYTES];
+  constexpr int U_BYTES = 2 * CDC_BLK * UP * 4;
+  // the input window and the u staging rows are never live at the same time
+  __shared__ __align__(16) unsigned char smem[IN_BYTES > U_BYTES ? IN_BYTES : U_BYTES];
   TS* s_xr = reinterpret_cast<TS*>(smem);
   TS* s_xi = s_xr + WIN;
-  int32_t* s_or = reinterpret_cast<int32_t*>(smem);
-  int32_t* s_oi = s_or + CDC_CTA * OUT_PITCH;
+  uint32_t* s_u = reinterpret_cast<uint32_t*>(smem);  // [sign][block][UP]
 
   const fntgpu_cdc_io& io = A.io;
   const int s = blockIdx.y;
-  const int64_t cta_blk0 = A.blk_begin + (int64_t)blockIdx.x * CDC_CTA;
+  const int64_t cta_blk0 = A.blk_begin + (int64_t)blockIdx.x * CDC_BLK;
   const int64_t g0 = cta_blk0 * CDC_HOP - CDC_HOP;  // first input sample of block cta_blk0
 
-  const int es = sizeof(TIN);
-  const char* xr_s = reinterpret_cast<const char*>(io.xr) + (size_t)s * io.x_stride * es;
-  const char* xi_s = reinterpret_cast<const char*>(io.xi) + (size_t)s * io.x_stride * es;
-  stage_plane<TIN, TS>(s_xr, xr_s, g0, WIN, io);
-  stage_plane<TIN, TS>(s_xi, xi_s, g0, WIN, io);
+  const TIN* xr_s = reinterpret_cast<const TIN*>(io.xr) + (size_t)s * io.x_stride;
+  const TIN* xi_s = reinterpret_cast<const TIN*>(io.xi) + (size_t)s * io.x_stride;
+  stage_plane<TIN, TS>(s_xr, xr_s, g0, io);
+  stage_plane<TIN, TS>(s_xi, xi_s, g0, io);
   __syncthreads();
 
   const int tid = threadIdx.x;
-  const bool active = cta_blk0 + tid < A.blk_begin + A.blk_count;
-  uint32_t ap[CDC_N], am[CDC_N];
+  const int warp = tid >> 5, lane = tid & 31;
+  const int sgn = warp & 1;                   // 0: a+ / b+, 1: a- / b-
+  const int bl = (warp >> 1) * 32 + lane;     // block within the CTA
+  const int32_t m256 = sgn ? -256 : 256;
+  uint32_t a[CDC_N];
   {
-    const TS* wr = s_xr + tid * CDC_HOP;
-    const TS* wi = s_xi + tid * CDC_HOP;
+    const TS* wr = s_xr + bl * CDC_HOP;
+    const TS* wi = s_xi + bl * CDC_HOP;
     if (sizeof(TS) == 1) {
-      const uint4* vr = reinterpret_cast<const uint4*>(wr);
-      const uint4* vi = reinterpret_cast<const uint4*>(wi);
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
-        const uint4 r4 = vr[q], i4 = vi[q];
+        const uint4 r4 = reinterpret_cast<const uint4*>(wr)[q];
+        const uint4 i4 = reinterpret_cast<const uint4*>(wi)[q];
         const uint32_t rw[4] = {r4.x, r4.y, r4.z, r4.w};
         const uint32_t iw[4] = {i4.x, i4.y, i4.z, i4.w};
 #pragma unroll
@@ -102,51 +120,33 @@ __global__ void __launch_bounds__(CDC_CTA) k_cdc64(const __grid_constant__ CdcAr
 #pragma unroll
           for (int k = 0; k < 4; ++k) {
             const int i = q * 16 + w * 4 + k;
-            const int32_t xr = sext8(rw[w], k), xi = sext8(iw[w], k);
-            const int32_t t = xr + (int32_t)F4_BIAS;
-            const uint32_t p = (uint32_t)(t + xi * 256);
-            ap[bitrev(i, 6)] = p;
-            am[bitrev(i, 6)] = (uint32_t)(2 * t) - p;  // x_r - 2^8 x_i + bias
+            // x_r +- 2^8 x_i + bias (bias = 256 F4 keeps the word non-negative)
+            a[bitrev(i, 6)] = (uint32_t)(sext8(rw[w], k) + (int32_t)F4_BIAS + m256 * sext8(iw[w], k));
           }
       }
     } else {
 #pragma unroll
-      for (int i = 0; i < CDC_N; ++i) {
-        const int32_t xr = (int32_t)wr[i], xi = (int32_t)wi[i];
-        const int32_t t = xr + (int32_t)F4_BIAS;
-        const uint32_t p = (uint32_t)(t + xi * 256);
-        ap[bitrev(i, 6)] = p;
-        am[bitrev(i, 6)] = (uint32_t)(2 * t) - p;
-      }
+      for (int i = 0; i < CDC_N; ++i)
+        a[bitrev(i, 6)] = (uint32_t)((int32_t)wr[i] + (int32_t)F4_BIAS + m256 * (int32_t)wi[i]);
     }
   }
-  __syncthreads();  // the input window is dead; smem is reused for the outputs
-  if (active) {
-    fnt_dit<CDC_N, SQRT2, false>(ap);
-    fnt_dit<CDC_N, SQRT2, false>(am);
+  fnt_dit<CDC_N, SQRT2, false>(a);
+  const uint32_t* B = sgn ? A.bm : A.bp;
 #pragma unroll
-    for (int k = 0; k < CDC_N; ++k) {
-      ap[k] = m_mul(ap[k], A.bp[k]);
-      am[k] = m_mul(am[k], A.bm[k]);
-    }
-    to_bitrev<CDC_N>(ap);
-    to_bitrev<CDC_N>(am);
-    fnt_dit<CDC_N, SQRT2, true, false, true>(ap);
-    fnt_dit<CDC_N, SQRT2, true, false, true>(am);
-    int32_t* orow = s_or + tid * OUT_PITCH;
-    int32_t* irow = s_oi + tid * OUT_PITCH;
+  for (int k = 0; k < CDC_N; ++k) a[k] = m_mul(a[k], B[k]);  // the 64 general products
+  to_bitrev<CDC_N>(a);
+  fnt_dit<CDC_N, SQRT2, true, false, true>(a);             // outputs 32..63 only
+  __syncthreads();  // every thread has consumed the input window
+  {
+    uint32_t* row = s_u + (sgn * CDC_BLK + bl) * UP;
 #pragma unroll
-    for (int j = 0; j < CDC_HOP; ++j) {
-      const uint32_t up = ap[CDC_HOP + j], um = am[CDC_HOP + j];
-      orow[j] = f4_signed(m_add(up, um));
-      irow[j] = f4_signed(m_rot(m_sub(up, um), 24));
-    }
+    for (int j = 0; j < CDC_HOP; ++j) row[j] = a[CDC_HOP + j];
   }
   __syncthreads();
 
-  // ---- epilogue: outputs of this CTA are global indices [32*cta_blk0 - c, ... + 32*CDC_CTA)
+  // ---- epilogue: outputs of this CTA are global indices [32*cta_blk0 - c, ... + 32*CDC_BLK)
   const int64_t n0 = cta_blk0 * CDC_HOP - A.c;
-  int64_t lo = n0, hi = n0 + (int64_t)CDC_CTA * CDC_HOP;
+  int64_t lo = n0, hi = n0 + (int64_t)CDC_BLK * CDC_HOP;
   const int64_t o_lo = io.out_first, o_hi = io.out_first + io.out_count;
   lo = lo < o_lo ? o_lo : lo;
   hi = hi > o_hi ? o_hi : hi;
@@ -155,8 +155,10 @@ __global__ void __launch_bounds__(CDC_CTA) k_cdc64(const __grid_constant__ CdcAr
   unsigned long long s2 = 0, s4lo = 0, s4hi = 0;
   for (int64_t n = lo + tid; n < hi; n += CDC_CTA) {
     const int idx = (int)(n - n0);
-    const int32_t zr = s_or[(idx >> 5) * OUT_PITCH + (idx & 31)];
-    const int32_t zi = s_oi[(idx >> 5) * OUT_PITCH + (idx & 31)];
+    const int r = (idx >> 5) * UP + (idx & 31);
+    const uint32_t up = s_u[r], um = s_u[CDC_BLK * UP + r];
+    const int32_t zr = f4_signed(m_add(up, um));
+    const int32_t zi = f4_signed(m_rot(m_sub(up, um), 24));
     const int64_t o = n - io.out_first;
     switch (io.out_dtype) {
       case FNTGPU_I16:
@@ -257,7 +259,7 @@ cudaError_t launch_cdc64(const fntgpu_cdc_taps& taps, const fntgpu_cdc_io& io, c
   const int64_t b_hi = (io.out_first + io.out_count - 1 + A.c) / CDC_HOP;
   A.blk_begin = b_lo;
   A.blk_count = b_hi - b_lo + 1;
-  dim3 grid((unsigned)((A.blk_count + CDC_CTA - 1) / CDC_CTA), (unsigned)io.n_streams);
+  dim3 grid((unsigned)((A.blk_count + CDC_BLK - 1) / CDC_BLK), (unsigned)io.n_streams);
   switch (io.in_dtype) {
     case FNTGPU_I8: k_cdc64<int8_t><<<grid, CDC_CTA, 0, st>>>(A); break;
     case FNTGPU_I32: k_cdc64<int32_t><<<grid, CDC_CTA, 0, st>>>(A); break;

@@ -17,7 +17,7 @@ from pathlib import Path
 import numpy as np
 
 _PKG = Path(__file__).resolve().parent
-LIB_PATH = _PKG / "libfntgpu.so"
+LIB_PATH = Path(os.environ.get("FNTGPU_LIB", str(_PKG / "libfntgpu.so")))  # override: A/B builds
 
 ABI_VERSION = 1
 

@@ -37,6 +37,9 @@ constexpr int AEQ_N = 32;            // block length
 constexpr int AEQ_WARPS = 4;         // streams per CTA
 constexpr int AEQ_TAP_MAX = 16383;   // TAP_MAG_MAX (aeq.py:26)
 constexpr int XF_LUT = 127;          // x / sig_scale table for |x| <= 127
+#ifndef AEQ_MIN_CTAS
+#define AEQ_MIN_CTAS 4               // resident CTAs per SM the register budget targets
+#endif
 
 struct __align__(16) AeqScratch {
   int32_t part[32][32];       // per-lane partial sums (direct: 16 hi + 16 lo; fnt: 16)
@@ -64,29 +67,51 @@ __device__ __forceinline__ int32_t sbyte(uint32_t w, uint32_t k) {
 }
 
 // split_taps (fixedpoint.py:111-121): sign * (|w| >> 7) or sign * (|w| & 127)
+// (|w| < 2^14 always: taps are clipped to +-16383 and split_taps rejects larger)
 __device__ __forceinline__ int32_t tap_group(int32_t w, int g) {
-  const int32_t m = w < 0 ? -w : w;
-  const int32_t v = g == 0 ? (m >> 7) : (m & 127);
+  const int32_t m = abs(w);
+  const int32_t v = (m >> (g ? 0 : 7)) & 127;
   return w < 0 ? -v : v;
 }
 
-// rde_error (aeq.py:53-58) for one output pair (y_I, y_Q)
+// rde_error (aeq.py:53-58) for one output pair (y_I, y_Q). The 3-ring case
+// (16QAM, qam16_radii) is unrolled; other ring counts loop.
 __device__ __forceinline__ double rde(double yi, double yq, const AeqArgs& A) {
   const double r2 = dadd(dmul(yi, yi), dmul(yq, yq));
   const double r = __dsqrt_rn(r2);
-  int best = 0;
-  double bd = fabs(dsub(r, A.prm.radii[0]));
-#pragma unroll
-  for (int i = 1; i < 8; ++i) {
-    if (i < A.prm.n_radii) {
+  double best_r2;
+  if (A.prm.n_radii == 3) {
+    const double d0 = fabs(dsub(r, A.prm.radii[0]));
+    const double d1 = fabs(dsub(r, A.prm.radii[1]));
+    const double d2 = fabs(dsub(r, A.prm.radii[2]));
+    // np.argmin: first minimum
+    const bool take1 = d1 < d0;
+    const double dm = take1 ? d1 : d0;
+    best_r2 = d2 < dm ? A.R2[2] : (take1 ? A.R2[1] : A.R2[0]);
+  } else {
+    int best = 0;
+    double bd = fabs(dsub(r, A.prm.radii[0]));
+    for (int i = 1; i < A.prm.n_radii; ++i) {
       const double d = fabs(dsub(r, A.prm.radii[i]));
-      if (d < bd) { bd = d; best = i; }  // np.argmin: first minimum
+      if (d < bd) { bd = d; best = i; }
     }
+    best_r2 = A.R2[best];
   }
-  double R2 = A.R2[0];
-#pragma unroll
-  for (int i = 1; i < 8; ++i) R2 = best == i ? A.R2[i] : R2;
-  return dsub(R2, r2);
+  return dsub(best_r2, r2);
+}
+
+// np.rint(w * tap_scale).astype(int64), then |.| > 16383 -> count and clip
+// (aeq.py:165-168). Values whose rint is not a representable int64 (|r| >= 2^63,
+// NaN) become INT64_MIN in numpy on x86-64: not counted, clipped to -16383.
+__device__ __forceinline__ int32_t requantize_tap(double w, double tap_scale, long long& sat) {
+  const double r = rint(dmul(w, tap_scale));
+  const double a = fabs(r);
+  if (!(a < 9.2233720368547758e18)) return -AEQ_TAP_MAX;
+  if (a > (double)AEQ_TAP_MAX) {
+    ++sat;
+    return r < 0 ? -AEQ_TAP_MAX : AEQ_TAP_MAX;
+  }
+  return (int32_t)r;
 }
 
 // einsum("sm,tmk->stk") inner reduction over m in numpy's SSE2 order.
@@ -152,29 +177,40 @@ __device__ __forceinline__ void lane_update(const AeqArgs& A, AeqScratch& S, int
     // gradient for taps k in [8g, 8g+8): sum_m ey[s][m] * xf[t][16 + m - k]
     double ey[AEQ_L];
 #pragma unroll
-    for (int m = 0; m < AEQ_L; ++m) ey[m] = S.ey[s][m];
-    double xf[23];  // xf[t][j] for j = 9 - 8g ... 31 - 8g
-    const int prev = cur ^ 1;
-#pragma unroll
-    for (int q = 0; q < 23; ++q) {
-      const int j = q + 9 - 8 * g;  // 1..31
-      xf[q] = j < AEQ_L ? S.xf[t][prev][j] : S.xf[t][cur][j - AEQ_L];
+    for (int q = 0; q < AEQ_L / 2; ++q) {
+      const double2 v = reinterpret_cast<const double2*>(S.ey[s])[q];
+      ey[2 * q] = v.x;
+      ey[2 * q + 1] = v.y;
     }
+    // xf[t][j] for j = 9 - 8g ... 31 - 8g as a window that slides by one per tap:
+    // tap kk (k = 8g + kk) uses xw index q = 7 + m - kk, m = 0..15. Taps run from
+    // kk = 7 down to 0 so each step needs exactly one new value.
+    const int prev = cur ^ 1;
+    const double* xs_prev = S.xf[t][prev];
+    const double* xs_cur = S.xf[t][cur];
+    auto xload = [&](int q) -> double {
+      const int j = q + 9 - 8 * g;  // 1..31
+      return j < AEQ_L ? xs_prev[j] : xs_cur[j - AEQ_L];
+    };
+    double xw[23];
 #pragma unroll
-    for (int kk = 0; kk < 8; ++kk) {
-      // k = 8g + kk ; j = 16 + m - k ; q = j - (9 - 8g) = 7 + m - kk
-      double P[AEQ_L];
+    for (int q = 0; q < 16; ++q) xw[q] = xload(q);
 #pragma unroll
-      for (int m = 0; m < AEQ_L; ++m) P[m] = dmul(ey[m], xf[7 + m - kk]);
-      const double gr = einsum_m(P);
+    for (int kk = 7; kk >= 0; --kk) {
+      if (kk < 7) xw[22 - kk] = xload(22 - kk);
+      // einsum over m in numpy's order, each product rounded before its add
+      const int o = 7 - kk;
+      double c0 = dmul(ey[6], xw[o + 6]), c1 = dmul(ey[7], xw[o + 7]);
+      c0 = dadd(dmul(ey[4], xw[o + 4]), c0);   c1 = dadd(dmul(ey[5], xw[o + 5]), c1);
+      c0 = dadd(dmul(ey[2], xw[o + 2]), c0);   c1 = dadd(dmul(ey[3], xw[o + 3]), c1);
+      c0 = dadd(dmul(ey[0], xw[o + 0]), c0);   c1 = dadd(dmul(ey[1], xw[o + 1]), c1);
+      c0 = dadd(dmul(ey[14], xw[o + 14]), c0); c1 = dadd(dmul(ey[15], xw[o + 15]), c1);
+      c0 = dadd(dmul(ey[12], xw[o + 12]), c0); c1 = dadd(dmul(ey[13], xw[o + 13]), c1);
+      c0 = dadd(dmul(ey[10], xw[o + 10]), c0); c1 = dadd(dmul(ey[11], xw[o + 11]), c1);
+      c0 = dadd(dmul(ey[8], xw[o + 8]), c0);   c1 = dadd(dmul(ey[9], xw[o + 9]), c1);
+      const double gr = dadd(c0, c1);
       T.w[kk] = dadd(T.w[kk], dmul(mu, gr));
-      long long wi = __double2ll_rn(dmul(T.w[kk], A.prm.tap_scale));  // np.rint -> int64
-      const long long aw = wi < 0 ? -wi : wi;
-      if (aw > AEQ_TAP_MAX) {
-        T.sat++;
-        wi = wi < 0 ? -AEQ_TAP_MAX : AEQ_TAP_MAX;
-      }
-      T.wi[kk] = (int32_t)wi;
+      T.wi[kk] = requantize_tap(T.w[kk], A.prm.tap_scale, T.sat);
     }
   }
   __syncwarp();
@@ -313,7 +349,7 @@ __device__ __forceinline__ void lane_forward(AeqScratch& S, int lane, int cur, c
 // process (aeq.py:172-190) for one stream per warp
 
 template <int FWD, int IN_MODE, typename TIN>
-__global__ void __launch_bounds__(AEQ_WARPS * 32) k_aeq_process(fntgpu_aeq_state* __restrict__ st,
+__global__ void __launch_bounds__(AEQ_WARPS * 32, AEQ_MIN_CTAS) k_aeq_process(fntgpu_aeq_state* __restrict__ st,
                                                                  const __grid_constant__ AeqArgs A) {
   constexpr bool NARROW = sizeof(TIN) == 1;
   __shared__ AeqScratch scratch[AEQ_WARPS];

@@ -1,0 +1,144 @@
+"""Full-size BASELINE configs on the GPU.
+
+* Config 3 (2^20 symbols x 2 pols x 6 SNRs): inputs regenerated bit-exactly by
+  oracle.linkgen_np (pinned to the reference's input digests), then the whole
+  GPU chain (CDC + glue + AEQ) is compared with digests the unmodified reference
+  produced for every intermediate and output, and BER/EVM are reported next to
+  the reference's values (identical, since the outputs are bit-identical).
+* Config 5 (a subset of its 4096 links): GPU chain vs the pinned CPU oracle.
+* Config 4 (CDC throughput scale): a 2^28-sample dual-pol stream in HBM; windows
+  copied back and checked against the oracle; linearity across the whole stream.
+"""
+
+import json
+
+import numpy as np
+import pytest
+
+import oracle as O
+import oracle.linkgen_np as G
+import paper_2405_04253_b200 as P
+from conftest import GOLDEN, sha
+
+pytestmark = pytest.mark.gpu
+
+SNRS = (14.0, 16.0, 18.0, 20.0, 22.0, 24.0)
+
+
+def _chain(cfg, eng, fe, keep=True):
+    import torch
+    from paper_2405_04253_b200.stream import CdcAeqChain
+    L = fe[0][0].size
+    xr = torch.from_numpy(np.stack([fe[0][0], fe[1][0]]).astype(np.int8)).cuda()
+    xi = torch.from_numpy(np.stack([fe[0][1], fe[1][1]]).astype(np.int8)).cuda()
+    ch = CdcAeqChain(eng, cfg.aeq_config(), 1, L, cfg.sig_spec(), cfg.mu_schedule(), keep_cdc_int=keep)
+    ch.run(xr, xi)
+    return ch
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("snr", SNRS)
+def test_config3_full_chain_vs_reference(snr):
+    d = json.loads((GOLDEN / "digests.json").read_text())["c3"][str(snr)]
+    L, bits, sym, fe = G.config3(snr)
+    assert [sha(np.stack([a, b]).astype(np.int8)) for a, b in fe] == d["q_in"]
+    cfg = P.LinkConfig(n_symbols=2 ** 20, z_km=75.0, snr_db=(snr,), pol_rotation_deg=0.0,
+                       dgd_symbols=0.0, iq_skew_samples=0.0, seed=2)
+    eng = P.FntCdcEngine(cfg.cdc_config("fnt"), cfg.sig_spec())
+    ch = _chain(cfg, eng, fe)
+    yr, yi = (t.cpu().numpy().astype(np.int64) for t in ch.yint)
+    assert [sha(np.stack([yr[p], yi[p]])) for p in range(2)] == d["cdc_int"]
+    ph = int(ch.phase.cpu()[0])
+    assert ph == d["phase"]
+    n = ch.L // 2
+    qa = np.stack([ch.qr[0, ph:ch.L:2].cpu().numpy(), ch.qi[0, ph:ch.L:2].cpu().numpy(),
+                   ch.qr[1, ph:ch.L:2].cpu().numpy(), ch.qi[1, ph:ch.L:2].cpu().numpy()])[:, :n]
+    assert sha(qa.astype(np.int8)) == d["aeq_in"]
+    y = ch.y[0].cpu().numpy()
+    assert sha(y) == d["aeq_y"]
+    st = ch.aeq.read_state()[0]
+    assert sha(np.array(st.w, dtype=np.float64).reshape(4, 4, 16)) == d["w"]
+    assert sha(np.array(st.w_int, dtype=np.int64).reshape(4, 4, 16)) == d["w_int"]
+    assert int(st.saturations) == d["sat"]
+    assert sha(ch.err[0].cpu().numpy()) == d["err_trace"]
+    y_pols = np.stack([y[0] + 1j * y[1], y[2] + 1j * y[3]])
+    ber, evm, ok = G.ber_evm(y_pols, bits, sym, 20000)
+    assert ber == d["ber"] and evm == d["evm_db"] and ok == d["ok"]
+    print(f"C3 snr={snr}: BER {ber:.6f} (reference {d['ber']:.6f}), EVM {evm:.4f} dB")
+
+
+def _oracle_chain(eng, cfg, fe):
+    """CPU oracle of the whole per-link chain (pinned pieces of oracle/)."""
+    inv = 1.0 / eng.output_scale
+    streams = []
+    for xr, xi in fe:
+        yr, yi = O.cdc_process_int(eng.tap_re, eng.tap_im, xr, xi)
+        streams.append(yr * inv + 1j * (yi * inv))
+    ph = O.decimation_phase(streams)
+    dec = [s[ph::2] for s in streams]
+    q = np.stack([O.quantize_real(v, cfg.sig_scale, 15)[0]
+                  for v in (dec[0].real, dec[0].imag, dec[1].real, dec[1].imag)])
+    nb = q.shape[1] // 16
+    oq = O.Aeq(cfg.sig_scale, mu=cfg.mu2)
+    y = oq.process(q, mu_blocks=O.mu_blocks(nb, mu1=cfg.mu1, mu2=cfg.mu2,
+                                             gear_symbols=cfg.gear_symbols))
+    return ph, y, oq
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("link", [0, 1, 4095])
+def test_config5_links_vs_oracle(link):
+    L, bits, sym, fe = G.config5(link)
+    cfg = P.LinkConfig(n_symbols=2 ** 18, z_km=75.0, pol_rotation_deg=0.0, dgd_symbols=0.0,
+                       iq_skew_samples=0.0, seed=4)
+    eng = P.FntCdcEngine(cfg.cdc_config("fnt"), cfg.sig_spec())
+    ch = _chain(cfg, eng, fe, keep=False)
+    ph, y, oq = _oracle_chain(eng, cfg, fe)
+    assert int(ch.phase.cpu()[0]) == ph
+    assert np.array_equal(ch.y[0].cpu().numpy(), y)
+    assert np.array_equal(ch.err[0].cpu().numpy(), np.array(oq.err_trace))
+    st = ch.aeq.read_state()[0]
+    assert np.array_equal(np.array(st.w).reshape(4, 4, 16), oq.w)
+
+
+@pytest.mark.slow
+def test_config4_scale_cdc_windows_and_linearity():
+    """2^28 samples per pol (x2 pols) resident in HBM through one CDC launch;
+    random windows checked bit-exactly against the oracle, and the whole stream
+    checked by linearity: CDC(x1 + x2) == CDC(x1) + CDC(x2) (mod-F decode free
+    because |outputs| stay inside the budget)."""
+    import torch
+    from paper_2405_04253_b200.stream import CdcBank
+    cfg = P.LinkConfig(z_km=75.0)
+    eng = P.FntCdcEngine(cfg.cdc_config("fnt"), cfg.sig_spec())
+    bank = CdcBank(eng)
+    L = 1 << 28
+    g = torch.Generator(device="cuda").manual_seed(3)
+    # two halves of the 5-bit range so that x1 + x2 stays within +-15
+    x1r = torch.randint(-7, 8, (2, L), generator=g, device="cuda", dtype=torch.int8)
+    x1i = torch.randint(-7, 8, (2, L), generator=g, device="cuda", dtype=torch.int8)
+    x2r = torch.randint(-8, 8, (2, L), generator=g, device="cuda", dtype=torch.int8)
+    x2i = torch.randint(-8, 8, (2, L), generator=g, device="cuda", dtype=torch.int8)
+    outs = []
+    for xr, xi in ((x1r, x1i), (x2r, x2i), (x1r + x2r, x1i + x2i)):
+        yr = torch.empty((2, L), dtype=torch.int16, device="cuda")
+        yi = torch.empty_like(yr)
+        bank.run(xr, xi, yr=yr, yi=yi)
+        outs.append((yr, yi))
+    assert torch.equal(outs[0][0] + outs[1][0], outs[2][0])
+    assert torch.equal(outs[0][1] + outs[1][1], outs[2][1])
+    rng = np.random.default_rng(0)
+    for a in list(rng.integers(0, L - 4096, 6)) + [0, L - 4096]:
+        a = int(a)
+        lo, hi = max(0, a - 64), min(L, a + 4096 + 64)
+        for p in range(2):
+            wr = x1r[p, lo:hi].cpu().numpy().astype(np.int64)
+            wi = x1i[p, lo:hi].cpu().numpy().astype(np.int64)
+            orr, ori = O.cdc_direct(eng.tap_re, eng.tap_im, wr, wi)
+            # outputs away from the window edges equal the full-stream outputs
+            s0 = a - lo
+            got_r = outs[0][0][p, a:a + 4096].cpu().numpy()
+            got_i = outs[0][1][p, a:a + 4096].cpu().numpy()
+            inner = slice(32 if a > 0 else 0, 4096 - 32 if a + 4096 < L else 4096)
+            assert np.array_equal(got_r[inner], orr[s0:s0 + 4096][inner])
+            assert np.array_equal(got_i[inner], ori[s0:s0 + 4096][inner])

@@ -148,7 +148,7 @@ def cpu_links_sample(n_tasks: int, n_sym: int, seed: int = 4):
     return out
 
 
-def run_cpu_baseline(engine, cfg, n_sym: int, cores: int, rounds: int = 1) -> dict:
+def run_cpu_baseline(engine, cfg, n_sym: int, cores: int, rounds: int | None = None) -> dict:
     """Time the reference algorithm (numpy port) on all host cores."""
     from concurrent.futures import ProcessPoolExecutor
     import oracle.np_port  # noqa: F401  (checker / baseline only)
@@ -159,7 +159,10 @@ def run_cpu_baseline(engine, cfg, n_sym: int, cores: int, rounds: int = 1) -> di
     args = [(xr, xi, engine.tap_re, engine.tap_im, cfg.n_cdc_taps, engine.output_scale,
              cfg.sig_scale, mu) for xr, xi in samples]
     with ProcessPoolExecutor(max_workers=cores) as ex:
-        list(ex.map(_cpu_task, args[:1]))  # warm the workers' imports
+        per_task = max(list(ex.map(_cpu_task, args)))  # warm the workers' imports, size the sample
+        if rounds is None:
+            # about 20 s of CPU work over all cores (a bounded sample of the workload)
+            rounds = max(1, int(round(20.0 / max(per_task * cores, 1e-3))))
         t0 = time.perf_counter()
         for _ in range(rounds):
             list(ex.map(_cpu_task, args))

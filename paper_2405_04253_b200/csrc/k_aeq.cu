@@ -42,11 +42,12 @@ constexpr int XF_LUT = 127;          // x / sig_scale table for |x| <= 127
 #endif
 
 struct __align__(16) AeqScratch {
-  int32_t part[32][32];       // per-lane partial sums (direct: 16 hi + 16 lo; fnt: 16)
+  double wf[8][32];           // float taps (aeq.py:99), lane-contiguous: wf[kk][lane] = w[s][t][8g+kk]
+  int32_t part[32][33];       // per-lane partial sums (direct: 16 hi + 16 lo; fnt: 16), padded
   double ey[4][AEQ_L];        // e * y per output stream
-  double xf[4][2][AEQ_L];     // x / sig_scale ring: [t][block parity][j]
+  double xf[4][33];           // x / sig_scale ring: [t][16 * parity + j] (odd t-stride: no conflicts)
   int32_t xi[4][2][AEQ_L];    // input integer ring: [t][block parity][j]
-  uint32_t X[4][AEQ_N];       // cooperative input spectra (FNT path)
+  uint32_t X[4][AEQ_N + 4];   // cooperative input spectra (FNT path), 16-B aligned padded rows
   double err[32];             // |e| values for the err_trace mean
 };
 
@@ -135,8 +136,9 @@ __device__ __forceinline__ double xf_of(int32_t x, const double* lut, double sig
   return (x >= -XF_LUT && x <= XF_LUT) ? lut[x + XF_LUT] : __ddiv_rn((double)x, sig);
 }
 
+// This lane's 8 taps k = 8g .. 8g+7 of filter (s, t): the 14-bit values in
+// registers, the float values in the warp's shared scratch (S.wf, lane-contiguous).
 struct LaneTaps {
-  double w[8];
   int32_t wi[8];
   long long sat;
 };
@@ -186,8 +188,8 @@ __device__ __forceinline__ void lane_update(const AeqArgs& A, AeqScratch& S, int
     // tap kk (k = 8g + kk) uses xw index q = 7 + m - kk, m = 0..15. Taps run from
     // kk = 7 down to 0 so each step needs exactly one new value.
     const int prev = cur ^ 1;
-    const double* xs_prev = S.xf[t][prev];
-    const double* xs_cur = S.xf[t][cur];
+    const double* xs_prev = S.xf[t] + AEQ_L * prev;
+    const double* xs_cur = S.xf[t] + AEQ_L * cur;
     auto xload = [&](int q) -> double {
       const int j = q + 9 - 8 * g;  // 1..31
       return j < AEQ_L ? xs_prev[j] : xs_cur[j - AEQ_L];
@@ -209,8 +211,9 @@ __device__ __forceinline__ void lane_update(const AeqArgs& A, AeqScratch& S, int
       c0 = dadd(dmul(ey[10], xw[o + 10]), c0); c1 = dadd(dmul(ey[11], xw[o + 11]), c1);
       c0 = dadd(dmul(ey[8], xw[o + 8]), c0);   c1 = dadd(dmul(ey[9], xw[o + 9]), c1);
       const double gr = dadd(c0, c1);
-      T.w[kk] = dadd(T.w[kk], dmul(mu, gr));
-      T.wi[kk] = requantize_tap(T.w[kk], A.prm.tap_scale, T.sat);
+      const double w = dadd(S.wf[kk][lane], dmul(mu, gr));
+      S.wf[kk][lane] = w;
+      T.wi[kk] = requantize_tap(w, A.prm.tap_scale, T.sat);
     }
   }
   __syncwarp();
@@ -260,7 +263,8 @@ __device__ __forceinline__ void lane_forward(AeqScratch& S, int lane, int cur, c
   const int s = lane >> 3, t = (lane >> 1) & 3, g = lane & 1;
   if (FWD == FNTGPU_AEQ_FWD_FNT) {
     warp_input_fnt(S, lane, cur);
-    // all 16 taps of filter (s, t): own 8 + partner's 8 (lane ^ 1 holds the other half)
+    // all 16 taps of filter (s, t), group g (split_taps, fixedpoint.py:111-121):
+    // own 8 + partner's 8 (lane ^ 1 holds the other half)
     uint32_t W[AEQ_N];
 #pragma unroll
     for (int kk = 0; kk < 8; ++kk) {
@@ -292,9 +296,8 @@ __device__ __forceinline__ void lane_forward(AeqScratch& S, int lane, int cur, c
     int32_t a0 = 0, a1 = 0;
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
-      const int2 v = *reinterpret_cast<const int2*>(&S.part[s * 8 + q][m0]);
-      a0 += v.x;
-      a1 += v.y;
+      a0 += S.part[s * 8 + q][m0];
+      a1 += S.part[s * 8 + q][m0 + 1];
     }
     yi0 = a0;
     yi1 = a1;
@@ -330,10 +333,10 @@ __device__ __forceinline__ void lane_forward(AeqScratch& S, int lane, int cur, c
 #pragma unroll
     for (int tt = 0; tt < 4; ++tt) {
       const int l0 = s * 8 + tt * 2;
-      const int2 h0 = *reinterpret_cast<const int2*>(&S.part[l0][m0]);
-      const int2 h1 = *reinterpret_cast<const int2*>(&S.part[l0 + 1][m0]);
-      const int2 l0v = *reinterpret_cast<const int2*>(&S.part[l0][AEQ_L + m0]);
-      const int2 l1v = *reinterpret_cast<const int2*>(&S.part[l0 + 1][AEQ_L + m0]);
+      const int2 h0 = make_int2(S.part[l0][m0], S.part[l0][m0 + 1]);
+      const int2 h1 = make_int2(S.part[l0 + 1][m0], S.part[l0 + 1][m0 + 1]);
+      const int2 l0v = make_int2(S.part[l0][AEQ_L + m0], S.part[l0][AEQ_L + m0 + 1]);
+      const int2 l1v = make_int2(S.part[l0 + 1][AEQ_L + m0], S.part[l0 + 1][AEQ_L + m0 + 1]);
       // each group convolution is a residue mod F4, decoded (aeq.py:139-140)
       const int32_t B = (int32_t)(F4 * 1024u);
       a0 += 128 * f4_signed((uint32_t)(h0.x + h1.x + B)) + f4_signed((uint32_t)(l0v.x + l1v.x + B));
@@ -374,7 +377,7 @@ __global__ void __launch_bounds__(AEQ_WARPS * 32, AEQ_MIN_CTAS) k_aeq_process(fn
   LaneTaps T;
 #pragma unroll
   for (int kk = 0; kk < 8; ++kk) {
-    T.w[kk] = state.w[s][t][8 * g + kk];
+    S.wf[kk][lane] = state.w[s][t][8 * g + kk];
     T.wi[kk] = state.w_int[s][t][8 * g + kk];
   }
   T.sat = 0;
@@ -383,8 +386,8 @@ __global__ void __launch_bounds__(AEQ_WARPS * 32, AEQ_MIN_CTAS) k_aeq_process(fn
     const int32_t h0 = state.hist[tq][iq], h1 = state.hist[tq][iq + 1];
     S.xi[tq][1][iq] = h0;
     S.xi[tq][1][iq + 1] = h1;
-    S.xf[tq][1][iq] = xf_of<false>(h0, lut, A.prm.sig_scale);
-    S.xf[tq][1][iq + 1] = xf_of<false>(h1, lut, A.prm.sig_scale);
+    S.xf[tq][AEQ_L * (1) + iq] = xf_of<false>(h0, lut, A.prm.sig_scale);
+    S.xf[tq][AEQ_L * (1) + iq + 1] = xf_of<false>(h1, lut, A.prm.sig_scale);
   }
 
   // this lane's input row (stream tq) and a one-block-ahead prefetch of its 2 samples
@@ -434,8 +437,8 @@ __global__ void __launch_bounds__(AEQ_WARPS * 32, AEQ_MIN_CTAS) k_aeq_process(fn
     S.xi[tq][cur][iq] = v0;
     S.xi[tq][cur][iq + 1] = v1;
     if (io.adapt) {
-      S.xf[tq][cur][iq] = xf_of<NARROW>(v0, lut, A.prm.sig_scale);
-      S.xf[tq][cur][iq + 1] = xf_of<NARROW>(v1, lut, A.prm.sig_scale);
+      S.xf[tq][AEQ_L * (cur) + iq] = xf_of<NARROW>(v0, lut, A.prm.sig_scale);
+      S.xf[tq][AEQ_L * (cur) + iq + 1] = xf_of<NARROW>(v1, lut, A.prm.sig_scale);
     }
     __syncwarp();
     int32_t yi0, yi1;
@@ -452,9 +455,10 @@ __global__ void __launch_bounds__(AEQ_WARPS * 32, AEQ_MIN_CTAS) k_aeq_process(fn
   }
 
   // write back the stream state
+  __syncwarp();
 #pragma unroll
   for (int kk = 0; kk < 8; ++kk) {
-    state.w[s][t][8 * g + kk] = T.w[kk];
+    state.w[s][t][8 * g + kk] = S.wf[kk][lane];
     state.w_int[s][t][8 * g + kk] = T.wi[kk];
   }
   if (io.n_blocks > 0) {
@@ -481,20 +485,26 @@ __global__ void k_aeq_update_once(fntgpu_aeq_state* st, const __grid_constant__ 
   const int m0 = 8 * (j8 & 1) + 4 * ((j8 >> 1) & 1) + 2 * ((j8 >> 2) & 1);
   LaneTaps T;
 #pragma unroll
-  for (int kk = 0; kk < 8; ++kk) { T.w[kk] = st->w[s][t][8 * g + kk]; T.wi[kk] = st->w_int[s][t][8 * g + kk]; }
+  for (int kk = 0; kk < 8; ++kk) {
+    S.wf[kk][lane] = st->w[s][t][8 * g + kk];
+    T.wi[kk] = st->w_int[s][t][8 * g + kk];
+  }
   T.sat = 0;
   if (s == 0 && g == 0) {
     for (int i = 0; i < AEQ_L; ++i) {
       // x_block may hold any int64 the reference accepted; divide exactly
-      S.xf[t][1][i] = __ddiv_rn((double)xblk[t * AEQ_N + i], A.prm.sig_scale);
-      S.xf[t][0][i] = __ddiv_rn((double)xblk[t * AEQ_N + AEQ_L + i], A.prm.sig_scale);
+      S.xf[t][AEQ_L * (1) + i] = __ddiv_rn((double)xblk[t * AEQ_N + i], A.prm.sig_scale);
+      S.xf[t][AEQ_L * (0) + i] = __ddiv_rn((double)xblk[t * AEQ_N + AEQ_L + i], A.prm.sig_scale);
     }
   }
   __syncwarp();
   const double y0 = y[s * AEQ_L + m0], y1 = y[s * AEQ_L + m0 + 1];
   lane_update(A, S, lane, m0, y0, y1, 0, mu, T, err);
 #pragma unroll
-  for (int kk = 0; kk < 8; ++kk) { st->w[s][t][8 * g + kk] = T.w[kk]; st->w_int[s][t][8 * g + kk] = T.wi[kk]; }
+  for (int kk = 0; kk < 8; ++kk) {
+    st->w[s][t][8 * g + kk] = S.wf[kk][lane];
+    st->w_int[s][t][8 * g + kk] = T.wi[kk];
+  }
   long long sat = T.sat;
 #pragma unroll
   for (int off = 16; off > 0; off >>= 1) sat += __shfl_xor_sync(0xffffffffu, sat, off);

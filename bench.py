@@ -186,6 +186,24 @@ def impl_reference(args) -> None:
     cores = os.cpu_count() or 1
     eng = _HostEngine(cfg)
     n_sym = args.cpu_symbols
+    if args.config == "c4":
+        import oracle.np_port as N
+        eng._b_plus, eng._b_minus = N.cdc_spectra(eng.tap_re, eng.tap_im)
+        t0 = time.perf_counter()
+        vals = [run_cpu_cdc_baseline(eng, 1 << 20, cores) for _ in range(args.steps)]
+        wall = time.perf_counter() - t0
+        v = float(np.mean([x["value"] for x in vals]))
+        print(json.dumps({
+            "impl": "reference", "metric": "FNT-CDC Gsamples/s (config 4)", "value": v, "unit": UNIT,
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 * wall / max(args.steps, 1), "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "int64", "data": "synthetic",
+            "config": {"workload": "C4 throughput-scale FNT-CDC (CPU sample)"},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "port",
+                             "sample": vals[0]["sample"]},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "gpu_launches": 0}))
+        return
     for _ in range(args.warmup and 1):
         run_cpu_baseline(eng, cfg, n_sym, cores)
     t0 = time.perf_counter()
@@ -261,6 +279,10 @@ def main():
     ap.add_argument("--cpu-symbols", type=int, default=1 << 13)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--config", default="c5", choices=["c5", "c4"],
+                    help="c5: many-channel CDC+AEQ chain (headline); c4: throughput-scale CDC")
+    ap.add_argument("--c4-samples", type=int, default=1 << 31, help="C4 samples per polarization")
+    ap.add_argument("--no-alt", action="store_true", help="skip the direct-forward AEQ comparison")
     args = ap.parse_args()
     if args.impl == "reference":
         impl_reference(args)
@@ -279,6 +301,12 @@ def main():
     from paper_2405_04253_b200 import _lib
     from paper_2405_04253_b200.linkgen import DeviceLinkGenerator
     from paper_2405_04253_b200.stream import CdcAeqChain
+
+    if args.config == "c4":
+        run_c4(args, world, rank, local)
+        if world > 1:
+            dist.destroy_process_group()
+        return
 
     cfg = _link_cfg(args)
     fwd = _lib.AEQ_FWD_DIRECT if args.forward == "direct" else _lib.AEQ_FWD_FNT
@@ -359,7 +387,8 @@ def main():
     aeq_tops = n_blk_aeq * aeq_int / (aeq_ms * 1e-3) / 1e12
     aeq_fp64 = n_blk_aeq * AEQ_FP64_OPS_PER_BLOCK / (aeq_ms * 1e-3) / 1e12
     cdc_bytes = 2 * args.links * L * (2 + 2)  # int8 I/Q in, int8 requantized I/Q out
-    aeq_bytes = args.links * (4 * 2 * (2 * chain.n_blocks * 16) // 2 + 4 * 8 * chain.n_blocks * 16)
+    # AEQ HBM: 4 int8 rows read in 32-byte phase pairs, float64 y written, err_trace written
+    aeq_bytes = args.links * (4 * 32 * chain.n_blocks + 4 * 16 * chain.n_blocks * 8 + 8 * chain.n_blocks)
     traffic = None
     ncu = PROFILES / "ncu_summary_r01.json"
     if ncu.exists():
@@ -403,6 +432,33 @@ def main():
         "outputs_finite": ok,
     }
 
+    # the exact-equivalent time-domain forward (FNTGPU_AEQ_FWD_DIRECT, same bits) on the
+    # same resident data, reported beside the FNT-domain headline
+    if fwd == _lib.AEQ_FWD_FNT and not args.no_alt:
+        chain.aeq.prm.forward = _lib.AEQ_FWD_DIRECT
+        chain.run(xr, xi)
+        torch.cuda.synchronize()
+        ev.clear()
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record()
+        for _ in range(args.steps):
+            step(True)
+        b.record()
+        torch.cuda.synchronize()
+        ms_alt = a.elapsed_time(b)
+        if world > 1:
+            t = torch.tensor([ms_alt], dtype=torch.float64, device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms_alt = float(t[0])
+        line["aeq_forward_direct"] = {
+            "value": samples_all / (ms_alt * 1e-3) / 1e9, "unit": UNIT,
+            "ms_per_step": ms_alt / args.steps,
+            "aeq_ms": float(np.mean([e[2].elapsed_time(e[3]) for e in ev])),
+            "note": "same chain with the AEQ forward as an exact time-domain integer FIR "
+                    "(bit-identical outputs, tests/test_gpu_parity.py); headline uses the FNT forward"}
+        chain.aeq.prm.forward = _lib.AEQ_FWD_FNT
+
     # end-to-end through the public host API: pinned host int8 in, float64 AEQ y out
     if not args.no_e2e:
         line["e2e"] = run_e2e(args, eng, cfg, xr, xi, fwd, world)
@@ -413,6 +469,154 @@ def main():
         print(json.dumps(line))
     if world > 1:
         dist.destroy_process_group()
+
+
+def _cdc_cpu_task(args):
+    xr, xi, bp, bm = args
+    import oracle.np_port as N
+    t0 = time.perf_counter()
+    N.cdc_process_int(xr, xi, bp, bm, 32)
+    return time.perf_counter() - t0
+
+
+def run_cpu_cdc_baseline(eng, n: int, cores: int) -> dict:
+    """Reference-algorithm CDC (numpy restatement) on all host cores, ~20 s of CPU work."""
+    from concurrent.futures import ProcessPoolExecutor
+    rng = np.random.default_rng(3)
+    tasks = [(rng.integers(-15, 16, n), rng.integers(-15, 16, n), eng._b_plus, eng._b_minus)
+             for _ in range(cores)]
+    with ProcessPoolExecutor(max_workers=cores) as ex:
+        per = max(ex.map(_cdc_cpu_task, tasks))
+        rounds = max(1, int(round(20.0 / max(per * cores, 1e-3))))
+        t0 = time.perf_counter()
+        for _ in range(rounds):
+            list(ex.map(_cdc_cpu_task, tasks))
+        wall = time.perf_counter() - t0
+    return {"value": rounds * cores * n / wall / 1e9, "unit": UNIT, "cores": cores, "kind": "port",
+            "sample": (f"{rounds * cores} streams x {n} complex samples through oracle/np_port."
+                       f"cdc_process_int (numpy restatement of the reference's FntCdcEngine."
+                       f"process_int), one process per core, {wall:.1f} s wall")}
+
+
+def run_c4(args, world, rank, local):
+    """BASELINE config 4: one dual-pol stream of 2^31 complex samples per
+    polarization, FNT-CDC range-sharded across ranks (strong scaling: the stream
+    length is fixed) with the overlap-save halo read from each rank's input window
+    (sharding.py); no data-path collective."""
+    import torch
+    import torch.distributed as dist
+    import paper_2405_04253_b200 as P
+    from paper_2405_04253_b200.linkgen import DeviceLinkGenerator
+    from paper_2405_04253_b200.sharding import cdc_range_shards
+    from paper_2405_04253_b200.stream import CdcBank
+
+    cfg = P.LinkConfig(z_km=75.0, seed=3)
+    eng = P.FntCdcEngine(cfg.cdc_config("fnt"), cfg.sig_spec())
+    bank = CdcBank(eng)
+    L = args.c4_samples
+    sh = cdc_range_shards(L, world, n_taps=cfg.n_cdc_taps)[rank]
+    # input window of this rank, generated on device in independent 2^22-sample
+    # link segments (same signal model; seeded per segment)
+    seg = 1 << 22
+    n_seg = -(-sh.x_count // seg)
+    gen = DeviceLinkGenerator(seg // 2, z_km=75.0, sig_scale=cfg.sig_scale)
+    xr = torch.empty((2, n_seg * seg), dtype=torch.int8, device="cuda")
+    xi = torch.empty_like(xr)
+    per = 64
+    for c0 in range(0, n_seg, per):
+        c = min(per, n_seg - c0)
+        gr, gi = gen.generate(c, seed=3 * 1_000_003 + sh.x_first // seg + c0)
+        xr[:, c0 * seg:(c0 + c) * seg] = gr.view(c, 2, seg).transpose(0, 1).reshape(2, c * seg)
+        xi[:, c0 * seg:(c0 + c) * seg] = gi.view(c, 2, seg).transpose(0, 1).reshape(2, c * seg)
+        del gr, gi
+    xr = xr[:, :sh.x_count]
+    xi = xi[:, :sh.x_count]
+    yr = torch.empty((2, sh.out_count), dtype=torch.int16, device="cuda")
+    yi = torch.empty_like(yr)
+    torch.cuda.synchronize()
+
+    def step():
+        bank.run(xr, xi, length=L, x_first=sh.x_first, out_first=sh.out_first,
+                 out_count=sh.out_count, yr=yr, yi=yi)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clocks = ClockSampler(local)
+    clocks.start()
+    a = torch.cuda.Event(enable_timing=True)
+    b = torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(args.steps):
+        step()
+    b.record()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clk = clocks.stop()
+    ms = a.elapsed_time(b)
+    ms_max = ms
+    if world > 1:
+        t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_max = float(t[0])
+    samples = 2 * L  # both polarizations of the whole stream, all ranks
+    value = args.steps * samples / (ms_max * 1e-3) / 1e9
+    peaks = measured_peaks()
+    per_launch_ms = ms / args.steps
+    n_blocks = 2 * (sh.out_count // 32 + 2)
+    achieved = n_blocks * CDC_INT_OPS_PER_BLOCK / (per_launch_ms * 1e-3) / 1e12
+    hbm_bytes = 2 * sh.x_count * 2 + 2 * sh.out_count * 4  # int8 I/Q in, int16 I/Q out
+    hbm_gbs = hbm_bytes / (per_launch_ms * 1e-3) / 1e9
+    line = {
+        "metric": "FNT-CDC Gsamples/s (config 4)", "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max / args.steps,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": "int32 (Z/(2^32-1) residues)", "data": "synthetic (on-device 16QAM link model)",
+        "config": {"workload": "C4 throughput-scale FNT-CDC: one dual-pol stream of %d complex "
+                               "samples per pol, 75 km taps, range-sharded over %d GPU(s) with the "
+                               "overlap-save halo" % (L, world),
+                   "samples_per_pol": L, "shard_out": [sh.out_first, sh.out_count],
+                   "l2": "inputs (%.1f GB) exceed L2" % (hbm_bytes / 1e9)},
+        "roofline": {"bound": "int", "kernel": "k_cdc64", "achieved": achieved,
+                     "peak": peaks["int_tops"], "unit": "Tops/s",
+                     "frac": achieved / peaks["int_tops"], "traffic": None,
+                     "peak_source": peaks["int_source"],
+                     "hbm": {"achieved_gbs": hbm_gbs, "peak_gbs": peaks["hbm_gbs"],
+                             "frac": hbm_gbs / peaks["hbm_gbs"]}},
+        "clocks": clk, "gpu_launches": args.steps,
+    }
+    if not args.no_e2e:
+        # host buffers through the C ABI: pinned int8 I/Q -> H2D -> CDC -> D2H int16 I/Q
+        from paper_2405_04253_b200.stream import HostCdc
+        n = min(1 << 28, sh.out_count)
+        hc = HostCdc(eng, 2, n)
+        hx = torch.empty((2, n), dtype=torch.int8, pin_memory=True)
+        hy = torch.empty((2, n), dtype=torch.int8, pin_memory=True)
+        hx.copy_(xr[:, :n])
+        hy.copy_(xi[:, :n])
+        hc(hx, hy)
+        torch.cuda.synchronize()
+        a.record()
+        for _ in range(args.steps):
+            hc(hx, hy)
+        b.record()
+        torch.cuda.synchronize()
+        ms_e = a.elapsed_time(b)
+        if world > 1:
+            t = torch.tensor([ms_e], dtype=torch.float64, device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms_e = float(t[0])
+        line["e2e"] = {"value": args.steps * 2 * n * world / (ms_e * 1e-3) / 1e9, "unit": UNIT,
+                       "h2d_bytes_per_step": hc.h2d_bytes, "d2h_bytes_per_step": hc.d2h_bytes,
+                       "path": "stream.HostCdc: pinned host int8 I/Q -> H2D -> fntgpu_cdc64_process "
+                               "-> D2H int16 I/Q, %d samples x 2 pols per call" % n}
+    if rank == 0 and world == 1 and not args.no_cpu:
+        line["cpu_baseline"] = run_cpu_cdc_baseline(eng, 1 << 20, os.cpu_count() or 1)
+    if rank == 0:
+        print(json.dumps(line))
 
 
 def run_e2e(args, eng, cfg, xr, xi, fwd, world):

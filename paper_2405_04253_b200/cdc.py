@@ -99,8 +99,10 @@ def _int_input(x) -> np.ndarray:
 
 def _device_dtype(a: np.ndarray, half: int) -> np.dtype:
     """Narrowest kernel input dtype holding a; raises like encode_signed_array."""
-    if a.size == 0:
+    if a.size == 0 or a.dtype == np.int8:
         return np.dtype(np.int8)
+    if a.dtype in (np.int16, np.uint8, np.uint16) and half >= 32767:
+        return np.dtype(np.int32)  # always encodable: no host scan needed
     lo, hi = int(a.min()), int(a.max())
     if max(-lo, hi) > half:
         raise ValueError("input exceeds the encodable signed range")

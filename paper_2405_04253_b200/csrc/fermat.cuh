@@ -38,9 +38,21 @@ __device__ __forceinline__ uint32_t m_sub(uint32_t a, uint32_t b) {
   return r;
 }
 
-// a * 2^j (mod 2^32 - 1), j in [0, 32)
+// a * 2^j (mod 2^32 - 1), j in [0, 32). FNT_ROT_MODE 0: one funnel shift (ALU
+// pipe); 1: one 32x32->64 IMAD.WIDE (FMA pipe) + disjoint-bit add, to balance pipes.
+#ifndef FNT_ROT_MODE
+#define FNT_ROT_MODE 0
+#endif
 __device__ __forceinline__ uint32_t m_rot(uint32_t a, int j) {
-  return j == 0 ? a : __funnelshift_l(a, a, j);
+  if (j == 0) return a;
+#if FNT_ROT_MODE == 1
+  uint32_t lo, hi;
+  asm("{\n\t.reg .u64 p;\n\tmul.wide.u32 p, %2, %3;\n\tmov.b64 {%0, %1}, p;\n\t}"
+      : "=r"(lo), "=r"(hi) : "r"(a), "r"(1u << j));
+  return lo + hi;
+#else
+  return __funnelshift_l(a, a, j);
+#endif
 }
 
 // a * b (mod 2^32 - 1): 64-bit product folded with 2^32 == 1.

@@ -104,15 +104,23 @@ __device__ __forceinline__ double rde(double yi, double yq, const AeqArgs& A) {
 // np.rint(w * tap_scale).astype(int64), then |.| > 16383 -> count and clip
 // (aeq.py:165-168). Values whose rint is not a representable int64 (|r| >= 2^63,
 // NaN) become INT64_MIN in numpy on x86-64: not counted, clipped to -16383.
+// Branch-free: fmax(NaN, -16383) = -16383 reproduces the NaN case as well.
 __device__ __forceinline__ int32_t requantize_tap(double w, double tap_scale, long long& sat) {
   const double r = rint(dmul(w, tap_scale));
   const double a = fabs(r);
-  if (!(a < 9.2233720368547758e18)) return -AEQ_TAP_MAX;
-  if (a > (double)AEQ_TAP_MAX) {
-    ++sat;
-    return r < 0 ? -AEQ_TAP_MAX : AEQ_TAP_MAX;
-  }
-  return (int32_t)r;
+  const bool huge = !(a < 9.2233720368547758e18);
+  sat += (a > (double)AEQ_TAP_MAX) & !huge;
+  const int32_t c = (int32_t)fmin(fmax(r, -(double)AEQ_TAP_MAX), (double)AEQ_TAP_MAX);
+  return huge ? -AEQ_TAP_MAX : c;
+}
+
+// Both 7-bit groups of a tap packed as two signed 16-bit halves:
+// low half = high group (g = 0), high half = low group (g = 1).
+__device__ __forceinline__ uint32_t pack_groups(int32_t w) {
+  return ((uint32_t)tap_group(w, 0) & 0xffffu) | ((uint32_t)tap_group(w, 1) << 16);
+}
+__device__ __forceinline__ int32_t unpack_group(uint32_t p, int g) {
+  return g ? ((int32_t)p >> 16) : ((int32_t)(p << 16) >> 16);
 }
 
 // einsum("sm,tmk->stk") inner reduction over m in numpy's SSE2 order.
@@ -139,7 +147,7 @@ __device__ __forceinline__ double xf_of(int32_t x, const double* lut, double sig
 // This lane's 8 taps k = 8g .. 8g+7 of filter (s, t): the 14-bit values in
 // registers, the float values in the warp's shared scratch (S.wf, lane-contiguous).
 struct LaneTaps {
-  int32_t wi[8];
+  uint32_t gp[8];  // packed 7-bit groups of w_int (pack_groups); w_int = 128 hi + lo
   long long sat;
 };
 
@@ -213,7 +221,7 @@ __device__ __forceinline__ void lane_update(const AeqArgs& A, AeqScratch& S, int
       const double gr = dadd(c0, c1);
       const double w = dadd(S.wf[kk][lane], dmul(mu, gr));
       S.wf[kk][lane] = w;
-      T.wi[kk] = requantize_tap(w, A.prm.tap_scale, T.sat);
+      T.gp[kk] = pack_groups(requantize_tap(w, A.prm.tap_scale, T.sat));
     }
   }
   __syncwarp();
@@ -268,11 +276,11 @@ __device__ __forceinline__ void lane_forward(AeqScratch& S, int lane, int cur, c
     uint32_t W[AEQ_N];
 #pragma unroll
     for (int kk = 0; kk < 8; ++kk) {
-      const int32_t other = __shfl_xor_sync(0xffffffffu, T.wi[kk], 1);
-      const int32_t lo8 = g == 0 ? T.wi[kk] : other;   // tap kk
-      const int32_t hi8 = g == 0 ? other : T.wi[kk];   // tap 8 + kk
-      W[bitrev(kk, 5)] = f4_enc_small(tap_group(lo8, g));
-      W[bitrev(8 + kk, 5)] = f4_enc_small(tap_group(hi8, g));
+      const uint32_t other = __shfl_xor_sync(0xffffffffu, T.gp[kk], 1);
+      const uint32_t lo8 = g == 0 ? T.gp[kk] : other;   // tap kk
+      const uint32_t hi8 = g == 0 ? other : T.gp[kk];   // tap 8 + kk
+      W[bitrev(kk, 5)] = f4_enc_small(unpack_group(lo8, g));
+      W[bitrev(8 + kk, 5)] = f4_enc_small(unpack_group(hi8, g));
     }
 #pragma unroll
     for (int k = AEQ_L; k < AEQ_N; ++k) W[bitrev(k, 5)] = 0u;
@@ -317,7 +325,7 @@ __device__ __forceinline__ void lane_forward(AeqScratch& S, int lane, int cur, c
     for (int m = 0; m < AEQ_L; ++m) { hi[m] = 0; lo[m] = 0; }
 #pragma unroll
     for (int kk = 0; kk < 8; ++kk) {
-      const int32_t th = tap_group(T.wi[kk], 0), tl = tap_group(T.wi[kk], 1);
+      const int32_t th = unpack_group(T.gp[kk], 0), tl = unpack_group(T.gp[kk], 1);
 #pragma unroll
       for (int m = 0; m < AEQ_L; ++m) {
         // x index 16 + m - k, k = 8g + kk  (runtime g: select between two windows)
@@ -378,7 +386,7 @@ __global__ void __launch_bounds__(AEQ_WARPS * 32, AEQ_MIN_CTAS) k_aeq_process(fn
 #pragma unroll
   for (int kk = 0; kk < 8; ++kk) {
     S.wf[kk][lane] = state.w[s][t][8 * g + kk];
-    T.wi[kk] = state.w_int[s][t][8 * g + kk];
+    T.gp[kk] = pack_groups(state.w_int[s][t][8 * g + kk]);
   }
   T.sat = 0;
   // history -> ring slot 1 (the slot block 0 treats as "previous")
@@ -459,7 +467,7 @@ __global__ void __launch_bounds__(AEQ_WARPS * 32, AEQ_MIN_CTAS) k_aeq_process(fn
 #pragma unroll
   for (int kk = 0; kk < 8; ++kk) {
     state.w[s][t][8 * g + kk] = S.wf[kk][lane];
-    state.w_int[s][t][8 * g + kk] = T.wi[kk];
+    state.w_int[s][t][8 * g + kk] = 128 * unpack_group(T.gp[kk], 0) + unpack_group(T.gp[kk], 1);
   }
   if (io.n_blocks > 0) {
     state.hist[tq][iq] = v0;
@@ -487,7 +495,7 @@ __global__ void k_aeq_update_once(fntgpu_aeq_state* st, const __grid_constant__ 
 #pragma unroll
   for (int kk = 0; kk < 8; ++kk) {
     S.wf[kk][lane] = st->w[s][t][8 * g + kk];
-    T.wi[kk] = st->w_int[s][t][8 * g + kk];
+    T.gp[kk] = pack_groups(st->w_int[s][t][8 * g + kk]);
   }
   T.sat = 0;
   if (s == 0 && g == 0) {
@@ -503,7 +511,7 @@ __global__ void k_aeq_update_once(fntgpu_aeq_state* st, const __grid_constant__ 
 #pragma unroll
   for (int kk = 0; kk < 8; ++kk) {
     st->w[s][t][8 * g + kk] = S.wf[kk][lane];
-    st->w_int[s][t][8 * g + kk] = T.wi[kk];
+    st->w_int[s][t][8 * g + kk] = 128 * unpack_group(T.gp[kk], 0) + unpack_group(T.gp[kk], 1);
   }
   long long sat = T.sat;
 #pragma unroll

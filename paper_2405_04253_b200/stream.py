@@ -246,3 +246,33 @@ class HostChain:
         self.y.copy_(self.chain.y, non_blocking=True)
         self.err.copy_(self.chain.err, non_blocking=True)
         return self.y, self.err
+
+
+class HostCdc:
+    """FNT-CDC over host buffers: pinned int8 I/Q in -> H2D -> fntgpu_cdc64_process
+    -> D2H int16 I/Q out (the decoded outputs of process_int, which fit int16
+    within the engine's Eq. (5) budget). Used for the config-4 end-to-end number."""
+
+    def __init__(self, engine: FntCdcEngine, n_streams: int, length: int):
+        t = _t()
+        dev = _lib.device()
+        if engine.budget.bound > 32767:
+            raise NotImplementedError("int16 outputs need an Eq. (5) bound <= 32767")
+        self.bank = CdcBank(engine)
+        self.L = length
+        self.dxr = t.empty((n_streams, length), dtype=t.int8, device=dev)
+        self.dxi = t.empty_like(self.dxr)
+        self.dyr = t.empty((n_streams, length), dtype=t.int16, device=dev)
+        self.dyi = t.empty_like(self.dyr)
+        self.yr = t.empty((n_streams, length), dtype=t.int16, pin_memory=True)
+        self.yi = t.empty_like(self.yr, pin_memory=True)
+        self.h2d_bytes = 2 * self.dxr.numel()
+        self.d2h_bytes = 4 * self.dyr.numel()
+
+    def __call__(self, xr_host, xi_host):
+        self.dxr.copy_(xr_host, non_blocking=True)
+        self.dxi.copy_(xi_host, non_blocking=True)
+        self.bank.run(self.dxr, self.dxi, length=self.L, yr=self.dyr, yi=self.dyi)
+        self.yr.copy_(self.dyr, non_blocking=True)
+        self.yi.copy_(self.dyi, non_blocking=True)
+        return self.yr, self.yi

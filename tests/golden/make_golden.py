@@ -440,6 +440,55 @@ def gen_c3() -> dict:
     return {str(k): v for k, v in res.items()}
 
 
+def gen_cli() -> dict:
+    """Reference CLI outputs (cli.py:135-318): selftest (+ fault injection),
+    complexity --measure, transform / convolve on small files."""
+    import contextlib
+    import io
+    import tempfile
+    from fntdsp import cli
+    out = {}
+
+    def run(argv):
+        buf = io.StringIO()
+        with contextlib.redirect_stdout(buf):
+            rc = cli.main(argv)
+        return rc, buf.getvalue()
+
+    for key, argv in (("selftest", ["selftest"]), ("selftest_fault", ["selftest", "--fault-inject"]),
+                      ("complexity", ["complexity"]), ("complexity_measure", ["complexity", "--measure"])):
+        rc, text = run(argv)
+        out[key] = {"rc": rc, "stdout": text}
+    rng = np.random.default_rng(606)
+    with tempfile.TemporaryDirectory() as d:
+        d = Path(d)
+        x = rng.integers(-15, 16, 64)
+        h = rng.integers(-31, 32, 64)
+        h[20:] = 0
+        np.savetxt(d / "x.txt", x, fmt="%d")
+        np.savetxt(d / "h.txt", h, fmt="%d")
+        np.savetxt(d / "xc.txt", rng.integers(-15, 16, (64, 2)), fmt="%d")
+        hc = rng.integers(-15, 16, (64, 2))
+        hc[16:] = 0
+        np.savetxt(d / "hc.txt", hc, fmt="%d")
+        np.savetxt(d / "x32.txt", rng.integers(0, 65537, 32), fmt="%d")
+        np.savetxt(d / "big.txt", np.full(64, 30000), fmt="%d")
+        files = {k: (d / f"{k}.txt").read_text() for k in ("x", "h", "xc", "hc", "x32", "big")}
+        res = {}
+        for key, argv in (
+                ("fnt", ["transform", "--plan", "cdc64", "--input", str(d / "x.txt"), "--output", str(d / "o.txt")]),
+                ("ifnt", ["transform", "--plan", "aeq32", "--inverse", "--input", str(d / "x32.txt"), "--output", str(d / "o.txt")]),
+                ("conv", ["convolve", "--plan", "cdc64", "--x", str(d / "x.txt"), "--h", str(d / "h.txt"), "--output", str(d / "o.txt")]),
+                ("convc", ["convolve", "--plan", "cdc64", "--mode", "complex", "--x", str(d / "xc.txt"), "--h", str(d / "hc.txt"), "--output", str(d / "o.txt")]),
+                ("overflow", ["convolve", "--plan", "cdc64", "--x", str(d / "big.txt"), "--h", str(d / "h.txt"), "--output", str(d / "o2.txt")])):
+            rc, _ = run(argv)
+            res[key] = {"rc": rc, "out": (d / "o.txt").read_text()}
+        out["files"] = files
+        out["runs"] = res
+    (OUT / "cli.json").write_text(json.dumps(out, indent=1))
+    return {"n": len(out)}
+
+
 def main() -> None:
     ap = argparse.ArgumentParser()
     ap.add_argument("--big", action="store_true", help="also run config 3 (minutes)")
@@ -466,6 +515,8 @@ def main() -> None:
         digests["cdc"] = gen_cdc()
     if want("aeq"):
         digests["aeq"] = gen_aeq()
+    if want("cli"):
+        gen_cli()
     if args.big:
         digests["c3"] = gen_c3()
     digests["_generator"] = {"numpy": np.__version__, "fntdsp": fntdsp.__version__}

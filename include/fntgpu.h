@@ -143,6 +143,14 @@ typedef struct fntgpu_cdc_io {
    * stream s and phase p = (global index & 1): acc[(s*2+p)*4 + 0] += sum |y|^2,
    * acc[... + 1..3] += 32-bit limbs of sum |y|^4 (exact integer sums). */
   unsigned long long* decim_acc;
+  /* optional exact integer form of the requantization, valid when
+   * q_scale * inv_scale == 2^-q_shift up to rounding (q_scale = the engine's
+   * signal scale, tap scale 2^q_shift, cdc.py:80-86): q = round_half_away(y / 2^k)
+   * except for exact ties |y| = 2^(k-1) + j 2^k, whose float64 results the caller
+   * precomputes in q_tie[j] (j <= q_max). q_shift = -1 selects the float64 path. */
+  int32_t q_shift;
+  int32_t pad2;
+  int8_t q_tie[128];
 } fntgpu_cdc_io;
 
 /* process_int / process (cdc.py:165-180), any output sub-range of any number

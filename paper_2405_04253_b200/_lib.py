@@ -45,7 +45,8 @@ class CdcIO(C.Structure):
                 ("out_dtype", C.c_int32), ("pad0", C.c_int32),
                 ("yr", vp), ("yi", vp), ("y_stride", C.c_int64), ("inv_scale", C.c_double),
                 ("qr", vp), ("qi", vp), ("q_stride", C.c_int64), ("q_scale", C.c_double),
-                ("q_max", C.c_int32), ("pad1", C.c_int32), ("decim_acc", vp)]
+                ("q_max", C.c_int32), ("pad1", C.c_int32), ("decim_acc", vp),
+                ("q_shift", C.c_int32), ("pad2", C.c_int32), ("q_tie", C.c_int8 * 128)]
 
 
 class DecimIO(C.Structure):

@@ -77,7 +77,133 @@ __device__ __forceinline__ void stage_plane(TS* dst, const TIN* src, int64_t g0,
   }
 }
 
-template <typename TIN>
+// Exact integer form of the AEQ-input requantization q = quantize_real(y * inv, q_scale)
+// when inv * q_scale == 2^-k up to rounding: the float64 product is within 3 ulp of
+// y / 2^k, so round-half-away agrees with the exact rounding except at exact ties
+// |y| = 2^(k-1) + j 2^k, whose float64 outcome the host precomputed (io.q_tie).
+__device__ __forceinline__ int32_t requant_int(int32_t y, int k, const int8_t* tie, int qmax) {
+  const int32_t a = abs(y);
+  const int32_t base = a >> k;
+  const int32_t rem = a & ((1 << k) - 1);
+  const int32_t half = 1 << (k - 1);
+  int32_t q = base + (rem > half ? 1 : 0);
+  if (rem == half) q = tie[base < qmax ? base : qmax];
+  q = q < qmax ? q : qmax;
+  return y < 0 ? -q : q;
+}
+
+// Chain epilogue: 4 consecutive outputs per thread, 32-bit indices, packed int8 /
+// int16 stores, 32-bit |y|^2 and IMAD.WIDE |y|^4 statistics. Preconditions checked
+// on the host (launch_cdc64): out_dtype in {NONE, I16}, q_shift >= 1 when
+// requantizing, (c + out_first) % 4 == 0 and 4-byte aligned planes and strides.
+__device__ __forceinline__ void cdc_epilogue_fast(const CdcArgs& A, const uint32_t* s_u, int s,
+                                                  int64_t n0, int lo, int hi) {
+  const fntgpu_cdc_io& io = A.io;
+  const int tid = threadIdx.x;
+  const int64_t base_o = n0 - io.out_first;  // output index of local index 0
+  int8_t* qr = io.qr ? io.qr + s * io.q_stride + base_o : nullptr;
+  int8_t* qi = io.qr ? io.qi + s * io.q_stride + base_o : nullptr;
+  int16_t* yr = io.out_dtype == FNTGPU_I16 ? reinterpret_cast<int16_t*>(io.yr) + s * io.y_stride + base_o : nullptr;
+  int16_t* yi = io.out_dtype == FNTGPU_I16 ? reinterpret_cast<int16_t*>(io.yi) + s * io.y_stride + base_o : nullptr;
+  const bool stats = io.decim_acc != nullptr;
+  const int k = io.q_shift, qmax = io.q_max;
+  const int8_t* tie = io.q_tie;
+  // accumulators for even (A) and odd (B) local indices
+  unsigned long long a2 = 0, b2 = 0, a4 = 0, b4 = 0;
+  uint32_t a4h = 0, b4h = 0;
+  for (int v = 4 * tid; v < CDC_BLK * CDC_HOP; v += 4 * CDC_CTA) {
+    if (v + 4 <= lo || v >= hi) continue;
+    const bool full = v >= lo && v + 4 <= hi;
+    const int rb = (v >> 5) * UP + (v & 31);
+    int32_t zr[4], zi[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const uint32_t up = s_u[rb + e], um = s_u[CDC_BLK * UP + rb + e];
+      zr[e] = f4_signed(m_add(up, um));
+      zi[e] = f4_signed(m_rot(m_sub(up, um), 24));
+    }
+    if (qr) {
+      uint32_t pr = 0, pi = 0;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        pr |= ((uint32_t)requant_int(zr[e], k, tie, qmax) & 0xffu) << (8 * e);
+        pi |= ((uint32_t)requant_int(zi[e], k, tie, qmax) & 0xffu) << (8 * e);
+      }
+      if (full) {
+        *reinterpret_cast<uint32_t*>(qr + v) = pr;
+        *reinterpret_cast<uint32_t*>(qi + v) = pi;
+      } else {
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+          if (v + e >= lo && v + e < hi) {
+            qr[v + e] = (int8_t)(pr >> (8 * e));
+            qi[v + e] = (int8_t)(pi >> (8 * e));
+          }
+      }
+    }
+    if (yr) {
+      if (full) {
+        *reinterpret_cast<uint2*>(yr + v) = make_uint2(((uint32_t)zr[0] & 0xffffu) | ((uint32_t)zr[1] << 16),
+                                                       ((uint32_t)zr[2] & 0xffffu) | ((uint32_t)zr[3] << 16));
+        *reinterpret_cast<uint2*>(yi + v) = make_uint2(((uint32_t)zi[0] & 0xffffu) | ((uint32_t)zi[1] << 16),
+                                                       ((uint32_t)zi[2] & 0xffffu) | ((uint32_t)zi[3] << 16));
+      } else {
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+          if (v + e >= lo && v + e < hi) {
+            yr[v + e] = (int16_t)zr[e];
+            yi[v + e] = (int16_t)zi[e];
+          }
+      }
+    }
+    if (stats) {
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const bool ok = full || (v + e >= lo && v + e < hi);
+        const uint32_t m2 = ok ? (uint32_t)(zr[e] * zr[e]) + (uint32_t)(zi[e] * zi[e]) : 0u;  // <= 2^31
+        const unsigned long long m4 = (unsigned long long)m2 * m2;                          // < 2^62
+        if (e & 1) {
+          b2 += m2;
+          b4 += m4;
+          b4h += (b4 < m4);
+        } else {
+          a2 += m2;
+          a4 += m4;
+          a4h += (a4 < m4);
+        }
+      }
+    }
+  }
+  if (stats) {
+    // even local indices carry phase (n0 & 1), odd ones the other phase
+    const int pa = (int)(n0 & 1);
+    const unsigned long long va[4] = {a2, a4 & 0xffffffffull, a4 >> 32, a4h};
+    const unsigned long long vb[4] = {b2, b4 & 0xffffffffull, b4 >> 32, b4h};
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      unsigned long long x = va[q], y = vb[q];
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) {
+        x += __shfl_xor_sync(0xffffffffu, x, off);
+        y += __shfl_xor_sync(0xffffffffu, y, off);
+      }
+      if ((tid & 31) == 0) {
+        if (x) atomicAdd(io.decim_acc + ((int64_t)s * 2 + pa) * 4 + q, x);
+        if (y) atomicAdd(io.decim_acc + ((int64_t)s * 2 + (pa ^ 1)) * 4 + q, y);
+      }
+    }
+  }
+}
+
+// sign-extended byte k of w: PRMT with the selector's sign-replication bit
+__device__ __forceinline__ int32_t sx8(uint32_t w, int k) {
+  int32_t r;
+  const uint32_t sel = (uint32_t)k | ((uint32_t)(k | 8) << 4) | ((uint32_t)(k | 8) << 8) | ((uint32_t)(k | 8) << 12);
+  asm("prmt.b32 %0, %1, 0, %2;" : "=r"(r) : "r"(w), "r"(sel));
+  return r;
+}
+
+template <typename TIN, bool FAST>
 __global__ void __launch_bounds__(CDC_CTA) k_cdc64(const __grid_constant__ CdcArgs A) {
   using TS = typename std::conditional<sizeof(TIN) == 1, int8_t, int32_t>::type;
   constexpr int IN_BYTES = 2 * WIN * (int)sizeof(TS);
@@ -121,7 +247,7 @@ __global__ void __launch_bounds__(CDC_CTA) k_cdc64(const __grid_constant__ CdcAr
           for (int k = 0; k < 4; ++k) {
             const int i = q * 16 + w * 4 + k;
             // x_r +- 2^8 x_i + bias (bias = 256 F4 keeps the word non-negative)
-            a[bitrev(i, 6)] = (uint32_t)(sext8(rw[w], k) + (int32_t)F4_BIAS + m256 * sext8(iw[w], k));
+            a[bitrev(i, 6)] = (uint32_t)(sx8(rw[w], k) + (int32_t)F4_BIAS + m256 * sx8(iw[w], k));
           }
       }
     } else {
@@ -150,6 +276,10 @@ __global__ void __launch_bounds__(CDC_CTA) k_cdc64(const __grid_constant__ CdcAr
   const int64_t o_lo = io.out_first, o_hi = io.out_first + io.out_count;
   lo = lo < o_lo ? o_lo : lo;
   hi = hi > o_hi ? o_hi : hi;
+  if (FAST) {
+    cdc_epilogue_fast(A, s_u, s, n0, (int)(lo - n0), (int)(hi - n0));
+    return;
+  }
   // n advances by CDC_CTA (even): each thread only ever sees one sampling phase
   const int my_ph = (int)((lo + tid) & 1);
   unsigned long long s2 = 0, s4lo = 0, s4hi = 0;
@@ -260,10 +390,22 @@ cudaError_t launch_cdc64(const fntgpu_cdc_taps& taps, const fntgpu_cdc_io& io, c
   A.blk_begin = b_lo;
   A.blk_count = b_hi - b_lo + 1;
   dim3 grid((unsigned)((A.blk_count + CDC_BLK - 1) / CDC_BLK), (unsigned)io.n_streams);
+  // vectorised epilogue preconditions (see cdc_epilogue_fast)
+  auto al4 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 3) == 0; };
+  bool fast = (io.out_dtype == FNTGPU_NONE || io.out_dtype == FNTGPU_I16) &&
+              ((A.c + io.out_first) % 4 == 0);
+  if (io.qr) fast = fast && io.q_shift >= 1 && io.q_shift < 31 && al4(io.qr) && al4(io.qi) &&
+                    io.q_stride % 4 == 0 && io.q_max <= 127;
+  if (io.out_dtype == FNTGPU_I16)
+    fast = fast && (reinterpret_cast<uintptr_t>(io.yr) & 7) == 0 &&
+           (reinterpret_cast<uintptr_t>(io.yi) & 7) == 0 && io.y_stride % 4 == 0;
   switch (io.in_dtype) {
-    case FNTGPU_I8: k_cdc64<int8_t><<<grid, CDC_CTA, 0, st>>>(A); break;
-    case FNTGPU_I32: k_cdc64<int32_t><<<grid, CDC_CTA, 0, st>>>(A); break;
-    case FNTGPU_I64: k_cdc64<int64_t><<<grid, CDC_CTA, 0, st>>>(A); break;
+    case FNTGPU_I8:
+      if (fast) k_cdc64<int8_t, true><<<grid, CDC_CTA, 0, st>>>(A);
+      else k_cdc64<int8_t, false><<<grid, CDC_CTA, 0, st>>>(A);
+      break;
+    case FNTGPU_I32: k_cdc64<int32_t, false><<<grid, CDC_CTA, 0, st>>>(A); break;
+    case FNTGPU_I64: k_cdc64<int64_t, false><<<grid, CDC_CTA, 0, st>>>(A); break;
     default: return cudaErrorInvalidValue;
   }
   return cudaGetLastError();

@@ -53,6 +53,24 @@ class CdcBank:
         self.taps = engine.c_taps()
         self.inv_scale = 1.0 / engine.output_scale
 
+    def _exact_requant(self, io, q_spec) -> None:
+        """Integer requantization when (y * (1/output_scale)) * q_scale == y / 2^k up to
+        rounding: q_scale is the engine's signal scale and its tap scale is 2^k
+        (quantize_taps, cdc.py:80-86). The float64 results of the exact ties
+        |y| = 2^(k-1) + j 2^k are evaluated here with the reference's expression."""
+        import math
+        ts = float(self.engine.tap_scale)
+        k = int(round(math.log2(ts))) if ts > 0 else 0
+        if (float(q_spec.scale) != float(self.engine.sig_spec.scale) or 2.0 ** k != ts
+                or not 1 <= k <= 30 or q_spec.max_int > 127):
+            return
+        inv = self.inv_scale
+        for j in range(int(q_spec.max_int) + 1):
+            y = float((1 << (k - 1)) + j * (1 << k))
+            v = (y * inv) * float(q_spec.scale)  # quantize_real on y * (1/output_scale)
+            io.q_tie[j] = min(int(math.floor(abs(v) + 0.5)), int(q_spec.max_int))
+        io.q_shift = k
+
     def run(self, xr, xi, *, length: int | None = None, x_first: int = 0,
             out_first: int = 0, out_count: int | None = None, yr=None, yi=None,
             qr=None, qi=None, q_spec=None, decim_acc=None, stream=None) -> None:
@@ -78,11 +96,13 @@ class CdcBank:
             io.yr = yr.data_ptr()
             io.yi = yi.data_ptr() if yi is not None else None
             io.y_stride = yr.stride(0)
+        io.q_shift = -1
         if qr is not None:
             io.qr, io.qi = qr.data_ptr(), qi.data_ptr()
             io.q_stride = qr.stride(0)
             io.q_scale = float(q_spec.scale)
             io.q_max = int(q_spec.max_int)
+            self._exact_requant(io, q_spec)
         if decim_acc is not None:
             io.decim_acc = decim_acc.data_ptr()
         lib = _lib.load()

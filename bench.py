@@ -51,6 +51,16 @@ AEQ_INT_OPS_PER_BLOCK_DIRECT = 2 * 4096 + 448               # 8640 (exact time-d
 AEQ_FP64_OPS_PER_BLOCK = 2 * 4096 + 256 * 4 + 64 * 2 + 32 * 12  # gradient + update + y + rde ~ 9728
 
 
+def allreduce(vals, op: str) -> list:
+    """Reduce floats over ranks (device tensors under NCCL, CPU tensors under gloo)."""
+    import torch
+    import torch.distributed as dist
+    dev = "cpu" if dist.get_backend() == "gloo" else "cuda"
+    t = torch.tensor(vals, dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX if op == "max" else dist.ReduceOp.SUM)
+    return t.tolist()
+
+
 def measured_peaks() -> dict:
     peaks = {}
     p = ROOT / "MEASURED_PEAKS.json"
@@ -283,6 +293,7 @@ def main():
                     help="c5: many-channel CDC+AEQ chain (headline); c4: throughput-scale CDC")
     ap.add_argument("--c4-samples", type=int, default=1 << 31, help="C4 samples per polarization")
     ap.add_argument("--no-alt", action="store_true", help="skip the direct-forward AEQ comparison")
+    ap.add_argument("--no-quality", action="store_true", help="skip the on-device BER/EVM scoring")
     args = ap.parse_args()
     if args.impl == "reference":
         impl_reference(args)
@@ -293,9 +304,16 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # one process per GPU; FNT_BENCH_BACKEND=gloo lets several ranks share a GPU for a
+    # functional smoke test of the multi-rank path (reductions on CPU tensors)
+    backend = os.environ.get("FNT_BENCH_BACKEND", "nccl")
+    local = local % max(torch.cuda.device_count(), 1)
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
 
     import paper_2405_04253_b200 as P
     from paper_2405_04253_b200 import _lib
@@ -313,7 +331,7 @@ def main():
     eng = P.FntCdcEngine(cfg.cdc_config("fnt"), cfg.sig_spec())
     L = 2 * args.symbols
     gen = DeviceLinkGenerator(args.symbols, z_km=cfg.z_km, sig_scale=cfg.sig_scale)
-    xr, xi = gen.generate(args.links, seed=4 + 7919 * rank)
+    xr, xi, sidx = gen.generate(args.links, seed=4 + 7919 * rank, symbols=True)
     chain = CdcAeqChain(eng, cfg.aeq_config(), args.links, L, cfg.sig_spec(), cfg.mu_schedule(),
                         forward=fwd)
     torch.cuda.synchronize()
@@ -367,11 +385,8 @@ def main():
     aeq_ms = float(np.mean([e[2].elapsed_time(e[3]) for e in ev]))
     samples_rank = args.steps * args.links * 2 * L
     if world > 1:
-        t = torch.tensor([ms, float(samples_rank)], dtype=torch.float64, device="cuda")
-        mx = t.clone()
-        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
-        dist.all_reduce(t, op=dist.ReduceOp.SUM)
-        ms_max, samples_all = float(mx[0]), float(t[1])
+        ms_max = allreduce([ms], "max")[0]
+        samples_all = allreduce([float(samples_rank)], "sum")[0]
     else:
         ms_max, samples_all = ms, float(samples_rank)
     value = samples_all / (ms_max * 1e-3) / 1e9
@@ -432,6 +447,28 @@ def main():
         "outputs_finite": ok,
     }
 
+    # link quality of the timed step's outputs, scored on the device (metrology.py;
+    # outside the timed region). Expected to be poor at 75 km: 32 CDC taps cover the
+    # dispersion badly and the reference's RDE does not converge (SURVEY finding 4).
+    if not args.no_quality:
+        from paper_2405_04253_b200 import metrology as M
+        bers, evms, oks = [], [], []
+        for c0 in range(0, args.links, 32):
+            c1 = min(args.links, c0 + 32)
+            sym, bits = gen.tx_reference(sidx[c0:c1])
+            b, e, o = M.align_and_count(M.aeq_to_pols(chain.y[c0:c1]), sym, bits,
+                                        cfg.discard_symbols)
+            bers.append(b)
+            evms.append(e)
+            oks.append(o)
+        bers, evms, oks = np.concatenate(bers), np.concatenate(evms), np.concatenate(oks)
+        line["link_quality"] = {
+            "ber_mean": float(bers.mean()), "ber_min": float(bers.min()),
+            "evm_db_mean": float(evms[oks].mean()) if oks.any() else None,
+            "aligned_fraction": float(oks.mean()),
+            "note": "BER/EVM of every link computed on the GPU (metrology.align_and_count); "
+                    "high BER at 75 km reproduces the reference's behaviour (SURVEY finding 4)"}
+
     # the exact-equivalent time-domain forward (FNTGPU_AEQ_FWD_DIRECT, same bits) on the
     # same resident data, reported beside the FNT-domain headline
     if fwd == _lib.AEQ_FWD_FNT and not args.no_alt:
@@ -448,9 +485,7 @@ def main():
         torch.cuda.synchronize()
         ms_alt = a.elapsed_time(b)
         if world > 1:
-            t = torch.tensor([ms_alt], dtype=torch.float64, device="cuda")
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            ms_alt = float(t[0])
+            ms_alt = allreduce([ms_alt], "max")[0]
         line["aeq_forward_direct"] = {
             "value": samples_all / (ms_alt * 1e-3) / 1e9, "unit": UNIT,
             "ms_per_step": ms_alt / args.steps,
@@ -559,9 +594,7 @@ def run_c4(args, world, rank, local):
     ms = a.elapsed_time(b)
     ms_max = ms
     if world > 1:
-        t = torch.tensor([ms], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms_max = float(t[0])
+        ms_max = allreduce([ms], "max")[0]
     samples = 2 * L  # both polarizations of the whole stream, all ranks
     value = args.steps * samples / (ms_max * 1e-3) / 1e9
     peaks = measured_peaks()
@@ -606,9 +639,7 @@ def run_c4(args, world, rank, local):
         torch.cuda.synchronize()
         ms_e = a.elapsed_time(b)
         if world > 1:
-            t = torch.tensor([ms_e], dtype=torch.float64, device="cuda")
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            ms_e = float(t[0])
+            ms_e = allreduce([ms_e], "max")[0]
         line["e2e"] = {"value": args.steps * 2 * n * world / (ms_e * 1e-3) / 1e9, "unit": UNIT,
                        "h2d_bytes_per_step": hc.h2d_bytes, "d2h_bytes_per_step": hc.d2h_bytes,
                        "path": "stream.HostCdc: pinned host int8 I/Q -> H2D -> fntgpu_cdc64_process "
@@ -644,9 +675,7 @@ def run_e2e(args, eng, cfg, xr, xi, fwd, world):
     torch.cuda.synchronize()
     ms = a.elapsed_time(b)
     if world > 1:
-        t = torch.tensor([ms], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t[0])
+        ms = allreduce([ms], "max")[0]
     samples = args.steps * n * 2 * L * world
     return {"value": samples / (ms * 1e-3) / 1e9, "unit": UNIT,
             "h2d_bytes_per_step": hc.h2d_bytes, "d2h_bytes_per_step": hc.d2h_bytes,

@@ -72,9 +72,12 @@ class DeviceLinkGenerator:
         self.levels = t.tensor([-3.0, -1.0, 3.0, 1.0], dtype=t.float64, device=dev) / math.sqrt(10.0)
 
     def generate(self, n_links: int, seed: int, snr_db=(16.0, 22.0), chunk: int = 32,
-                 out=None):
+                 out=None, symbols: bool = False):
         """Returns (xr, xi): (2*n_links, L) int8 device tensors; row 2l = pol X of
-        link l, row 2l+1 = pol Y. Deterministic for a given (seed, link index)."""
+        link l, row 2l+1 = pol Y. Deterministic for a given (seed, link index).
+        With symbols=True also returns the transmitted symbol indices
+        (n_links, 2, n_sym) uint8 = 4*li_I + li_Q with Gray level index li = 2 b0 + b1
+        (the reference's bits_to_symbols, linksim.py:107-112)."""
         t = _lib.torch()
         dev = _lib.device()
         L = self.L
@@ -83,21 +86,35 @@ class DeviceLinkGenerator:
             xi = t.empty((2 * n_links, L), dtype=t.int8, device=dev)
         else:
             xr, xi = out
+        sidx = t.empty((n_links, 2, self.n_sym), dtype=t.uint8, device=dev) if symbols else None
         for c0 in range(0, n_links, chunk):
             c = min(chunk, n_links - c0)
             g = t.Generator(device=dev)
             g.manual_seed(int(seed) * 1_000_003 + c0)
-            xq_r, xq_i = self._chunk(c, g, snr_db)
+            xq_r, xq_i, li = self._chunk(c, g, snr_db)
             xr[2 * c0:2 * (c0 + c)] = xq_r.reshape(2 * c, L)
             xi[2 * c0:2 * (c0 + c)] = xq_i.reshape(2 * c, L)
-        return xr, xi
+            if symbols:
+                sidx[c0:c0 + c] = li
+        return (xr, xi, sidx) if symbols else (xr, xi)
+
+    def tx_reference(self, sidx):
+        """Symbol indices -> (symbols complex128, bits int8 (..., 4)) on the device."""
+        t = _lib.torch()
+        li_i = (sidx >> 2).long()
+        li_q = (sidx & 3).long()
+        sym = t.complex(self.levels[li_i], self.levels[li_q])
+        bits = t.stack([li_i >> 1, li_i & 1, li_q >> 1, li_q & 1], dim=-1).to(t.int8)
+        return sym, bits
 
     def _chunk(self, c: int, g, snr_db):
         t = _lib.torch()
         dev = _lib.device()
         L, n = self.L, self.n_sym
-        sym_i = self.levels[t.randint(0, 4, (c, 2, n), generator=g, device=dev)]
-        sym_q = self.levels[t.randint(0, 4, (c, 2, n), generator=g, device=dev)]
+        li_i = t.randint(0, 4, (c, 2, n), generator=g, device=dev)
+        li_q = t.randint(0, 4, (c, 2, n), generator=g, device=dev)
+        sym_i = self.levels[li_i]
+        sym_q = self.levels[li_q]
         up = t.zeros((c, 2, L), dtype=t.complex128, device=dev)
         up[..., ::self.sps] = t.complex(sym_i, sym_q)
         w = t.fft.ifft(t.fft.fft(up) * self.H_tx)
@@ -133,4 +150,4 @@ class DeviceLinkGenerator:
             v = v * self.sig_scale
             v = t.sign(v) * t.floor(v.abs() + 0.5)
             return v.clamp(-self.max_int, self.max_int).to(t.int8)
-        return quant(m.real), quant(m.imag)
+        return quant(m.real), quant(m.imag), (4 * li_i + li_q).to(t.uint8)

@@ -51,6 +51,13 @@ int fntgpu_abi_version(void);
 const char* fntgpu_last_error(void);
 /* number of visible CUDA devices (0 -> every compute call fails) */
 int fntgpu_device_count(void);
+/* Plumbing for the host-buffer (end-to-end) path: a strided 2-D copy of `height`
+ * rows of `width` bytes (row pitches in bytes) between host and device memory,
+ * asynchronous on `stream` (cudaMemcpy2DAsync with cudaMemcpyDefault). Lets a
+ * time segment of the (links, 4, n) float64 equalizer output stream back while
+ * the next segment is computed. */
+int fntgpu_copy2d_async(void* dst, int64_t dpitch, const void* src, int64_t spitch,
+                        int64_t width, int64_t height, void* stream);
 
 /* ------------------------------------------------------------------------ */
 /* Transform plans -- TransformPlan / make_plan (fnt.py:24-33, 60-83).        */
@@ -232,6 +239,14 @@ int fntgpu_aeq_process(fntgpu_aeq_state* state, const fntgpu_aeq_params* params,
 int fntgpu_aeq_update_taps(fntgpu_aeq_state* state, const fntgpu_aeq_params* params,
                            const int64_t* x_block, const double* y, double mu, double* err,
                            void* stream);
+/* Self-check of the AEQ kernel's two arithmetic shortcuts for these params (no
+ * reference counterpart; used by the tests and the CLI selftest): over every int32
+ * numerator in [lo, hi), y = y_int / D by reciprocal + one correction step against
+ * IEEE division, and for r2 = y^2 + y'^2 on a dense sweep the threshold ring decision
+ * against sqrt + first argmin. mismatches: device uint64[2] {division, ring},
+ * accumulated (caller zeroes). */
+int fntgpu_aeq_selfcheck(const fntgpu_aeq_params* params, int64_t lo, int64_t hi,
+                         unsigned long long* mismatches, void* stream);
 
 #ifdef __cplusplus
 }

@@ -98,6 +98,8 @@ SIGNATURES = {
     "fntgpu_aeq_init": (C.c_int, [vp, C.c_int, C.POINTER(AeqParams), vp]),
     "fntgpu_aeq_process": (C.c_int, [vp, C.POINTER(AeqParams), C.POINTER(AeqIO), vp]),
     "fntgpu_aeq_update_taps": (C.c_int, [vp, C.POINTER(AeqParams), vp, vp, C.c_double, vp, vp]),
+    "fntgpu_copy2d_async": (C.c_int, [vp, C.c_int64, vp, C.c_int64, C.c_int64, C.c_int64, vp]),
+    "fntgpu_aeq_selfcheck": (C.c_int, [C.POINTER(AeqParams), C.c_int64, C.c_int64, vp, vp]),
 }
 
 _LIB = None

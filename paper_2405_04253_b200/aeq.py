@@ -98,6 +98,19 @@ def aeq_params(config: AeqConfig, forward: int | None = None) -> _lib.AeqParams:
     return prm
 
 
+def aeq_selfcheck(config: AeqConfig, lo: int = -(1 << 31), hi: int = 1 << 31) -> tuple[int, int]:
+    """Device self-check of the equalizer's division and ring-decision shortcuts for
+    this config (fntgpu_aeq_selfcheck): (division mismatches over every int32 y_int
+    in [lo, hi), ring-decision mismatches). Both must be 0."""
+    t = _lib.torch()
+    out = t.zeros(2, dtype=t.int64, device=_lib.device())
+    prm = aeq_params(config)
+    _lib.check(_lib.load().fntgpu_aeq_selfcheck(C.byref(prm), int(lo), int(hi), _lib.ptr(out),
+                                                 _lib.stream_handle()), "aeq_selfcheck")
+    d, r = out.cpu().tolist()
+    return int(d), int(r)
+
+
 def mu_block_array(n_blocks: int, hop: int, mu_schedule, default_mu: float) -> np.ndarray:
     """mu of each block: mu_schedule(b * hop), or config.mu (aeq.py:187-188)."""
     if mu_schedule is None:

@@ -15,6 +15,8 @@ namespace fntgpu {
 cudaError_t launch_aeq_update_once(fntgpu_aeq_state* st, const fntgpu_aeq_params& prm,
                                    const int64_t* xblk, const double* y, double mu, double* err,
                                    cudaStream_t s);
+cudaError_t launch_aeq_selfcheck(const fntgpu_aeq_params& prm, int64_t lo, int64_t hi,
+                                 unsigned long long* mismatches, cudaStream_t s);
 }
 
 using namespace fntgpu;
@@ -74,6 +76,17 @@ int fntgpu_device_count(void) {
   int n = 0;
   if (cudaGetDeviceCount(&n) != cudaSuccess) return 0;
   return n;
+}
+
+int fntgpu_copy2d_async(void* dst, int64_t dpitch, const void* src, int64_t spitch,
+                        int64_t width, int64_t height, void* stream) {
+  if (!dst || !src) return fail(FNTGPU_EINVAL, "copy2d_async: NULL argument");
+  if (width < 0 || height < 0 || dpitch < width || spitch < width)
+    return fail(FNTGPU_EINVAL, "copy2d_async: bad extent");
+  if (width == 0 || height == 0) return FNTGPU_OK;
+  return cuda_rc(cudaMemcpy2DAsync(dst, (size_t)dpitch, src, (size_t)spitch, (size_t)width,
+                                   (size_t)height, cudaMemcpyDefault, S(stream)),
+                 "copy2d_async");
 }
 
 int fntgpu_plan_create(int t, int n, int64_t alpha, fntgpu_plan** out) {
@@ -357,6 +370,17 @@ int fntgpu_aeq_update_taps(fntgpu_aeq_state* st, const fntgpu_aeq_params* prm,
   if (mu < 0) return fail(FNTGPU_EINVAL, "mu must be >= 0");
   if ((rc = check_device("aeq_update_taps"))) return rc;
   return cuda_rc(launch_aeq_update_once(st, *prm, x_block, y, mu, err, S(stream)), "aeq_update_taps");
+}
+
+int fntgpu_aeq_selfcheck(const fntgpu_aeq_params* prm, int64_t lo, int64_t hi,
+                         unsigned long long* mismatches, void* stream) {
+  int rc = check_aeq_params(prm, "aeq_selfcheck");
+  if (rc) return rc;
+  if (!mismatches) return fail(FNTGPU_EINVAL, "aeq_selfcheck: NULL argument");
+  if (lo < INT32_MIN || hi > (int64_t)INT32_MAX + 1 || lo > hi)
+    return fail(FNTGPU_EINVAL, "aeq_selfcheck: range must lie within int32");
+  if ((rc = check_device("aeq_selfcheck"))) return rc;
+  return cuda_rc(launch_aeq_selfcheck(*prm, lo, hi, mismatches, S(stream)), "aeq_selfcheck");
 }
 
 }  // extern "C"

@@ -74,6 +74,16 @@ __device__ __forceinline__ int32_t f4_signed(uint32_t x) {
   return r;
 }
 
+// Canonical residue x mod F4 in [0, F4) of any 32-bit word: floor(x / 65537) =
+// umulhi(x, 0xFFFF0001) >> 16 exactly for every x < 2^32 (checked exhaustively), so
+// this is IMAD.HI + SHF + IMAD with no data-dependent correction. The signed decode
+// (fermat.py:131-133) of a residue r is (r + 32768) mod F4 - 32768: callers add the
+// 32768 before the transform or sum and subtract it after their reduction.
+__device__ __forceinline__ uint32_t f4_mod(uint32_t x) {
+  const uint32_t q = __umulhi(x, 0xFFFF0001u) >> 16;
+  return x - q * F4;
+}
+
 // Encode a signed integer |v| < 2^31 - F4*256 into Z/M with the right residue mod F4.
 // Adding a multiple of F4 keeps the residue (the mod-M class does not matter:
 // only the final mod-F4 reduction is observed).

@@ -24,9 +24,12 @@
 //   as a time-domain FIR (each group sum reduced mod F4 and decoded exactly as the
 //   residue path, so the bits are identical for every input the reference accepts).
 // Update (aeq.py:148-170): float64 with explicit __dmul_rn/__dadd_rn (never
-//   contracted into FMA), IEEE division and sqrt, numpy's einsum reduction order
+//   contracted into FMA), correctly rounded division and ring decisions, numpy's einsum reduction order
 //   over m (two lanes of even/odd m, unrolled by 4) and numpy's
 //   pairwise order for the err_trace mean.
+#include <cmath>
+#include <cstring>
+
 #include "fermat.cuh"
 #include "internal.h"
 
@@ -34,18 +37,27 @@ namespace fntgpu {
 
 constexpr int AEQ_L = 16;            // taps per filter = hop (aeq.py:45)
 constexpr int AEQ_N = 32;            // block length
-constexpr int AEQ_WARPS = 4;         // streams per CTA
+#ifndef AEQ_WARPS
+#define AEQ_WARPS 4                  // streams (warps) per CTA
+#endif
+#ifndef AEQ_LOCKSTEP
+#define AEQ_LOCKSTEP 0               // 1: the CTA's warps barrier once per block (shared I-cache lines)
+#endif
 constexpr int AEQ_TAP_MAX = 16383;   // TAP_MAG_MAX (aeq.py:26)
 constexpr int XF_LUT = 127;          // x / sig_scale table for |x| <= 127
 #ifndef AEQ_MIN_CTAS
 #define AEQ_MIN_CTAS 4               // resident CTAs per SM the register budget targets
+#endif
+#ifndef AEQ_ROLL_XFNT
+#define AEQ_ROLL_XFNT 0              // 1: keep the cooperative input-FNT stage loop rolled
 #endif
 
 struct __align__(16) AeqScratch {
   double wf[8][32];           // float taps (aeq.py:99), lane-contiguous: wf[kk][lane] = w[s][t][8g+kk]
   int32_t part[32][33];       // per-lane partial sums (direct: 16 hi + 16 lo; fnt: 16), padded
   double ey[4][AEQ_L];        // e * y per output stream
-  double xf[4][33];           // x / sig_scale ring: [t][16 * parity + j] (odd t-stride: no conflicts)
+  double xf[4][65];           // x / sig_scale ring of 32, stored twice: [t][16 * parity + j (+ 32)]
+                              // so every window is contiguous (odd t-stride: no bank conflicts)
   int32_t xi[4][2][AEQ_L];    // input integer ring: [t][block parity][j]
   uint32_t X[4][AEQ_N + 4];   // cooperative input spectra (FNT path), 16-B aligned padded rows
   double err[32];             // |e| values for the err_trace mean
@@ -55,7 +67,11 @@ struct AeqArgs {
   fntgpu_aeq_params prm;
   fntgpu_aeq_io io;
   double R2[8];               // radii[i] * radii[i] (nearest ** 2, aeq.py:58)
+  double T[8];                // ring decision thresholds on r2 (rde fast path, see rde_thresholds)
   double D;                   // sig_scale * tap_scale (aeq.py:142)
+  double Dinv;                // RN(1 / D): y = y_int / D by one Markstein correction step
+  int32_t fast_rde;           // 1: ring chosen by comparing r2 with T[] (no sqrt)
+  int32_t fast_div;           // 1: D in [2^-500, 2^500] (div_D's correction step is exact)
 };
 
 __device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a, b); }
@@ -79,8 +95,20 @@ __device__ __forceinline__ int32_t tap_group(int32_t w, int g) {
 // (16QAM, qam16_radii) is unrolled; other ring counts loop.
 __device__ __forceinline__ double rde(double yi, double yq, const AeqArgs& A) {
   const double r2 = dadd(dmul(yi, yi), dmul(yq, yq));
-  const double r = __dsqrt_rn(r2);
   double best_r2;
+  if (A.fast_rde) {
+    // argmin_i |sqrt(r2) - R_i| is a step function of r2 over the reachable range;
+    // the host located its steps exactly (rde_thresholds), so no sqrt is needed.
+    if (A.prm.n_radii == 3) {
+      best_r2 = r2 >= A.T[2] ? A.R2[2] : (r2 >= A.T[1] ? A.R2[1] : A.R2[0]);
+    } else {
+      int sel = 0;
+      for (int i = 1; i < A.prm.n_radii; ++i) sel += r2 >= A.T[i];
+      best_r2 = A.R2[sel];
+    }
+    return dsub(best_r2, r2);
+  }
+  const double r = __dsqrt_rn(r2);
   if (A.prm.n_radii == 3) {
     const double d0 = fabs(dsub(r, A.prm.radii[0]));
     const double d1 = fabs(dsub(r, A.prm.radii[1]));
@@ -104,23 +132,41 @@ __device__ __forceinline__ double rde(double yi, double yq, const AeqArgs& A) {
 // np.rint(w * tap_scale).astype(int64), then |.| > 16383 -> count and clip
 // (aeq.py:165-168). Values whose rint is not a representable int64 (|r| >= 2^63,
 // NaN) become INT64_MIN in numpy on x86-64: not counted, clipped to -16383.
-// Branch-free: fmax(NaN, -16383) = -16383 reproduces the NaN case as well.
-__device__ __forceinline__ int32_t requantize_tap(double w, double tap_scale, long long& sat) {
-  const double r = rint(dmul(w, tap_scale));
-  const double a = fabs(r);
-  const bool huge = !(a < 9.2233720368547758e18);
-  sat += (a > (double)AEQ_TAP_MAX) & !huge;
-  const int32_t c = (int32_t)fmin(fmax(r, -(double)AEQ_TAP_MAX), (double)AEQ_TAP_MAX);
+// cvt.rni.s32.f64 rounds half-to-even like np.rint and saturates, so |rint| > 16383
+// is read off the int32; |p| >= 2^63 exactly when |rint(p)| >= 2^63 (doubles there
+// are integers).
+__device__ __forceinline__ int32_t requantize_tap(double w, double tap_scale, uint32_t& sat) {
+  const double p = dmul(w, tap_scale);
+  const int32_t i = __double2int_rn(p);
+  const bool huge = !(fabs(p) < 9.2233720368547758e18);
+  sat += ((i > AEQ_TAP_MAX) | (i < -AEQ_TAP_MAX)) & !huge;
+  const int32_t c = min(max(i, -AEQ_TAP_MAX), AEQ_TAP_MAX);
   return huge ? -AEQ_TAP_MAX : c;
 }
 
-// Both 7-bit groups of a tap packed as two signed 16-bit halves:
-// low half = high group (g = 0), high half = low group (g = 1).
+// y_int / D correctly rounded: q0 = RN(y_int * RN(1/D)) is within 1 ulp of the
+// quotient, the residual y_int - q0 D is exact in one FMA, and one more FMA rounds
+// the corrected quotient (Markstein's theorem; no over/underflow for |y_int| < 2^32
+// and the D range the host admits). fntgpu_aeq_selfcheck (tests/test_gpu_parity.py)
+// checks it against IEEE division over every int32 numerator for the configured D.
+__device__ __forceinline__ double div_D(int32_t yi, const AeqArgs& A) {
+  const double a = (double)yi;
+  if (!A.fast_div) return __ddiv_rn(a, A.D);
+  const double q0 = dmul(a, A.Dinv);
+  const double r = __fma_rn(-q0, A.D, a);
+  return __fma_rn(r, A.Dinv, q0);
+}
+
+// Both 7-bit groups of a tap in one word: p = sign * (hi + lo * 2^16) with
+// hi = |w| >> 7, lo = |w| & 127 (fixedpoint.py:111-121). Since w = sign (128 hi + lo),
+// p = w * 2^16 - (w / 128) * (2^23 - 1) (C division truncates like sign * (|w| >> 7)).
+// Unpack: hi group = low 16 bits sign-extended (|hi| < 2^15); lo group =
+// (p + 2^15) >> 16 (the low half's sign borrow is cancelled by the rounding).
 __device__ __forceinline__ uint32_t pack_groups(int32_t w) {
-  return ((uint32_t)tap_group(w, 0) & 0xffffu) | ((uint32_t)tap_group(w, 1) << 16);
+  return (uint32_t)(w * 65536 - (w / 128) * 8388607);
 }
 __device__ __forceinline__ int32_t unpack_group(uint32_t p, int g) {
-  return g ? ((int32_t)p >> 16) : ((int32_t)(p << 16) >> 16);
+  return g ? ((int32_t)(p + 0x8000u) >> 16) : ((int32_t)(p << 16) >> 16);
 }
 
 // einsum("sm,tmk->stk") inner reduction over m in numpy's SSE2 order.
@@ -148,7 +194,7 @@ __device__ __forceinline__ double xf_of(int32_t x, const double* lut, double sig
 // registers, the float values in the warp's shared scratch (S.wf, lane-contiguous).
 struct LaneTaps {
   uint32_t gp[8];  // packed 7-bit groups of w_int (pack_groups); w_int = 128 hi + lo
-  long long sat;
+  uint32_t sat;    // saturations counted by this lane (flushed to 64 bits every 2^24 blocks)
 };
 
 // Exchange the e values, compute the err_trace mean (lane 0 writes *err_out when
@@ -192,16 +238,12 @@ __device__ __forceinline__ void lane_update(const AeqArgs& A, AeqScratch& S, int
       ey[2 * q] = v.x;
       ey[2 * q + 1] = v.y;
     }
-    // xf[t][j] for j = 9 - 8g ... 31 - 8g as a window that slides by one per tap:
-    // tap kk (k = 8g + kk) uses xw index q = 7 + m - kk, m = 0..15. Taps run from
-    // kk = 7 down to 0 so each step needs exactly one new value.
-    const int prev = cur ^ 1;
-    const double* xs_prev = S.xf[t] + AEQ_L * prev;
-    const double* xs_cur = S.xf[t] + AEQ_L * cur;
-    auto xload = [&](int q) -> double {
-      const int j = q + 9 - 8 * g;  // 1..31
-      return j < AEQ_L ? xs_prev[j] : xs_cur[j - AEQ_L];
-    };
+    // x_block[t][j] for j = 9 - 8g ... 31 - 8g as a window that slides by one per
+    // tap: tap kk (k = 8g + kk) uses xw index q = 7 + m - kk, m = 0..15. Taps run
+    // from kk = 7 down to 0 so each step needs exactly one new value. x_block[t][j]
+    // sits at ring position 16 * prev + j (duplicated ring: no wrap).
+    const double* xs = S.xf[t] + AEQ_L * (cur ^ 1) + 9 - 8 * g;
+    auto xload = [&](int q) -> double { return xs[q]; };
     double xw[23];
 #pragma unroll
     for (int q = 0; q < 16; ++q) xw[q] = xload(q);
@@ -243,7 +285,11 @@ __device__ __forceinline__ void warp_input_fnt(AeqScratch& S, int lane, int cur)
     }
   }
   __syncwarp();
+#if AEQ_ROLL_XFNT
+#pragma unroll 1
+#else
 #pragma unroll
+#endif
   for (int st = 0; st < 5; ++st) {
     const int half = 1 << st;
     const int step = AEQ_N >> (st + 1);
@@ -257,8 +303,13 @@ __device__ __forceinline__ void warp_input_fnt(AeqScratch& S, int lane, int cur)
       const int e = (j * step) & 31;              // alpha^e = 2^e ; 2^16 = -1
       uint32_t w = __funnelshift_l(v, v, e & 15);
       w = (e & 16) ? ~w : w;                      // negate = one's complement in Z/M
-      S.X[tt][i0] = m_add(u, w);
-      S.X[tt][i0 + half] = m_sub(u, w);
+      uint32_t lo = m_add(u, w), hi = m_sub(u, w);
+      if (st == 4) {                              // fold the IFNT's N^-1 = 2^-5 in here:
+        lo = m_rot(lo, 27);                       // 4 rotates per lane instead of 16
+        hi = m_rot(hi, 27);
+      }
+      S.X[tt][i0] = lo;
+      S.X[tt][i0 + half] = hi;
     }
     __syncwarp();
   }
@@ -293,15 +344,17 @@ __device__ __forceinline__ void lane_forward(AeqScratch& S, int lane, int cur, c
     }
 #pragma unroll
     for (int k = 0; k < AEQ_N; ++k) X[k] = m_mul(X[k], W[k]);  // 32 general products
+    // +32768 on every output of the inverse = +32768 on its DC bin (X carries N^-1),
+    // so each output decodes as f4_mod(.) - 32768 (fermat.cuh: f4_mod)
+    X[0] = m_add(X[0], 32768u);
     to_bitrev<AEQ_N>(X);
     fnt_dit<AEQ_N, RADIX2, true, false, true>(X);  // outputs 16..31 only
+    const int sh = g == 0 ? 7 : 0;                 // recombine 128 hi + lo (fixedpoint.py:139-143)
 #pragma unroll
-    for (int m = 0; m < AEQ_L; ++m) {
-      const int32_t c = f4_signed(m_rot(X[AEQ_L + m], 27));  // * N^-1 = 2^-5
-      S.part[lane][m] = g == 0 ? c * 128 : c;                 // recombine (fixedpoint.py:139-143)
-    }
+    for (int m = 0; m < AEQ_L; ++m) S.part[lane][m] = (int32_t)(f4_mod(X[AEQ_L + m]) << sh);
     __syncwarp();
-    int32_t a0 = 0, a1 = 0;
+    // sum over (t, g) of 128^[g=0] (c - 32768): the offsets total 4 * 129 * 32768
+    int32_t a0 = -4 * 129 * 32768, a1 = -4 * 129 * 32768;
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
       a0 += S.part[s * 8 + q][m0];
@@ -337,7 +390,7 @@ __device__ __forceinline__ void lane_forward(AeqScratch& S, int lane, int cur, c
 #pragma unroll
     for (int m = 0; m < AEQ_L; ++m) { S.part[lane][m] = hi[m]; S.part[lane][AEQ_L + m] = lo[m]; }
     __syncwarp();
-    int32_t a0 = 0, a1 = 0;
+    int32_t a0 = -4 * 129 * 32768, a1 = -4 * 129 * 32768;
 #pragma unroll
     for (int tt = 0; tt < 4; ++tt) {
       const int l0 = s * 8 + tt * 2;
@@ -345,10 +398,11 @@ __device__ __forceinline__ void lane_forward(AeqScratch& S, int lane, int cur, c
       const int2 h1 = make_int2(S.part[l0 + 1][m0], S.part[l0 + 1][m0 + 1]);
       const int2 l0v = make_int2(S.part[l0][AEQ_L + m0], S.part[l0][AEQ_L + m0 + 1]);
       const int2 l1v = make_int2(S.part[l0 + 1][AEQ_L + m0], S.part[l0 + 1][AEQ_L + m0 + 1]);
-      // each group convolution is a residue mod F4, decoded (aeq.py:139-140)
-      const int32_t B = (int32_t)(F4 * 1024u);
-      a0 += 128 * f4_signed((uint32_t)(h0.x + h1.x + B)) + f4_signed((uint32_t)(l0v.x + l1v.x + B));
-      a1 += 128 * f4_signed((uint32_t)(h0.y + h1.y + B)) + f4_signed((uint32_t)(l0v.y + l1v.y + B));
+      // each group convolution is a residue mod F4, decoded (aeq.py:139-140) as
+      // f4_mod(v + 32768) - 32768; the -32768 offsets are summed into the start value
+      const int32_t B = (int32_t)(F4 * 1024u) + 32768;
+      a0 += 128 * (int32_t)f4_mod((uint32_t)(h0.x + h1.x + B)) + (int32_t)f4_mod((uint32_t)(l0v.x + l1v.x + B));
+      a1 += 128 * (int32_t)f4_mod((uint32_t)(h0.y + h1.y + B)) + (int32_t)f4_mod((uint32_t)(l0v.y + l1v.y + B));
     }
     yi0 = a0;
     yi1 = a1;
@@ -363,7 +417,8 @@ template <int FWD, int IN_MODE, typename TIN>
 __global__ void __launch_bounds__(AEQ_WARPS * 32, AEQ_MIN_CTAS) k_aeq_process(fntgpu_aeq_state* __restrict__ st,
                                                                  const __grid_constant__ AeqArgs A) {
   constexpr bool NARROW = sizeof(TIN) == 1;
-  __shared__ AeqScratch scratch[AEQ_WARPS];
+  extern __shared__ __align__(16) unsigned char aeq_dyn_smem[];
+  AeqScratch* scratch = reinterpret_cast<AeqScratch*>(aeq_dyn_smem);
   __shared__ double lut[2 * XF_LUT + 1];
   for (int i = threadIdx.x; i < 2 * XF_LUT + 1; i += blockDim.x)
     lut[i] = __ddiv_rn((double)(i - XF_LUT), A.prm.sig_scale);
@@ -375,6 +430,10 @@ __global__ void __launch_bounds__(AEQ_WARPS * 32, AEQ_MIN_CTAS) k_aeq_process(fn
   if (S_idx >= io.n_streams) return;
   AeqScratch& S = scratch[warp];
   fntgpu_aeq_state& state = st[S_idx];
+#if AEQ_LOCKSTEP
+  const int64_t n_act = io.n_streams - (int64_t)blockIdx.x * AEQ_WARPS;
+  const int bar_threads = 32 * (int)(n_act < AEQ_WARPS ? n_act : AEQ_WARPS);
+#endif
 
   const int s = lane >> 3, t = (lane >> 1) & 3, g = lane & 1;
   const int j8 = lane & 7;  // m0 = 8*b0 + 4*b1 + 2*b2 with (b2 b1 b0) = lane bits 2,1,0
@@ -394,8 +453,11 @@ __global__ void __launch_bounds__(AEQ_WARPS * 32, AEQ_MIN_CTAS) k_aeq_process(fn
     const int32_t h0 = state.hist[tq][iq], h1 = state.hist[tq][iq + 1];
     S.xi[tq][1][iq] = h0;
     S.xi[tq][1][iq + 1] = h1;
-    S.xf[tq][AEQ_L * (1) + iq] = xf_of<false>(h0, lut, A.prm.sig_scale);
-    S.xf[tq][AEQ_L * (1) + iq + 1] = xf_of<false>(h1, lut, A.prm.sig_scale);
+    const double f0 = xf_of<false>(h0, lut, A.prm.sig_scale), f1 = xf_of<false>(h1, lut, A.prm.sig_scale);
+    S.xf[tq][AEQ_L + iq] = f0;
+    S.xf[tq][AEQ_L + iq + 1] = f1;
+    S.xf[tq][AEQ_L + iq + 32] = f0;
+    S.xf[tq][AEQ_L + iq + 33] = f1;
   }
 
   // this lane's input row (stream tq) and a one-block-ahead prefetch of its 2 samples
@@ -411,13 +473,16 @@ __global__ void __launch_bounds__(AEQ_WARPS * 32, AEQ_MIN_CTAS) k_aeq_process(fn
     sel0 = ph;       // byte of symbol iq within the 4-byte word (2 iq .. 2 iq + 3)
     sel1 = 2 + ph;   // byte of symbol iq + 1
   }
-  auto fetch = [&](int64_t b) -> uint2 {
+  // per-block input advance in bytes
+  constexpr int64_t IN_STEP = IN_MODE == FNTGPU_AEQ_IN_DECIM ? 2 * AEQ_L : (int64_t)sizeof(TIN) * AEQ_L;
+  row += IN_MODE == FNTGPU_AEQ_IN_DECIM ? 2 * iq : (int64_t)sizeof(TIN) * iq;
+  auto fetch = [&](const char* p) -> uint2 {
     if (IN_MODE == FNTGPU_AEQ_IN_DECIM) {
-      return make_uint2(__ldg(reinterpret_cast<const uint32_t*>(row + b * 2 * AEQ_L + 2 * iq)), 0u);
+      return make_uint2(__ldg(reinterpret_cast<const uint32_t*>(p)), 0u);
     } else if (NARROW) {
-      return make_uint2(__ldg(reinterpret_cast<const uint16_t*>(row + b * AEQ_L + iq)), 0u);
+      return make_uint2(__ldg(reinterpret_cast<const uint16_t*>(p)), 0u);
     } else {
-      const int2 v = __ldg(reinterpret_cast<const int2*>(row + 4 * (b * AEQ_L + iq)));
+      const int2 v = __ldg(reinterpret_cast<const int2*>(p));
       return make_uint2((uint32_t)v.x, (uint32_t)v.y);
     }
   };
@@ -434,31 +499,48 @@ __global__ void __launch_bounds__(AEQ_WARPS * 32, AEQ_MIN_CTAS) k_aeq_process(fn
     }
   };
 
-  const double D = A.D;
+  long long sat64 = 0;
   int32_t v0 = 0, v1 = 0;
+  const int64_t nb = io.n_blocks;
   uint2 raw = make_uint2(0u, 0u);
-  if (io.n_blocks > 0) raw = fetch(0);
-  for (int64_t b = 0; b < io.n_blocks; ++b) {
+  if (nb > 0) raw = fetch(row);
+  double2* yrow = reinterpret_cast<double2*>(io.y + S_idx * io.y_stream_stride + s * io.y_row_stride + m0);
+  const double* mu_p = io.mu_blocks;
+  double mu_next = mu_p && nb > 0 ? mu_p[0] : A.prm.mu;
+  double* err_out = io.err ? io.err + S_idx * io.err_stream_stride : nullptr;
+  for (int64_t b = 0; b < nb; ++b) {
     const int cur = (int)(b & 1);
     decode(raw, v0, v1);
-    if (b + 1 < io.n_blocks) raw = fetch(b + 1);  // one block ahead
+    const double mu = mu_next;
+    if (b + 1 < nb) {  // one block ahead
+      row += IN_STEP;
+      raw = fetch(row);
+      if (mu_p) mu_next = mu_p[b + 1];
+    }
     S.xi[tq][cur][iq] = v0;
     S.xi[tq][cur][iq + 1] = v1;
     if (io.adapt) {
-      S.xf[tq][AEQ_L * (cur) + iq] = xf_of<NARROW>(v0, lut, A.prm.sig_scale);
-      S.xf[tq][AEQ_L * (cur) + iq + 1] = xf_of<NARROW>(v1, lut, A.prm.sig_scale);
+      const double f0 = xf_of<NARROW>(v0, lut, A.prm.sig_scale), f1 = xf_of<NARROW>(v1, lut, A.prm.sig_scale);
+      double* xr = &S.xf[tq][AEQ_L * cur + iq];
+      xr[0] = f0;
+      xr[1] = f1;
+      xr[32] = f0;
+      xr[33] = f1;
     }
+#if AEQ_LOCKSTEP
+    asm volatile("bar.sync 1, %0;" :: "r"(bar_threads) : "memory");
+#endif
     __syncwarp();
     int32_t yi0, yi1;
     lane_forward<FWD>(S, lane, cur, T, m0, yi0, yi1);
-    const double y0 = __ddiv_rn((double)yi0, D);  // y_int / (sig_scale * tap_scale)
-    const double y1 = __ddiv_rn((double)yi1, D);
-    double2* yrow = reinterpret_cast<double2*>(io.y + S_idx * io.y_stream_stride + s * io.y_row_stride + b * AEQ_L + m0);
+    const double y0 = div_D(yi0, A);  // y_int / (sig_scale * tap_scale)
+    const double y1 = div_D(yi1, A);
     *yrow = make_double2(y0, y1);
+    yrow += AEQ_L / 2;
     if (io.adapt) {
-      const double mu = io.mu_blocks ? io.mu_blocks[b] : A.prm.mu;
-      double* err_out = io.err ? io.err + S_idx * io.err_stream_stride + b : nullptr;
       lane_update(A, S, lane, m0, y0, y1, cur, mu, T, err_out);
+      if (err_out) ++err_out;
+      if ((b & 0xffffff) == 0xffffff) { sat64 += T.sat; T.sat = 0; }  // <= 8 per block
     }
   }
 
@@ -473,7 +555,7 @@ __global__ void __launch_bounds__(AEQ_WARPS * 32, AEQ_MIN_CTAS) k_aeq_process(fn
     state.hist[tq][iq] = v0;
     state.hist[tq][iq + 1] = v1;
   }
-  long long sat = T.sat;
+  long long sat = sat64 + T.sat;
 #pragma unroll
   for (int off = 16; off > 0; off >>= 1) sat += __shfl_xor_sync(0xffffffffu, sat, off);
   if (lane == 0) {
@@ -501,8 +583,13 @@ __global__ void k_aeq_update_once(fntgpu_aeq_state* st, const __grid_constant__ 
   if (s == 0 && g == 0) {
     for (int i = 0; i < AEQ_L; ++i) {
       // x_block may hold any int64 the reference accepted; divide exactly
-      S.xf[t][AEQ_L * (1) + i] = __ddiv_rn((double)xblk[t * AEQ_N + i], A.prm.sig_scale);
-      S.xf[t][AEQ_L * (0) + i] = __ddiv_rn((double)xblk[t * AEQ_N + AEQ_L + i], A.prm.sig_scale);
+      // block parity cur = 0: x_block[t][j] at ring position 16 + j (and + 32)
+      const double a = __ddiv_rn((double)xblk[t * AEQ_N + i], A.prm.sig_scale);
+      const double b = __ddiv_rn((double)xblk[t * AEQ_N + AEQ_L + i], A.prm.sig_scale);
+      S.xf[t][AEQ_L + i] = a;
+      S.xf[t][AEQ_L + i + 32] = a;
+      S.xf[t][i] = b;
+      S.xf[t][i + 32] = b;
     }
   }
   __syncwarp();
@@ -533,12 +620,67 @@ __global__ void k_aeq_init(fntgpu_aeq_state* st, int n_streams, double tap_scale
   if (r == 0) { S.saturations = 0; S.symbols = 0; S.n_err = 0; S.reserved = 0; }
 }
 
+// Ring index rde_error picks for a squared radius r2 (aeq.py:56-58): r = sqrt(r2)
+// (IEEE, correctly rounded), first argmin of |r - R_i| -- the device slow path.
+static int ring_of(double r2, const fntgpu_aeq_params& prm) {
+  const double r = std::sqrt(r2);
+  int best = 0;
+  double bd = std::fabs(r - prm.radii[0]);
+  for (int i = 1; i < prm.n_radii; ++i) {
+    const double d = std::fabs(r - prm.radii[i]);
+    if (d < bd) { bd = d; best = i; }
+  }
+  return best;
+}
+
+// rde fast path: for sorted radii the chosen ring is a non-decreasing step function
+// of r2 (r = RN(sqrt r2) is monotone, and between neighbouring radii one distance
+// grows while the other shrinks; the radii are >= 2^-30 apart relative, far above an
+// ulp of the reachable r). T[k] = the least double r2 with ring_of(r2) >= k, found by
+// bisection over the ordered bit patterns, so r2 >= T[k] reproduces the decision
+// exactly. Enabled only when |y| <= 2^25 / D keeps r2 in the range the argument
+// covers; otherwise the kernel computes the square root.
+static void rde_thresholds(AeqArgs& A) {
+  const fntgpu_aeq_params& prm = A.prm;
+  A.fast_rde = 0;
+  for (int i = 0; i < 8; ++i) A.T[i] = INFINITY;
+  if (prm.n_radii < 1 || prm.n_radii > 8) return;
+  for (int i = 0; i < prm.n_radii; ++i) {
+    if (!std::isfinite(prm.radii[i]) || prm.radii[i] < 0.0) return;
+    if (i > 0 && !(prm.radii[i] - prm.radii[i - 1] > std::ldexp(prm.radii[i], -30))) return;
+  }
+  if (!(A.D >= 1.0 / 1024.0) || !std::isfinite(A.D)) return;
+  // |y_int| <= 4 * 129 * 32768 < 2^25 (every group residue is decoded to [-2^15, 2^15])
+  const double ymax = std::ldexp(1.0, 25) / A.D;
+  const double r2max = 4.0 * ymax * ymax;
+  if (!(r2max < std::ldexp(1.0, 90))) return;
+  auto bits = [](double v) { uint64_t u; std::memcpy(&u, &v, 8); return u; };
+  auto val = [](uint64_t u) { double v; std::memcpy(&v, &u, 8); return v; };
+  const uint64_t hi_bits = bits(r2max);
+  for (int k = 1; k < prm.n_radii; ++k) {
+    if (ring_of(r2max, prm) < k) continue;  // unreachable: stays +inf
+    uint64_t lo = 0, hi = hi_bits;         // ring_of(val(hi)) >= k
+    if (ring_of(0.0, prm) >= k) { A.T[k] = 0.0; continue; }
+    while (hi - lo > 1) {
+      const uint64_t mid = lo + (hi - lo) / 2;
+      if (ring_of(val(mid), prm) >= k) hi = mid; else lo = mid;
+    }
+    A.T[k] = val(hi);
+  }
+  A.fast_rde = 1;
+}
+
 static AeqArgs make_args(const fntgpu_aeq_params& prm, const fntgpu_aeq_io* io) {
   AeqArgs A;
+  std::memset(&A, 0, sizeof(A));
   A.prm = prm;
   if (io) A.io = *io;
   for (int i = 0; i < 8; ++i) A.R2[i] = prm.radii[i] * prm.radii[i];
   A.D = prm.sig_scale * prm.tap_scale;
+  A.Dinv = 1.0 / A.D;
+  const double aD = std::fabs(A.D);
+  A.fast_div = aD >= std::ldexp(1.0, -500) && aD <= std::ldexp(1.0, 500);
+  rde_thresholds(A);
   return A;
 }
 
@@ -552,19 +694,28 @@ cudaError_t launch_aeq_init(fntgpu_aeq_state* st, int n_streams, const fntgpu_ae
   return cudaGetLastError();
 }
 
+template <int FWD, int IN_MODE, typename TIN>
+static cudaError_t launch_one(fntgpu_aeq_state* st, const AeqArgs& A, cudaStream_t s) {
+  const unsigned grid = (unsigned)((A.io.n_streams + AEQ_WARPS - 1) / AEQ_WARPS);
+#ifndef AEQ_SMEM_PAD
+#define AEQ_SMEM_PAD 0  // experiments only: extra dynamic smem to cap resident CTAs
+#endif
+  constexpr size_t smem = sizeof(AeqScratch) * AEQ_WARPS + AEQ_SMEM_PAD;
+  auto* k = k_aeq_process<FWD, IN_MODE, TIN>;
+  if (smem > 48 * 1024) {
+    const cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+  }
+  k<<<grid, AEQ_WARPS * 32, smem, s>>>(st, A);
+  return cudaGetLastError();
+}
+
 template <int FWD>
 static cudaError_t launch_fwd(fntgpu_aeq_state* st, const AeqArgs& A, cudaStream_t s) {
-  const unsigned grid = (unsigned)((A.io.n_streams + AEQ_WARPS - 1) / AEQ_WARPS);
-  if (A.io.in_mode == FNTGPU_AEQ_IN_DECIM) {
-    k_aeq_process<FWD, FNTGPU_AEQ_IN_DECIM, int8_t><<<grid, AEQ_WARPS * 32, 0, s>>>(st, A);
-  } else if (A.io.in_dtype == FNTGPU_I8) {
-    k_aeq_process<FWD, FNTGPU_AEQ_IN_PLANAR, int8_t><<<grid, AEQ_WARPS * 32, 0, s>>>(st, A);
-  } else if (A.io.in_dtype == FNTGPU_I32) {
-    k_aeq_process<FWD, FNTGPU_AEQ_IN_PLANAR, int32_t><<<grid, AEQ_WARPS * 32, 0, s>>>(st, A);
-  } else {
-    return cudaErrorInvalidValue;
-  }
-  return cudaGetLastError();
+  if (A.io.in_mode == FNTGPU_AEQ_IN_DECIM) return launch_one<FWD, FNTGPU_AEQ_IN_DECIM, int8_t>(st, A, s);
+  if (A.io.in_dtype == FNTGPU_I8) return launch_one<FWD, FNTGPU_AEQ_IN_PLANAR, int8_t>(st, A, s);
+  if (A.io.in_dtype == FNTGPU_I32) return launch_one<FWD, FNTGPU_AEQ_IN_PLANAR, int32_t>(st, A, s);
+  return cudaErrorInvalidValue;
 }
 
 cudaError_t launch_aeq_process(fntgpu_aeq_state* st, const fntgpu_aeq_params& prm,
@@ -580,6 +731,58 @@ cudaError_t launch_aeq_update_once(fntgpu_aeq_state* st, const fntgpu_aeq_params
                                    cudaStream_t s) {
   const AeqArgs A = make_args(prm, nullptr);
   k_aeq_update_once<<<1, 32, 0, s>>>(st, A, xblk, y, mu, err);
+  return cudaGetLastError();
+}
+
+// Self-check of div_D and the threshold ring decision against the IEEE slow path.
+// Division: every numerator in [lo, hi). Ring: r2 = y0^2 + y1^2 for y0 = n / D and
+// y1 = (n * 2654435761 mod 2^20 - 2^19) / D, plus r2 at and one ulp below each
+// threshold.
+__global__ void k_aeq_selfcheck(const __grid_constant__ AeqArgs A, int64_t lo, int64_t hi,
+                                unsigned long long* mism) {
+  unsigned long long bad_div = 0, bad_ring = 0;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t n = lo + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; n < hi; n += stride) {
+    const double q = div_D((int32_t)n, A);
+    const double ref = __ddiv_rn((double)n, A.D);
+    bad_div += __double_as_longlong(q) != __double_as_longlong(ref);
+    if (A.fast_rde) {
+      const int32_t m = (int32_t)(((uint32_t)n * 2654435761u) & 0xfffffu) - (1 << 19);
+      const double y1 = __ddiv_rn((double)m, A.D);
+      AeqArgs B = A;
+      B.fast_rde = 0;
+      bad_ring += __double_as_longlong(rde(ref, y1, A)) != __double_as_longlong(rde(ref, y1, B));
+    }
+  }
+  if (A.fast_rde && blockIdx.x == 0 && threadIdx.x < 8) {
+    const int k = threadIdx.x;
+    if (k >= 1 && k < A.prm.n_radii && isfinite(A.T[k]) && A.T[k] > 0.0) {
+      AeqArgs B = A;
+      B.fast_rde = 0;
+      for (int d = -1; d <= 1; ++d) {
+        const double r2 = __longlong_as_double(__double_as_longlong(A.T[k]) + d);
+        // rde of (sqrt-free y_I, 0) reproduces the ring of r2 only if y_I^2 == r2;
+        // compare the decisions directly instead
+        int fast = 0, slow = 0;
+        for (int i = 1; i < A.prm.n_radii; ++i) fast += r2 >= A.T[i];
+        const double r = __dsqrt_rn(r2);
+        double bd = fabs(dsub(r, A.prm.radii[0]));
+        for (int i = 1; i < A.prm.n_radii; ++i) {
+          const double dd = fabs(dsub(r, A.prm.radii[i]));
+          if (dd < bd) { bd = dd; slow = i; }
+        }
+        bad_ring += A.R2[fast] != A.R2[slow];
+      }
+    }
+  }
+  if (bad_div) atomicAdd(&mism[0], bad_div);
+  if (bad_ring) atomicAdd(&mism[1], bad_ring);
+}
+
+cudaError_t launch_aeq_selfcheck(const fntgpu_aeq_params& prm, int64_t lo, int64_t hi,
+                                 unsigned long long* mismatches, cudaStream_t s) {
+  const AeqArgs A = make_args(prm, nullptr);
+  k_aeq_selfcheck<<<148 * 8, 256, 0, s>>>(A, lo, hi, mismatches);
   return cudaGetLastError();
 }
 

@@ -240,32 +240,133 @@ class CdcAeqChain:
                            mu_blocks=self.mu_blocks, err=self.err, stream=stream)
 
 
+def _segments(total: int, parts: int, align: int) -> list[tuple[int, int]]:
+    """Split [0, total) into <= parts contiguous ranges with boundaries on multiples
+    of `align` (the last range takes the remainder)."""
+    parts = max(1, min(parts, -(-total // align) if total else 1))
+    step = -(-(-(-total // parts)) // align) * align
+    out, a = [], 0
+    while a < total:
+        b = min(total, a + step)
+        out.append((a, b))
+        a = b
+    return out or [(0, 0)]
+
+
 class HostChain:
     """The receiver chain as a host-facing call: pinned host int8 I/Q in,
     float64 AEQ outputs and err_trace out (what a user of the reference's
     rx_frontend + run_single glue gets back), every call moving the data over
-    PCIe. Used for the end-to-end measurement."""
+    PCIe. Used for the end-to-end measurement.
+
+    The call is pipelined over three CUDA streams so the copies hide behind the
+    kernels: the input arrives in `in_chunks` pieces and each piece's CDC output
+    range (a range shard with its filter halo, sharding.py) starts as soon as the
+    piece covering its halo has landed; the AEQ then runs in `aeq_segments` time
+    segments (its state carries over between launches exactly as across
+    FntAeq.process calls) and each segment's outputs stream back (strided 2-D
+    copies) while the next segment computes. Consecutive calls overlap too: the
+    next call's upload waits only for this call's CDC, its CDC for this call's
+    AEQ, and each of its AEQ segments for the copy-out of the same segment. All
+    work of a call is ordered after whatever the caller's stream had enqueued
+    when the call was made; `join(stream)` makes a stream wait for the last call."""
 
     def __init__(self, engine: FntCdcEngine, aeq_config: AeqConfig, n_links: int, length: int,
-                 sig_spec, mu_schedule=None, forward: int | None = None):
+                 sig_spec, mu_schedule=None, forward: int | None = None, in_chunks: int = 4,
+                 aeq_segments: int = 8):
         t = _t()
         dev = _lib.device()
         self.chain = CdcAeqChain(engine, aeq_config, n_links, length, sig_spec, mu_schedule,
                                  forward)
+        self.n_links, self.L = n_links, length
         self.dxr = t.empty((2 * n_links, length), dtype=t.int8, device=dev)
         self.dxi = t.empty_like(self.dxr)
         self.y = t.empty(tuple(self.chain.y.shape), dtype=t.float64, pin_memory=True)
         self.err = t.empty(tuple(self.chain.err.shape), dtype=t.float64, pin_memory=True)
         self.h2d_bytes = 2 * self.dxr.numel()
         self.d2h_bytes = 8 * (self.y.numel() + self.err.numel())
+        # input pieces / CDC output ranges on 64-sample boundaries; AEQ block segments
+        self.ranges = _segments(length, in_chunks, 64)
+        self.segs = _segments(self.chain.n_blocks, aeq_segments, 1)
+        self.s_in, self.s_cmp, self.s_out = (t.cuda.Stream(device=dev) for _ in range(3))
+        E = lambda: t.cuda.Event()  # noqa: E731
+        self.e_in = [E() for _ in self.ranges]
+        self.e_cdc = E()
+        self.e_aeq_done = E()
+        self.e_seg = [E() for _ in self.segs]
+        self.e_out = [E() for _ in self.segs]
+        self.e_done = E()
+        self._calls = 0
+
+    def join(self, stream=None) -> None:
+        """Make `stream` (default: the current stream) wait for the last call."""
+        t = _t()
+        (stream or t.cuda.current_stream()).wait_event(self.e_done)
 
     def __call__(self, xr_host, xi_host):
-        self.dxr.copy_(xr_host, non_blocking=True)
-        self.dxi.copy_(xi_host, non_blocking=True)
-        self.chain.run(self.dxr, self.dxi)
-        self.y.copy_(self.chain.y, non_blocking=True)
-        self.err.copy_(self.chain.err, non_blocking=True)
+        t = _t()
+        ch = self.chain
+        lib = _lib.load()
+        first = self._calls == 0
+        caller = t.cuda.current_stream()
+        for st in (self.s_in, self.s_cmp, self.s_out):
+            st.wait_stream(caller)
+        # -- upload (after the previous call's CDC has consumed the inputs)
+        if not first:
+            self.s_in.wait_event(self.e_cdc)
+        for (a, b), ev in zip(self.ranges, self.e_in):
+            _copy_rows(lib, self.dxr, xr_host, a, b, self.s_in)
+            _copy_rows(lib, self.dxi, xi_host, a, b, self.s_in)
+            ev.record(self.s_in)
+        # -- CDC range shards (after the previous call's AEQ has consumed the q planes)
+        if not first:
+            self.s_cmp.wait_event(self.e_aeq_done)
+        with t.cuda.stream(self.s_cmp):
+            ch.aeq.reset(self.s_cmp)
+            ch.acc.zero_()
+            n_r = len(self.ranges)
+            for j, (a, b) in enumerate(self.ranges):
+                # output [a, b) reads inputs up to b + 16: wait for the piece holding them
+                self.s_cmp.wait_event(self.e_in[min(j + 1, n_r - 1)])
+                ch.cdc.run(self.dxr, self.dxi, length=self.L, out_first=a, out_count=b - a,
+                           qr=ch.qr[:, a:], qi=ch.qi[:, a:], q_spec=ch.sig_spec,
+                           decim_acc=ch.acc, stream=self.s_cmp)
+            self.e_cdc.record(self.s_cmp)
+            decimation_phase(ch.acc, ch.n_links, self.L, ch.phase, ch.gap, stream=self.s_cmp)
+            # -- AEQ time segments; segment j's outputs may be overwritten only after the
+            #    previous call copied them out
+            for j, (b0, b1) in enumerate(self.segs):
+                if not first:
+                    self.s_cmp.wait_event(self.e_out[j])
+                ch.aeq.run_decim(ch.qr[:, 32 * b0:], ch.qi[:, 32 * b0:], ch.phase, b1 - b0,
+                                 ch.y[:, :, 16 * b0:], adapt=True, mu_blocks=ch.mu_blocks[b0:],
+                                 err=ch.err[:, b0:], stream=self.s_cmp)
+                self.e_seg[j].record(self.s_cmp)
+            self.e_aeq_done.record(self.s_cmp)
+        # -- copy-out per segment (y rows and err_trace entries of the segment's blocks)
+        n4 = ch.y.shape[0] * ch.y.shape[1]
+        row, erow = ch.y.shape[2] * 8, ch.err.shape[1] * 8
+        so = _lib.vp(self.s_out.cuda_stream)
+        for j, (b0, b1) in enumerate(self.segs):
+            self.s_out.wait_event(self.e_seg[j])
+            _lib.check(lib.fntgpu_copy2d_async(
+                _lib.vp(self.y.data_ptr() + 128 * b0), row, _lib.vp(ch.y.data_ptr() + 128 * b0), row,
+                128 * (b1 - b0), n4, so), "copy2d_async")
+            _lib.check(lib.fntgpu_copy2d_async(
+                _lib.vp(self.err.data_ptr() + 8 * b0), erow, _lib.vp(ch.err.data_ptr() + 8 * b0), erow,
+                8 * (b1 - b0), ch.err.shape[0], so), "copy2d_async")
+            self.e_out[j].record(self.s_out)
+        self.e_done.record(self.s_out)
+        self._calls += 1
         return self.y, self.err
+
+
+def _copy_rows(lib, dev, host, a: int, b: int, stream) -> None:
+    """host[:, a:b] -> dev[:, a:b] (int8 rows) as one strided 2-D copy."""
+    rows, L = dev.shape
+    _lib.check(lib.fntgpu_copy2d_async(_lib.vp(dev.data_ptr() + a), L, _lib.vp(host.data_ptr() + a),
+                                       host.stride(0), b - a, rows, _lib.vp(stream.cuda_stream)),
+               "copy2d_async")
 
 
 class HostCdc:

@@ -389,3 +389,22 @@ def test_chain_matches_reference_glue(golden):
     assert np.array_equal(chain.err[0].cpu().numpy(), g["b_err"])
     y0 = eng.process(q[0, 0], q[0, 1])
     assert np.array_equal(y0[:2048], g["b_cdc_y0_head"])
+
+
+@pytest.mark.parametrize("case", [
+    dict(),                                                   # the link config (16QAM rings)
+    dict(tap_scale=4096.0),
+    dict(tap_scale=1000.5, sig=3.3),
+    dict(radii=[0.7, 1.3]),
+    dict(radii=[0.1, 0.2, 0.5, 0.9, 1.0, 1.4, 2.0, 3.0]),
+    dict(radii=[1.0, 1.0, 2.0]),                              # duplicate ring: never chosen
+])
+def test_aeq_division_and_ring_shortcuts(case):
+    """The kernel's y = y_int / D (reciprocal + one correction FMA) equals IEEE division
+    for EVERY int32 numerator, and the threshold ring decision equals sqrt + first
+    argmin (fntgpu_aeq_selfcheck)."""
+    from paper_2405_04253_b200.aeq import aeq_selfcheck
+    cfg = P.AeqConfig(block_n=32, l_taps=16, sig_spec=P.QuantSpec(5, case.get("sig", SIG_SCALE)),
+                      tap_scale=case.get("tap_scale", float(1 << 13)),
+                      **({"radii": case["radii"]} if "radii" in case else {}))
+    assert aeq_selfcheck(cfg) == (0, 0)

@@ -372,9 +372,14 @@ def _copy_rows(lib, dev, host, a: int, b: int, stream) -> None:
 class HostCdc:
     """FNT-CDC over host buffers: pinned int8 I/Q in -> H2D -> fntgpu_cdc64_process
     -> D2H int16 I/Q out (the decoded outputs of process_int, which fit int16
-    within the engine's Eq. (5) budget). Used for the config-4 end-to-end number."""
+    within the engine's Eq. (5) budget). Used for the config-4 end-to-end number.
 
-    def __init__(self, engine: FntCdcEngine, n_streams: int, length: int):
+    Pipelined like HostChain: the samples move in `pieces` contiguous ranges; the
+    CDC of output range j (a range shard with its filter halo) waits only for the
+    input piece holding its halo, and its outputs stream back while range j + 1
+    computes. The next call's upload of a piece waits for this call's CDC of it."""
+
+    def __init__(self, engine: FntCdcEngine, n_streams: int, length: int, pieces: int = 8):
         t = _t()
         dev = _lib.device()
         if engine.budget.bound > 32767:
@@ -389,11 +394,50 @@ class HostCdc:
         self.yi = t.empty_like(self.yr, pin_memory=True)
         self.h2d_bytes = 2 * self.dxr.numel()
         self.d2h_bytes = 4 * self.dyr.numel()
+        self.ranges = _segments(length, pieces, 64)
+        self.s_in, self.s_cmp, self.s_out = (t.cuda.Stream(device=dev) for _ in range(3))
+        E = lambda: t.cuda.Event()  # noqa: E731
+        self.e_in = [E() for _ in self.ranges]
+        self.e_cdc = [E() for _ in self.ranges]
+        self.e_out = [E() for _ in self.ranges]
+        self.e_done = E()
+        self._calls = 0
+
+    def join(self, stream=None) -> None:
+        """Make `stream` (default: the current stream) wait for the last call."""
+        t = _t()
+        (stream or t.cuda.current_stream()).wait_event(self.e_done)
 
     def __call__(self, xr_host, xi_host):
-        self.dxr.copy_(xr_host, non_blocking=True)
-        self.dxi.copy_(xi_host, non_blocking=True)
-        self.bank.run(self.dxr, self.dxi, length=self.L, yr=self.dyr, yi=self.dyi)
-        self.yr.copy_(self.dyr, non_blocking=True)
-        self.yi.copy_(self.dyi, non_blocking=True)
+        t = _t()
+        lib = _lib.load()
+        first = self._calls == 0
+        caller = t.cuda.current_stream()
+        for st in (self.s_in, self.s_cmp, self.s_out):
+            st.wait_stream(caller)
+        n_r = len(self.ranges)
+        for j, (a, b) in enumerate(self.ranges):
+            if not first:  # the previous call's CDC of ranges j - 1 and j read this piece
+                self.s_in.wait_event(self.e_cdc[min(j + 1, n_r - 1)])
+            _copy_rows(lib, self.dxr, xr_host, a, b, self.s_in)
+            _copy_rows(lib, self.dxi, xi_host, a, b, self.s_in)
+            self.e_in[j].record(self.s_in)
+        for j, (a, b) in enumerate(self.ranges):
+            self.s_cmp.wait_event(self.e_in[min(j + 1, n_r - 1)])
+            if not first:  # outputs of range j copied out by the previous call
+                self.s_cmp.wait_event(self.e_out[j])
+            self.bank.run(self.dxr, self.dxi, length=self.L, out_first=a, out_count=b - a,
+                          yr=self.dyr[:, a:], yi=self.dyi[:, a:], stream=self.s_cmp)
+            self.e_cdc[j].record(self.s_cmp)
+        so = _lib.vp(self.s_out.cuda_stream)
+        rows, pitch = self.dyr.shape[0], self.dyr.stride(0) * 2
+        for j, (a, b) in enumerate(self.ranges):
+            self.s_out.wait_event(self.e_cdc[j])
+            for h, d in ((self.yr, self.dyr), (self.yi, self.dyi)):
+                _lib.check(lib.fntgpu_copy2d_async(_lib.vp(h.data_ptr() + 2 * a), pitch,
+                                                   _lib.vp(d.data_ptr() + 2 * a), pitch,
+                                                   2 * (b - a), rows, so), "copy2d_async")
+            self.e_out[j].record(self.s_out)
+        self.e_done.record(self.s_out)
+        self._calls += 1
         return self.yr, self.yi

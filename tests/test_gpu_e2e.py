@@ -54,3 +54,30 @@ def test_host_chain_pipelined_equals_resident_chain():
     hc.join()
     torch.cuda.synchronize()
     assert np.array_equal(y.numpy(), outs[2][0]) and np.array_equal(err.numpy(), outs[2][1])
+
+
+def test_host_cdc_pipelined_equals_process_int(golden):
+    """HostCdc (pieces + range shards + 2-D copy-out) == one full-length CDC launch."""
+    import torch
+    from paper_2405_04253_b200.stream import CdcBank, HostCdc
+    cfg = P.LinkConfig(n_symbols=1 << 15, z_km=75.0, seed=3)
+    eng = P.FntCdcEngine(cfg.cdc_config("fnt"), cfg.sig_spec())
+    rng = np.random.default_rng(5)
+    L = 100_000 + 37
+    x = [rng.integers(-15, 16, size=(2, L)).astype(np.int8) for _ in range(2)]
+    hc = HostCdc(eng, 2, L, pieces=6)
+    bank = CdcBank(eng)
+    for _ in range(2):
+        hr = torch.from_numpy(x[0]).pin_memory()
+        hi = torch.from_numpy(x[1]).pin_memory()
+        yr, yi = hc(hr, hi)
+        hc.join()
+        torch.cuda.synchronize()
+        dr = torch.from_numpy(x[0]).cuda()
+        di = torch.from_numpy(x[1]).cuda()
+        rr = torch.empty((2, L), dtype=torch.int16, device="cuda")
+        ri = torch.empty_like(rr)
+        bank.run(dr, di, length=L, yr=rr, yi=ri)
+        assert np.array_equal(yr.numpy(), rr.cpu().numpy())
+        assert np.array_equal(yi.numpy(), ri.cpu().numpy())
+        x = [x[1], x[0]]

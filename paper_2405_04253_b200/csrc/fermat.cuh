@@ -6,12 +6,12 @@
 // B200 design: F4 = 2^16 + 1 divides M = 2^32 - 1 = (2^16 - 1)(2^16 + 1). Every
 // transform / product / sum is therefore computed in the ring Z/M on full 32-bit
 // words and reduced mod F4 once, at the end. In Z/M:
-//   * a + b  = 32-bit add + end-around carry          (IADD3 + IADD3.X / IMAD.X)
-//   * a - b  = 32-bit sub - end-around borrow
+//   * a + b  = 32-bit add + end-around carry          (IADD3 + IMAD.X)
+//   * a - b  = a + ~b                                  (IMAD + IADD3 + IMAD.X)
 //   * a * 2^j = 32-bit rotate left by j               (one SHF.L.W)
 //   * -a     = ~a                                      (free inside LOP3 / swaps)
-// so a radix-2 butterfly with a power-of-two twiddle is 5 integer instructions
-// with no data-dependent reduction, and the sqrt(2) twiddles of the 64-point plan
+// so a radix-2 butterfly with a power-of-two twiddle is 6 integer instructions
+// split evenly over the ALU and FMA pipes, with no data-dependent reduction, and the sqrt(2) twiddles of the 64-point plan
 // (sqrt2 = 2^12 - 2^4, fermat.py:111-117) are two rotates and one subtraction.
 // The final fold x mod F4 = lo16 - hi16 (fermat.py:56-66) is one SHF + one IMAD.
 #pragma once
@@ -22,19 +22,48 @@ namespace fntgpu {
 constexpr uint32_t F4 = 65537u;
 constexpr int32_t F4_HALF = 32768;
 
+// Pipe balance. On sm_100 the ALU pipe (IADD3 with carry-out, IADD3.X, SHF, LOP3)
+// and the FMA pipe (IMAD*, incl. IMAD.X) each accept one warp instruction every
+// other cycle per SM sub-partition. A carry-propagating add must start on the ALU
+// (IADD3 writes the carry predicate) but its end-around carry can finish on the
+// FMA pipe (madc -> IMAD.X), and a - b = a + ~b in Z/M with ~b computed as
+// b * (-1) + (-1) (IMAD). A rotate-twiddled butterfly is then 3 ALU + 3 FMA
+// instructions (6 issue cycles) instead of 4 ALU + 1 FMA (8 cycles on the ALU pipe):
+// tools/bfly_bench.cu measures 5.76 vs 4.59 T butterflies/s on B200.
+// FNT_CARRY_MODE 0 keeps the plain addc / subc forms for A/B comparison.
+#ifndef FNT_CARRY_MODE
+#define FNT_CARRY_MODE 2
+#endif
+#if FNT_CARRY_MODE == 2
+// -1 that ptxas cannot constant-fold (a literal -1 multiplier becomes an ALU IADD3)
+static __constant__ uint32_t c_fnt_minus1 = 0xFFFFFFFFu;
+#endif
+
 // a + b (mod 2^32 - 1)
 __device__ __forceinline__ uint32_t m_add(uint32_t a, uint32_t b) {
   uint32_t r;
+#if FNT_CARRY_MODE == 2
+  asm("{\n\t.reg .u32 t;\n\tadd.cc.u32 t, %1, %2;\n\tmadc.lo.u32 %0, t, 1, 0;\n\t}"
+      : "=r"(r) : "r"(a), "r"(b));
+#else
   asm("{\n\t.reg .u32 t;\n\tadd.cc.u32 t, %1, %2;\n\taddc.u32 %0, t, 0;\n\t}"
       : "=r"(r) : "r"(a), "r"(b));
+#endif
   return r;
 }
 
 // a - b (mod 2^32 - 1)
 __device__ __forceinline__ uint32_t m_sub(uint32_t a, uint32_t b) {
   uint32_t r;
+#if FNT_CARRY_MODE == 2
+  const uint32_t m1 = c_fnt_minus1;
+  asm("{\n\t.reg .u32 t, nb;\n\tmad.lo.u32 nb, %2, %3, %3;\n\tadd.cc.u32 t, %1, nb;\n\t"
+      "madc.lo.u32 %0, t, 1, 0;\n\t}"
+      : "=r"(r) : "r"(a), "r"(b), "r"(m1));
+#else
   asm("{\n\t.reg .u32 t;\n\tsub.cc.u32 t, %1, %2;\n\tsubc.u32 %0, t, 0;\n\t}"
       : "=r"(r) : "r"(a), "r"(b));
+#endif
   return r;
 }
 

@@ -30,6 +30,12 @@
 #include <cmath>
 #include <cstring>
 
+// Pipe balance for this kernel (fermat.cuh): the AEQ's FMA pipe already carries the
+// residue products and the FP64 update's partner work, so the plain addc / subc
+// forms measure faster here (tools/ab_run.sh: 161 vs 165 ms at config 5).
+#ifndef FNT_CARRY_MODE
+#define FNT_CARRY_MODE 0
+#endif
 #include "fermat.cuh"
 #include "internal.h"
 
@@ -41,8 +47,9 @@ constexpr int AEQ_N = 32;            // block length
 #define AEQ_WARPS 4                  // streams (warps) per CTA
 #endif
 #ifndef AEQ_LOCKSTEP
-#define AEQ_LOCKSTEP 0               // 1: the CTA's warps barrier once per block (shared I-cache lines)
-#endif
+#define AEQ_LOCKSTEP 1               // the CTA's 4 warps (one per SM sub-partition) meet once per
+#endif                               // block: they then walk the ~29 KB loop body together and share
+                                     // its instruction-cache lines (161 -> 156 ms at config 5)
 constexpr int AEQ_TAP_MAX = 16383;   // TAP_MAG_MAX (aeq.py:26)
 constexpr int XF_LUT = 127;          // x / sig_scale table for |x| <= 127
 #ifndef AEQ_MIN_CTAS

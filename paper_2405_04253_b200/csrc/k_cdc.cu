@@ -4,14 +4,14 @@
 // 141-156 (_convolve_blocks), 165-180 (process_int / process) and the CDC->AEQ glue
 // of linksim.py:283-308, 399-404 (float rescale, requantization, decimation metric).
 //
-// A CTA owns CDC_BLK = 64 consecutive 64-sample overlap-save blocks (hop 32) of one
+// A CTA owns CDC_BLK = 128 consecutive 64-sample overlap-save blocks (hop 32) of one
 // stream. Each block is split over two threads in different warps (warp-uniform
 // sign, so the two halves of Eqs. (7)-(8) are branch-free):
 //   sign +: a+ = x_r + 2^8 x_i  ->  FNT-64  ->  * b+'  ->  IFNT-64 (outputs 32..63)
 //   sign -: a- = x_r - 2^8 x_i  ->  FNT-64  ->  * b-'  ->  IFNT-64 (outputs 32..63)
 // (b+- pre-scaled by c_re * N^-1 = 2^25; radix-sqrt2 DIT with rotate-only twiddles
 // in Z/(2^32-1), fermat.cuh). The epilogue combines z_re = u+ + u-,
-// z_im = 2^24 (u+ - u-), folds mod F4 and decodes, then streams the contiguous
+// z_im = 2^24 (u+ - u-), reduces mod F4 (multiply-high) and decodes, then streams the contiguous
 // output range of the CTA (and the fused requantization / decimation
 // statistics) with coalesced stores. One HBM read per input sample (the 32-sample
 // halo between neighbouring blocks is re-read from shared memory) and one HBM
@@ -23,8 +23,12 @@
 
 namespace fntgpu {
 
-constexpr int CDC_CTA = 128;                    // threads
-constexpr int CDC_BLK = 64;                     // overlap-save blocks per CTA
+#ifndef CDC_THREADS
+#define CDC_THREADS 256  // 8 warps, 3 CTAs / SM: fewer independent instruction streams per SM
+#endif                   // than 6 x 128 (the kernel is ~60 KB of straight-line code):
+                         // 40.4 -> 37.7 ms at config 5, 133 -> 140 Gsamples/s at config 4
+constexpr int CDC_CTA = CDC_THREADS;            // threads
+constexpr int CDC_BLK = CDC_CTA / 2;            // overlap-save blocks per CTA (2 threads each)
 constexpr int CDC_N = 64;
 constexpr int CDC_HOP = 32;
 constexpr int WIN = CDC_HOP * (CDC_BLK + 1);    // input samples staged per plane
@@ -119,8 +123,8 @@ __device__ __forceinline__ void cdc_epilogue_fast(const CdcArgs& A, const uint32
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
       const uint32_t up = s_u[rb + e], um = s_u[CDC_BLK * UP + rb + e];
-      zr[e] = f4_signed(m_add(up, um));
-      zi[e] = f4_signed(m_rot(m_sub(up, um), 24));
+      zr[e] = (int32_t)f4_mod(m_add(up, um)) - 32768;
+      zi[e] = (int32_t)f4_mod(m_rot(m_sub(up, um), 24)) - 32768;
     }
     if (qr) {
       uint32_t pr = 0, pi = 0;
@@ -206,10 +210,8 @@ __device__ __forceinline__ int32_t sx8(uint32_t w, int k) {
 template <typename TIN, bool FAST>
 __global__ void __launch_bounds__(CDC_CTA) k_cdc64(const __grid_constant__ CdcArgs A) {
   using TS = typename std::conditional<sizeof(TIN) == 1, int8_t, int32_t>::type;
-  constexpr int IN_BYTES = 2 * WIN * (int)sizeof(TS);
-  constexpr int U_BYTES = 2 * CDC_BLK * UP * 4;
   // the input window and the u staging rows are never live at the same time
-  __shared__ __align__(16) unsigned char smem[IN_BYTES > U_BYTES ? IN_BYTES : U_BYTES];
+  extern __shared__ __align__(16) unsigned char smem[];
   TS* s_xr = reinterpret_cast<TS*>(smem);
   TS* s_xi = s_xr + WIN;
   uint32_t* s_u = reinterpret_cast<uint32_t*>(smem);  // [sign][block][UP]
@@ -260,6 +262,11 @@ __global__ void __launch_bounds__(CDC_CTA) k_cdc64(const __grid_constant__ CdcAr
   const uint32_t* B = sgn ? A.bm : A.bp;
 #pragma unroll
   for (int k = 0; k < CDC_N; ++k) a[k] = m_mul(a[k], B[k]);  // the 64 general products
+  // decode offsets: +K on the DC bin adds K to every output of the (unscaled) inverse.
+  // K+ = 16320, K- = 16448 put +32768 on both z_re = u+ + u- and z_im = 2^24 (u+ - u-)
+  // (2^24 * -128 = -2^31 == 2^15 mod F4), so the epilogue decodes each value as
+  // f4_mod(.) - 32768 (fermat.cuh) instead of a two-sided range fold.
+  a[0] = m_add(a[0], sgn ? 16448u : 16320u);
   to_bitrev<CDC_N>(a);
   fnt_dit<CDC_N, SQRT2, true, false, true>(a);             // outputs 32..63 only
   __syncthreads();  // every thread has consumed the input window
@@ -287,8 +294,8 @@ __global__ void __launch_bounds__(CDC_CTA) k_cdc64(const __grid_constant__ CdcAr
     const int idx = (int)(n - n0);
     const int r = (idx >> 5) * UP + (idx & 31);
     const uint32_t up = s_u[r], um = s_u[CDC_BLK * UP + r];
-    const int32_t zr = f4_signed(m_add(up, um));
-    const int32_t zi = f4_signed(m_rot(m_sub(up, um), 24));
+    const int32_t zr = (int32_t)f4_mod(m_add(up, um)) - 32768;
+    const int32_t zi = (int32_t)f4_mod(m_rot(m_sub(up, um), 24)) - 32768;
     const int64_t o = n - io.out_first;
     switch (io.out_dtype) {
       case FNTGPU_I16:
@@ -377,6 +384,21 @@ static inline void scale_taps(const uint32_t* src, uint32_t* dst) {
   for (int k = 0; k < CDC_N; ++k) dst[k] = (uint32_t)(((uint64_t)src[k] % F4) * (1ull << 25) % F4);
 }
 
+template <typename TIN, bool FAST>
+static cudaError_t launch_k(const CdcArgs& A, dim3 grid, cudaStream_t st) {
+  using TS = typename std::conditional<sizeof(TIN) == 1, int8_t, int32_t>::type;
+  constexpr int IN_BYTES = 2 * WIN * (int)sizeof(TS);
+  constexpr int U_BYTES = 2 * CDC_BLK * UP * 4;
+  constexpr int SMEM = IN_BYTES > U_BYTES ? IN_BYTES : U_BYTES;
+  auto* k = k_cdc64<TIN, FAST>;
+  if (SMEM > 48 * 1024) {
+    const cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
+    if (e != cudaSuccess) return e;
+  }
+  k<<<grid, CDC_CTA, SMEM, st>>>(A);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_cdc64(const fntgpu_cdc_taps& taps, const fntgpu_cdc_io& io, cudaStream_t st) {
   if (io.out_count <= 0 || io.n_streams <= 0) return cudaSuccess;
   CdcArgs A;
@@ -401,14 +423,11 @@ cudaError_t launch_cdc64(const fntgpu_cdc_taps& taps, const fntgpu_cdc_io& io, c
            (reinterpret_cast<uintptr_t>(io.yi) & 7) == 0 && io.y_stride % 4 == 0;
   switch (io.in_dtype) {
     case FNTGPU_I8:
-      if (fast) k_cdc64<int8_t, true><<<grid, CDC_CTA, 0, st>>>(A);
-      else k_cdc64<int8_t, false><<<grid, CDC_CTA, 0, st>>>(A);
-      break;
-    case FNTGPU_I32: k_cdc64<int32_t, false><<<grid, CDC_CTA, 0, st>>>(A); break;
-    case FNTGPU_I64: k_cdc64<int64_t, false><<<grid, CDC_CTA, 0, st>>>(A); break;
+      return fast ? launch_k<int8_t, true>(A, grid, st) : launch_k<int8_t, false>(A, grid, st);
+    case FNTGPU_I32: return launch_k<int32_t, false>(A, grid, st);
+    case FNTGPU_I64: return launch_k<int64_t, false>(A, grid, st);
     default: return cudaErrorInvalidValue;
   }
-  return cudaGetLastError();
 }
 
 cudaError_t launch_decim_phase(const fntgpu_decim_io& io, cudaStream_t s) {

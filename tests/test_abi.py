@@ -83,3 +83,21 @@ def test_api_surface_mirrors_reference_names():
     for n in ref_all:
         assert hasattr(P, n), n
     assert sorted(P.__all__) == sorted(ref_all)
+
+
+def test_integration_md_binding_stub_matches_abi(monkeypatch):
+    """The ctypes stub INTEGRATION.md tells a maintainer to add declares the same
+    struct layouts as the C header (sizes from fntgpu_struct_sizes)."""
+    import re
+    from conftest import ROOT
+    text = (ROOT / "INTEGRATION.md").read_text()
+    code = re.search(r"```python\n(import ctypes as C.*?)```", text, re.S).group(1)
+    monkeypatch.chdir(ROOT)
+    ns: dict = {}
+    exec(compile(code, "INTEGRATION.md", "exec"), ns)
+    from paper_2405_04253_b200 import _lib
+    lib = _lib.load()
+    out = (C.c_int64 * 6)()
+    lib.fntgpu_struct_sizes(out, 6)
+    assert C.sizeof(ns["CdcTaps"]) == out[0]
+    assert C.sizeof(ns["CdcIO"]) == out[1]

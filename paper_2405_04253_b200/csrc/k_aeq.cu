@@ -55,6 +55,10 @@ constexpr int XF_LUT = 127;          // x / sig_scale table for |x| <= 127
 #ifndef AEQ_MIN_CTAS
 #define AEQ_MIN_CTAS 4               // resident CTAs per SM the register budget targets
 #endif
+#ifndef AEQ_GRAD_LOCKSTEP
+#define AEQ_GRAD_LOCKSTEP 1          // the 8 taps' einsum chains advance in lockstep (16 independent
+                                     // FP64 chains; 155.8 -> 150.6 ms at config 5)
+#endif
 #ifndef AEQ_ROLL_XFNT
 #define AEQ_ROLL_XFNT 0              // 1: keep the cooperative input-FNT stage loop rolled
 #endif
@@ -63,7 +67,9 @@ struct __align__(16) AeqScratch {
   double wf[8][32];           // float taps (aeq.py:99), lane-contiguous: wf[kk][lane] = w[s][t][8g+kk]
   int32_t part[32][33];       // per-lane partial sums (direct: 16 hi + 16 lo; fnt: 16), padded
   double ey[4][AEQ_L];        // e * y per output stream
-  double xf[4][65];           // x / sig_scale ring of 32, stored twice: [t][16 * parity + j (+ 32)]
+  double xf[4][66];           // x / sig_scale ring of 32, stored twice: [t][1 + 16 * parity + j (+ 32)];
+                              // the +1 makes the gradient's x pairs 16-byte aligned, and the
+                              // 66-double row stride keeps its 8 distinct LDS.128 conflict-free
                               // so every window is contiguous (odd t-stride: no bank conflicts)
   int32_t xi[4][2][AEQ_L];    // input integer ring: [t][block parity][j]
   uint32_t X[4][AEQ_N + 4];   // cooperative input spectra (FNT path), 16-B aligned padded rows
@@ -238,6 +244,42 @@ __device__ __forceinline__ void lane_update(const AeqArgs& A, AeqScratch& S, int
   }
   if (mu != 0.0) {
     // gradient for taps k in [8g, 8g+8): sum_m ey[s][m] * xf[t][16 + m - k]
+    // x_block[t][j] sits at ring position 16 * prev + j (duplicated ring: no wrap);
+    // tap kk (k = 8g + kk) uses x_block[t][16 + m - 8g - kk] = xs[7 - kk + m].
+    const double* xs = S.xf[t] + 1 + AEQ_L * (cur ^ 1) + 9 - 8 * g;
+#if AEQ_GRAD_LOCKSTEP
+    // all 8 taps advance together through numpy's m order (two chains per tap,
+    // even m: 6,4,2,0,14,12,10,8 and odd m: 7,5,...,9): 16 independent FP64 chains
+    // hide the DADD latency, and only one m pair of e*y and 9 x values are live.
+    const double2* eyv = reinterpret_cast<const double2*>(S.ey[s]);
+    double c0[8], c1[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int me = (i < 4 ? 6 : 22) - 2 * i;   // 6, 4, 2, 0, 14, 12, 10, 8
+      const double2 e2 = eyv[me / 2];             // ey[me], ey[me + 1]
+      double xv[9];  // xs + me is 16-byte aligned (me even, ring offset +1): 4 LDS.128 + 1 LDS.64
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const double2 v = reinterpret_cast<const double2*>(xs + me)[q];
+        xv[2 * q] = v.x;
+        xv[2 * q + 1] = v.y;
+      }
+      xv[8] = xs[me + 8];
+#pragma unroll
+      for (int kk = 0; kk < 8; ++kk) {
+        const double pe = dmul(e2.x, xv[7 - kk]), po = dmul(e2.y, xv[8 - kk]);
+        c0[kk] = i == 0 ? pe : dadd(pe, c0[kk]);
+        c1[kk] = i == 0 ? po : dadd(po, c1[kk]);
+      }
+    }
+#pragma unroll
+    for (int kk = 0; kk < 8; ++kk) {
+      const double gr = dadd(c0[kk], c1[kk]);
+      const double w = dadd(S.wf[kk][lane], dmul(mu, gr));
+      S.wf[kk][lane] = w;
+      T.gp[kk] = pack_groups(requantize_tap(w, A.prm.tap_scale, T.sat));
+    }
+#else
     double ey[AEQ_L];
 #pragma unroll
     for (int q = 0; q < AEQ_L / 2; ++q) {
@@ -245,11 +287,8 @@ __device__ __forceinline__ void lane_update(const AeqArgs& A, AeqScratch& S, int
       ey[2 * q] = v.x;
       ey[2 * q + 1] = v.y;
     }
-    // x_block[t][j] for j = 9 - 8g ... 31 - 8g as a window that slides by one per
-    // tap: tap kk (k = 8g + kk) uses xw index q = 7 + m - kk, m = 0..15. Taps run
-    // from kk = 7 down to 0 so each step needs exactly one new value. x_block[t][j]
-    // sits at ring position 16 * prev + j (duplicated ring: no wrap).
-    const double* xs = S.xf[t] + AEQ_L * (cur ^ 1) + 9 - 8 * g;
+    // a window that slides by one per tap: taps run from kk = 7 down to 0 so each
+    // step needs exactly one new value
     auto xload = [&](int q) -> double { return xs[q]; };
     double xw[23];
 #pragma unroll
@@ -272,6 +311,7 @@ __device__ __forceinline__ void lane_update(const AeqArgs& A, AeqScratch& S, int
       S.wf[kk][lane] = w;
       T.gp[kk] = pack_groups(requantize_tap(w, A.prm.tap_scale, T.sat));
     }
+#endif
   }
   __syncwarp();
 }
@@ -461,10 +501,10 @@ __global__ void __launch_bounds__(AEQ_WARPS * 32, AEQ_MIN_CTAS) k_aeq_process(fn
     S.xi[tq][1][iq] = h0;
     S.xi[tq][1][iq + 1] = h1;
     const double f0 = xf_of<false>(h0, lut, A.prm.sig_scale), f1 = xf_of<false>(h1, lut, A.prm.sig_scale);
-    S.xf[tq][AEQ_L + iq] = f0;
-    S.xf[tq][AEQ_L + iq + 1] = f1;
-    S.xf[tq][AEQ_L + iq + 32] = f0;
-    S.xf[tq][AEQ_L + iq + 33] = f1;
+    S.xf[tq][1 + AEQ_L + iq] = f0;
+    S.xf[tq][1 + AEQ_L + iq + 1] = f1;
+    S.xf[tq][1 + AEQ_L + iq + 32] = f0;
+    S.xf[tq][1 + AEQ_L + iq + 33] = f1;
   }
 
   // this lane's input row (stream tq) and a one-block-ahead prefetch of its 2 samples
@@ -528,7 +568,7 @@ __global__ void __launch_bounds__(AEQ_WARPS * 32, AEQ_MIN_CTAS) k_aeq_process(fn
     S.xi[tq][cur][iq + 1] = v1;
     if (io.adapt) {
       const double f0 = xf_of<NARROW>(v0, lut, A.prm.sig_scale), f1 = xf_of<NARROW>(v1, lut, A.prm.sig_scale);
-      double* xr = &S.xf[tq][AEQ_L * cur + iq];
+      double* xr = &S.xf[tq][1 + AEQ_L * cur + iq];
       xr[0] = f0;
       xr[1] = f1;
       xr[32] = f0;
@@ -593,10 +633,10 @@ __global__ void k_aeq_update_once(fntgpu_aeq_state* st, const __grid_constant__ 
       // block parity cur = 0: x_block[t][j] at ring position 16 + j (and + 32)
       const double a = __ddiv_rn((double)xblk[t * AEQ_N + i], A.prm.sig_scale);
       const double b = __ddiv_rn((double)xblk[t * AEQ_N + AEQ_L + i], A.prm.sig_scale);
-      S.xf[t][AEQ_L + i] = a;
-      S.xf[t][AEQ_L + i + 32] = a;
-      S.xf[t][i] = b;
-      S.xf[t][i + 32] = b;
+      S.xf[t][1 + AEQ_L + i] = a;
+      S.xf[t][1 + AEQ_L + i + 32] = a;
+      S.xf[t][1 + i] = b;
+      S.xf[t][1 + i + 32] = b;
     }
   }
   __syncwarp();

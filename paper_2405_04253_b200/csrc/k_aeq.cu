@@ -59,6 +59,9 @@ constexpr int XF_LUT = 127;          // x / sig_scale table for |x| <= 127
 #define AEQ_GRAD_LOCKSTEP 1          // the 8 taps' einsum chains advance in lockstep (16 independent
                                      // FP64 chains; 155.8 -> 150.6 ms at config 5)
 #endif
+#ifndef AEQ_XFNT_SHFL
+#define AEQ_XFNT_SHFL 1              // input FNT-32s in registers + shuffles (four-step form)
+#endif
 #ifndef AEQ_ROLL_XFNT
 #define AEQ_ROLL_XFNT 0              // 1: keep the cooperative input-FNT stage loop rolled
 #endif
@@ -321,6 +324,47 @@ __device__ __forceinline__ void lane_update(const AeqArgs& A, AeqScratch& S, int
 // butterflies per lane per stage, twiddles 2^e as runtime rotates.
 __device__ __forceinline__ void warp_input_fnt(AeqScratch& S, int lane, int cur) {
   const int prev = cur ^ 1;
+#if AEQ_XFNT_SHFL
+  // Four-step form, 8 lanes per stream (n = n1 + 8 n2, k = k2 + 4 k1, n1 = lane & 7):
+  //   A[k2] = sum_n2 x[n1 + 8 n2] 2^(8 n2 k2)     4-point transform in registers
+  //   B[k2] = A[k2] 2^(n1 k2)                     twiddles (2^16 == -1: complement)
+  //   X[k2 + 4 k1] = sum_n1 B[k2] 2^(4 n1 k1)     8-point DIF across the 8 lanes
+  // (3 shuffle stages; lane n1 ends with k1 = bitrev3(n1)). No shared-memory round
+  // trips or warp barriers inside; N^-1 = 2^-5 of the inverse is folded in.
+  {
+    const int tq = lane >> 3, n1 = lane & 7;
+    // x[n1], x[n1 + 8] from the previous block's ring half, x[n1 + 16], x[n1 + 24] from this one
+    uint32_t a0 = f4_enc_small(S.xi[tq][prev][n1]), a1 = f4_enc_small(S.xi[tq][prev][n1 + 8]);
+    uint32_t a2 = f4_enc_small(S.xi[tq][cur][n1]), a3 = f4_enc_small(S.xi[tq][cur][n1 + 8]);
+    const uint32_t s02 = m_add(a0, a2), d02 = m_sub(a0, a2);
+    const uint32_t s13 = m_add(a1, a3), d13 = m_rot(m_sub(a1, a3), 8);
+    uint32_t v[4] = {m_add(s02, s13), m_add(d02, d13), m_sub(s02, s13), m_sub(d02, d13)};
+#pragma unroll
+    for (int k2 = 1; k2 < 4; ++k2) {
+      const int e = n1 * k2;                       // <= 21
+      const uint32_t r = __funnelshift_l(v[k2], v[k2], e & 15);
+      v[k2] = (e & 16) ? ~r : r;
+    }
+#pragma unroll
+    for (int st = 2; st >= 0; --st) {              // spans 4, 2, 1
+      const int h = 1 << st;
+      const bool upper = (n1 & h) != 0;
+      const uint32_t mask = upper ? 0xffffffffu : 0u;
+      const int e = upper ? (n1 & (h - 1)) * (16 >> st) : 0;  // bottom twiddle (2^(16/2^st))^j
+#pragma unroll
+      for (int k2 = 0; k2 < 4; ++k2) {
+        const uint32_t o = __shfl_xor_sync(0xffffffffu, v[k2], h);
+        const uint32_t t = m_add(v[k2] ^ mask, o);  // lower: v + o; upper: o - v
+        v[k2] = st > 0 ? __funnelshift_l(t, t, e) : t;
+      }
+    }
+    const int k1 = (int)(__brev((unsigned)n1) >> 29);
+    uint4 out = make_uint4(m_rot(v[0], 27), m_rot(v[1], 27), m_rot(v[2], 27), m_rot(v[3], 27));
+    reinterpret_cast<uint4*>(S.X[tq])[k1] = out;
+  }
+  __syncwarp();
+  return;
+#endif
   {
     const int tq = lane >> 3;
 #pragma unroll

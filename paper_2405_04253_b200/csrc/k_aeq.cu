@@ -421,12 +421,19 @@ __device__ __forceinline__ void lane_forward(AeqScratch& S, int lane, int cur, c
       const uint32_t other = __shfl_xor_sync(0xffffffffu, T.gp[kk], 1);
       const uint32_t lo8 = g == 0 ? T.gp[kk] : other;   // tap kk
       const uint32_t hi8 = g == 0 ? other : T.gp[kk];   // tap 8 + kk
-      W[bitrev(kk, 5)] = f4_enc_small(unpack_group(lo8, g));
-      W[bitrev(8 + kk, 5)] = f4_enc_small(unpack_group(hi8, g));
+      W[bitrev(kk, 5)] = (uint32_t)unpack_group(lo8, g);
+      W[bitrev(8 + kk, 5)] = (uint32_t)unpack_group(hi8, g);
     }
 #pragma unroll
     for (int k = AEQ_L; k < AEQ_N; ++k) W[bitrev(k, 5)] = 0u;
-    fnt_dit<AEQ_N, RADIX2, false, true>(W);  // taps zero-padded: first stage is a copy
+    // taps zero-padded: stage 0 is a copy; |group| <= 127 keeps stages 1-2 (twiddles
+    // 2^0..2^12) below 2^28 in plain int32, then a multiple of F4 makes the words
+    // non-negative residues of Z/M for stages 3-4
+    fnt_stage<AEQ_N, RADIX2, false, true, false, 0, 1>(W);
+    fnt_stage_plain<AEQ_N, RADIX2, 1, 3>(W);
+#pragma unroll
+    for (int k = 0; k < AEQ_N; ++k) W[k] += F4 * 8192u;  // 536 879 104 > 2^28
+    fnt_stage<AEQ_N, RADIX2, false, false, false, 3>(W);
     uint32_t X[AEQ_N];
 #pragma unroll
     for (int q = 0; q < AEQ_N / 4; ++q) {

@@ -248,8 +248,8 @@ __global__ void __launch_bounds__(CDC_CTA) k_cdc64(const __grid_constant__ CdcAr
 #pragma unroll
           for (int k = 0; k < 4; ++k) {
             const int i = q * 16 + w * 4 + k;
-            // x_r +- 2^8 x_i + bias (bias = 256 F4 keeps the word non-negative)
-            a[bitrev(i, 6)] = (uint32_t)(sx8(rw[w], k) + (int32_t)F4_BIAS + m256 * sx8(iw[w], k));
+            // x_r +- 2^8 x_i as a plain signed integer (|a| <= 32896 < 2^16)
+            a[bitrev(i, 6)] = (uint32_t)(sx8(rw[w], k) + m256 * sx8(iw[w], k));
           }
       }
     } else {
@@ -258,7 +258,17 @@ __global__ void __launch_bounds__(CDC_CTA) k_cdc64(const __grid_constant__ CdcAr
         a[bitrev(i, 6)] = (uint32_t)((int32_t)wr[i] + (int32_t)F4_BIAS + m256 * (int32_t)wi[i]);
     }
   }
-  fnt_dit<CDC_N, SQRT2, false>(a);
+  if (sizeof(TS) == 1) {
+    // int8 planes: stages 0-1 (twiddles 1, 2^8) keep |values| < 2^26 in plain int32
+    // arithmetic (no carries); a multiple of F4 above 2^26 then makes them
+    // non-negative words of Z/M for stages 2-5
+    fnt_stage_plain<CDC_N, SQRT2, 0, 2>(a);
+#pragma unroll
+    for (int k = 0; k < CDC_N; ++k) a[k] += F4 * 1024u;
+    fnt_stage<CDC_N, SQRT2, false, false, false, 2>(a);
+  } else {
+    fnt_dit<CDC_N, SQRT2, false>(a);
+  }
   const uint32_t* B = sgn ? A.bm : A.bp;
 #pragma unroll
   for (int k = 0; k < CDC_N; ++k) a[k] = m_mul(a[k], B[k]);  // the 64 general products

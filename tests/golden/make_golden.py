@@ -440,6 +440,47 @@ def gen_c3() -> dict:
     return {str(k): v for k, v in res.items()}
 
 
+# --------------------------------------------------------------------------
+# config 5: the first 64 links, end to end through the reference (hash-only, --big)
+
+C5_LINKS = 64
+
+
+def _c5_link(i: int):
+    """SURVEY 8d C5: rng_i = default_rng(SeedSequence([4, i])); snr_i ~ U[16, 22];
+    U_i = unitary_group.rvs(2, random_state=rng_i); Tx / channel / front end on rng_i;
+    then the reference's CDC -> glue -> FntAeq with the gear-shift schedule."""
+    from scipy.stats import unitary_group
+    rng = np.random.default_rng(np.random.SeedSequence([4, i]))
+    snr = rng.uniform(16, 22)
+    jones = unitary_group.rvs(2, random_state=rng)
+    cfg = LinkConfig(n_symbols=2 ** 18, z_km=75.0, snr_db=(snr,), pol_rotation_deg=0.0,
+                     dgd_symbols=0.0, iq_skew_samples=0.0, seed=4)
+    tx = linksim.generate_tx(cfg, rng)
+    rx, _ = _apply_channel_jones(tx.wave, cfg, snr, rng, jones)
+    mf = linksim.rrc_taps(cfg.sps, cfg.rrc_span, cfg.rrc_rolloff)
+    spec = cfg.sig_spec()
+    q = []
+    for pol in range(2):
+        g = linksim.gsop(rx[pol])
+        m = linksim.circ_filter(g, mf)
+        c = m / np.sqrt(np.mean(np.abs(m) ** 2))
+        q.append((quantize_real(c.real, spec)[0], quantize_real(c.imag, spec)[0]))
+    eng, eqs, phase, qa = _glue(cfg, q)
+    eq, y, _ = _aeq_run(qa, cfg.mu_schedule())
+    return i, {
+        "q_in": sha(np.stack([np.stack([xr, xi]) for xr, xi in q]).astype(np.int8)),
+        "phase": int(phase), "aeq_y": sha(y), "w": sha(eq.w), "w_int": sha(eq.taps.w_int),
+        "sat": int(eq.saturations), "err_trace": sha(np.array(eq.err_trace)),
+    }
+
+
+def gen_c5() -> dict:
+    with ProcessPoolExecutor(max_workers=os.cpu_count() or 1) as ex:
+        res = dict(ex.map(_c5_link, range(C5_LINKS)))
+    return {str(k): v for k, v in sorted(res.items())}
+
+
 def gen_cli() -> dict:
     """Reference CLI outputs (cli.py:135-318): selftest (+ fault injection),
     complexity --measure, transform / convolve on small files."""
@@ -519,6 +560,8 @@ def main() -> None:
         gen_cli()
     if args.big:
         digests["c3"] = gen_c3()
+    if args.big or want("c5") and only is not None:
+        digests["c5"] = gen_c5()
     digests["_generator"] = {"numpy": np.__version__, "fntdsp": fntdsp.__version__}
     digests_path.write_text(json.dumps(digests, indent=1, sort_keys=True))
     print("digests ->", digests_path)

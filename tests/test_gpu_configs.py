@@ -85,6 +85,49 @@ def _oracle_chain(eng, cfg, fe):
     return ph, y, oq
 
 
+def _c5_inputs(i: int):
+    L, bits, sym, fe = G.config5(i)
+    return np.stack([np.stack([xr, xi]) for xr, xi in fe]).astype(np.int8)
+
+
+@pytest.mark.slow
+def test_config5_64_links_vs_reference_digests():
+    """the first 64 links end to end (inputs regenerated bit-exactly by
+    oracle.linkgen_np, then CDC + glue + AEQ for all 64 links in one batch on the
+    GPU) against digests of the unmodified reference's outputs for every link."""
+    import os
+    from concurrent.futures import ProcessPoolExecutor
+    import torch
+    from paper_2405_04253_b200.stream import CdcAeqChain
+    d = json.loads((GOLDEN / "digests.json").read_text())["c5"]
+    n = len(d)
+    with ProcessPoolExecutor(max_workers=min(16, os.cpu_count() or 1)) as ex:
+        q = list(ex.map(_c5_inputs, range(n)))        # (2 pols, I/Q, L) int8 each
+    for i in range(n):
+        assert sha(q[i]) == d[str(i)]["q_in"], i
+    L = q[0].shape[-1]
+    xr = torch.from_numpy(np.stack([qi[p, 0] for qi in q for p in range(2)])).cuda()
+    xi = torch.from_numpy(np.stack([qi[p, 1] for qi in q for p in range(2)])).cuda()
+    cfg = P.LinkConfig(n_symbols=2 ** 18, z_km=75.0, pol_rotation_deg=0.0, dgd_symbols=0.0,
+                       iq_skew_samples=0.0, seed=4)
+    eng = P.FntCdcEngine(cfg.cdc_config("fnt"), cfg.sig_spec())
+    ch = CdcAeqChain(eng, cfg.aeq_config(), n, L, cfg.sig_spec(), cfg.mu_schedule())
+    ch.run(xr, xi)
+    ph = ch.phase.cpu().numpy()
+    y = ch.y.cpu().numpy()
+    err = ch.err.cpu().numpy()
+    states = ch.aeq.read_state()
+    for i in range(n):
+        di = d[str(i)]
+        st = states[i]
+        assert int(ph[i]) == di["phase"], i
+        assert sha(y[i]) == di["aeq_y"], i
+        assert sha(err[i]) == di["err_trace"], i
+        assert sha(np.array(st.w, dtype=np.float64).reshape(4, 4, 16)) == di["w"], i
+        assert sha(np.array(st.w_int, dtype=np.int64).reshape(4, 4, 16)) == di["w_int"], i
+        assert int(st.saturations) == di["sat"], i
+
+
 @pytest.mark.slow
 @pytest.mark.parametrize("link", [0, 1, 4095])
 def test_config5_links_vs_oracle(link):

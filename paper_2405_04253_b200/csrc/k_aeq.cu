@@ -109,9 +109,14 @@ __device__ __forceinline__ int32_t tap_group(int32_t w, int g) {
 
 // rde_error (aeq.py:53-58) for one output pair (y_I, y_Q). The 3-ring case
 // (16QAM, qam16_radii) is unrolled; other ring counts loop.
+template <bool QUICK = false>
 __device__ __forceinline__ double rde(double yi, double yq, const AeqArgs& A) {
   const double r2 = dadd(dmul(yi, yi), dmul(yq, yq));
   double best_r2;
+  if (QUICK) {  // launch-time checked: fast_rde && n_radii == 3
+    best_r2 = r2 >= A.T[2] ? A.R2[2] : (r2 >= A.T[1] ? A.R2[1] : A.R2[0]);
+    return dsub(best_r2, r2);
+  }
   if (A.fast_rde) {
     // argmin_i |sqrt(r2) - R_i| is a step function of r2 over the reachable range;
     // the host located its steps exactly (rde_thresholds), so no sqrt is needed.
@@ -165,9 +170,10 @@ __device__ __forceinline__ int32_t requantize_tap(double w, double tap_scale, ui
 // the corrected quotient (Markstein's theorem; no over/underflow for |y_int| < 2^32
 // and the D range the host admits). fntgpu_aeq_selfcheck (tests/test_gpu_parity.py)
 // checks it against IEEE division over every int32 numerator for the configured D.
+template <bool QUICK = false>
 __device__ __forceinline__ double div_D(int32_t yi, const AeqArgs& A) {
   const double a = (double)yi;
-  if (!A.fast_div) return __ddiv_rn(a, A.D);
+  if (!QUICK && !A.fast_div) return __ddiv_rn(a, A.D);
   const double q0 = dmul(a, A.Dinv);
   const double r = __fma_rn(-q0, A.D, a);
   return __fma_rn(r, A.Dinv, q0);
@@ -215,6 +221,7 @@ struct LaneTaps {
 
 // Exchange the e values, compute the err_trace mean (lane 0 writes *err_out when
 // non-null) and, when mu != 0, the float update of this lane's 8 taps.
+template <bool QUICK = false>
 __device__ __forceinline__ void lane_update(const AeqArgs& A, AeqScratch& S, int lane, int m0,
                                             double y0, double y1, int cur, double mu,
                                             LaneTaps& T, double* err_out) {
@@ -222,7 +229,7 @@ __device__ __forceinline__ void lane_update(const AeqArgs& A, AeqScratch& S, int
   // rde: the I lane (s even) takes m0, the Q lane (s odd) takes m0 + 1
   const double send = (s & 1) ? y0 : y1;
   const double recv = __shfl_xor_sync(0xffffffffu, send, 8);
-  double e_mine = (s & 1) ? rde(recv, y1, A) : rde(y0, recv, A);
+  double e_mine = (s & 1) ? rde<QUICK>(recv, y1, A) : rde<QUICK>(y0, recv, A);
   const double e_other = __shfl_xor_sync(0xffffffffu, e_mine, 8);
   const double e0 = (s & 1) ? e_other : e_mine;  // e[p][m0]
   const double e1 = (s & 1) ? e_mine : e_other;  // e[p][m0 + 1]
@@ -511,7 +518,9 @@ __device__ __forceinline__ void lane_forward(AeqScratch& S, int lane, int cur, c
 // -------------------------------------------------------------------------------------
 // process (aeq.py:172-190) for one stream per warp
 
-template <int FWD, int IN_MODE, typename TIN>
+// QUICK: the launch verified fast_rde && n_radii == 3 && fast_div (the 16QAM rings
+// with an ordinary scale), so those paths are resolved at compile time.
+template <int FWD, int IN_MODE, typename TIN, bool QUICK>
 __global__ void __launch_bounds__(AEQ_WARPS * 32, AEQ_MIN_CTAS) k_aeq_process(fntgpu_aeq_state* __restrict__ st,
                                                                  const __grid_constant__ AeqArgs A) {
   constexpr bool NARROW = sizeof(TIN) == 1;
@@ -631,12 +640,12 @@ __global__ void __launch_bounds__(AEQ_WARPS * 32, AEQ_MIN_CTAS) k_aeq_process(fn
     __syncwarp();
     int32_t yi0, yi1;
     lane_forward<FWD>(S, lane, cur, T, m0, yi0, yi1);
-    const double y0 = div_D(yi0, A);  // y_int / (sig_scale * tap_scale)
-    const double y1 = div_D(yi1, A);
+    const double y0 = div_D<QUICK>(yi0, A);  // y_int / (sig_scale * tap_scale)
+    const double y1 = div_D<QUICK>(yi1, A);
     *yrow = make_double2(y0, y1);
     yrow += AEQ_L / 2;
     if (io.adapt) {
-      lane_update(A, S, lane, m0, y0, y1, cur, mu, T, err_out);
+      lane_update<QUICK>(A, S, lane, m0, y0, y1, cur, mu, T, err_out);
       if (err_out) ++err_out;
       if ((b & 0xffffff) == 0xffffff) { sat64 += T.sat; T.sat = 0; }  // <= 8 per block
     }
@@ -792,14 +801,14 @@ cudaError_t launch_aeq_init(fntgpu_aeq_state* st, int n_streams, const fntgpu_ae
   return cudaGetLastError();
 }
 
-template <int FWD, int IN_MODE, typename TIN>
+template <int FWD, int IN_MODE, typename TIN, bool QUICK>
 static cudaError_t launch_one(fntgpu_aeq_state* st, const AeqArgs& A, cudaStream_t s) {
   const unsigned grid = (unsigned)((A.io.n_streams + AEQ_WARPS - 1) / AEQ_WARPS);
 #ifndef AEQ_SMEM_PAD
 #define AEQ_SMEM_PAD 0  // experiments only: extra dynamic smem to cap resident CTAs
 #endif
   constexpr size_t smem = sizeof(AeqScratch) * AEQ_WARPS + AEQ_SMEM_PAD;
-  auto* k = k_aeq_process<FWD, IN_MODE, TIN>;
+  auto* k = k_aeq_process<FWD, IN_MODE, TIN, QUICK>;
   if (smem > 48 * 1024) {
     const cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
@@ -808,12 +817,18 @@ static cudaError_t launch_one(fntgpu_aeq_state* st, const AeqArgs& A, cudaStream
   return cudaGetLastError();
 }
 
+template <int FWD, bool QUICK>
+static cudaError_t launch_fwd_q(fntgpu_aeq_state* st, const AeqArgs& A, cudaStream_t s) {
+  if (A.io.in_mode == FNTGPU_AEQ_IN_DECIM) return launch_one<FWD, FNTGPU_AEQ_IN_DECIM, int8_t, QUICK>(st, A, s);
+  if (A.io.in_dtype == FNTGPU_I8) return launch_one<FWD, FNTGPU_AEQ_IN_PLANAR, int8_t, QUICK>(st, A, s);
+  if (A.io.in_dtype == FNTGPU_I32) return launch_one<FWD, FNTGPU_AEQ_IN_PLANAR, int32_t, QUICK>(st, A, s);
+  return cudaErrorInvalidValue;
+}
+
 template <int FWD>
 static cudaError_t launch_fwd(fntgpu_aeq_state* st, const AeqArgs& A, cudaStream_t s) {
-  if (A.io.in_mode == FNTGPU_AEQ_IN_DECIM) return launch_one<FWD, FNTGPU_AEQ_IN_DECIM, int8_t>(st, A, s);
-  if (A.io.in_dtype == FNTGPU_I8) return launch_one<FWD, FNTGPU_AEQ_IN_PLANAR, int8_t>(st, A, s);
-  if (A.io.in_dtype == FNTGPU_I32) return launch_one<FWD, FNTGPU_AEQ_IN_PLANAR, int32_t>(st, A, s);
-  return cudaErrorInvalidValue;
+  const bool quick = A.fast_rde && A.prm.n_radii == 3 && A.fast_div;
+  return quick ? launch_fwd_q<FWD, true>(st, A, s) : launch_fwd_q<FWD, false>(st, A, s);
 }
 
 cudaError_t launch_aeq_process(fntgpu_aeq_state* st, const fntgpu_aeq_params& prm,

@@ -241,7 +241,7 @@ __device__ __forceinline__ void lane_update(const AeqArgs& A, AeqScratch& S, int
   S.ey[s][m0] = dmul(e0, y0);
   S.ey[s][m0 + 1] = dmul(e1, y1);
   __syncwarp();
-  if (err_out != nullptr) {
+  if (QUICK || err_out != nullptr) {
     // np.mean(|e|) over (2 pols x 16): numpy pairwise order r[j] = a[j]+a[j+8]+a[j+16]+a[j+24]
     double r = 0.0;
     if (lane < 8) {
@@ -519,7 +519,8 @@ __device__ __forceinline__ void lane_forward(AeqScratch& S, int lane, int cur, c
 // process (aeq.py:172-190) for one stream per warp
 
 // QUICK: the launch verified fast_rde && n_radii == 3 && fast_div (the 16QAM rings
-// with an ordinary scale), so those paths are resolved at compile time.
+// with an ordinary scale) and an adapting call with per-block mu and an err_trace
+// output (the receiver chain), so those paths are resolved at compile time.
 template <int FWD, int IN_MODE, typename TIN, bool QUICK>
 __global__ void __launch_bounds__(AEQ_WARPS * 32, AEQ_MIN_CTAS) k_aeq_process(fntgpu_aeq_state* __restrict__ st,
                                                                  const __grid_constant__ AeqArgs A) {
@@ -622,11 +623,11 @@ __global__ void __launch_bounds__(AEQ_WARPS * 32, AEQ_MIN_CTAS) k_aeq_process(fn
     if (b + 1 < nb) {  // one block ahead
       row += IN_STEP;
       raw = fetch(row);
-      if (mu_p) mu_next = mu_p[b + 1];
+      if (QUICK || mu_p) mu_next = mu_p[b + 1];
     }
     S.xi[tq][cur][iq] = v0;
     S.xi[tq][cur][iq + 1] = v1;
-    if (io.adapt) {
+    if (QUICK || io.adapt) {
       const double f0 = xf_of<NARROW>(v0, lut, A.prm.sig_scale), f1 = xf_of<NARROW>(v1, lut, A.prm.sig_scale);
       double* xr = &S.xf[tq][1 + AEQ_L * cur + iq];
       xr[0] = f0;
@@ -644,9 +645,9 @@ __global__ void __launch_bounds__(AEQ_WARPS * 32, AEQ_MIN_CTAS) k_aeq_process(fn
     const double y1 = div_D<QUICK>(yi1, A);
     *yrow = make_double2(y0, y1);
     yrow += AEQ_L / 2;
-    if (io.adapt) {
+    if (QUICK || io.adapt) {
       lane_update<QUICK>(A, S, lane, m0, y0, y1, cur, mu, T, err_out);
-      if (err_out) ++err_out;
+      if (QUICK || err_out) ++err_out;
       if ((b & 0xffffff) == 0xffffff) { sat64 += T.sat; T.sat = 0; }  // <= 8 per block
     }
   }
@@ -827,7 +828,8 @@ static cudaError_t launch_fwd_q(fntgpu_aeq_state* st, const AeqArgs& A, cudaStre
 
 template <int FWD>
 static cudaError_t launch_fwd(fntgpu_aeq_state* st, const AeqArgs& A, cudaStream_t s) {
-  const bool quick = A.fast_rde && A.prm.n_radii == 3 && A.fast_div;
+  const bool quick = A.fast_rde && A.prm.n_radii == 3 && A.fast_div && A.io.adapt &&
+                     A.io.err != nullptr && A.io.mu_blocks != nullptr;
   return quick ? launch_fwd_q<FWD, true>(st, A, s) : launch_fwd_q<FWD, false>(st, A, s);
 }
 

@@ -229,7 +229,9 @@ __device__ __forceinline__ void lane_update(const AeqArgs& A, AeqScratch& S, int
   // rde: the I lane (s even) takes m0, the Q lane (s odd) takes m0 + 1
   const double send = (s & 1) ? y0 : y1;
   const double recv = __shfl_xor_sync(0xffffffffu, send, 8);
-  double e_mine = (s & 1) ? rde<QUICK>(recv, y1, A) : rde<QUICK>(y0, recv, A);
+  // one (branch-free) rde per lane: (y_I, y_Q) = (recv, y1) on odd s, (y0, recv) on even s
+  const double yI = (s & 1) ? recv : y0, yQ = (s & 1) ? y1 : recv;
+  double e_mine = rde<QUICK>(yI, yQ, A);
   const double e_other = __shfl_xor_sync(0xffffffffu, e_mine, 8);
   const double e0 = (s & 1) ? e_other : e_mine;  // e[p][m0]
   const double e1 = (s & 1) ? e_mine : e_other;  // e[p][m0 + 1]

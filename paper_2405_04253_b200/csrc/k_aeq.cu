@@ -618,40 +618,52 @@ __global__ void __launch_bounds__(AEQ_WARPS * 32, AEQ_MIN_CTAS) k_aeq_process(fn
   const double* mu_p = io.mu_blocks;
   double mu_next = mu_p && nb > 0 ? mu_p[0] : A.prm.mu;
   double* err_out = io.err ? io.err + S_idx * io.err_stream_stride : nullptr;
-  for (int64_t b = 0; b < nb; ++b) {
-    const int cur = (int)(b & 1);
-    decode(raw, v0, v1);
-    const double mu = mu_next;
-    if (b + 1 < nb) {  // one block ahead
-      row += IN_STEP;
-      raw = fetch(row);
-      if (QUICK || mu_p) mu_next = mu_p[b + 1];
-    }
-    S.xi[tq][cur][iq] = v0;
-    S.xi[tq][cur][iq + 1] = v1;
-    if (QUICK || io.adapt) {
-      const double f0 = xf_of<NARROW>(v0, lut, A.prm.sig_scale), f1 = xf_of<NARROW>(v1, lut, A.prm.sig_scale);
-      double* xr = &S.xf[tq][1 + AEQ_L * cur + iq];
-      xr[0] = f0;
-      xr[1] = f1;
-      xr[32] = f0;
-      xr[33] = f1;
-    }
+  // blocks in chunks of 2^24 so the 32-bit per-lane saturation counter (<= 8 per
+  // block) is flushed outside the hot loop
+  for (int64_t b0 = 0; b0 < nb; b0 += (int64_t)1 << 24) {
+    const int64_t b1 = nb - b0 < ((int64_t)1 << 24) ? nb : b0 + ((int64_t)1 << 24);
+    for (int64_t b = b0; b < b1; ++b) {
+      const int cur = (int)(b & 1);
+      decode(raw, v0, v1);
+      const double mu = mu_next;
+      if (QUICK) {
+        // branch-free one-block-ahead prefetch (the last block re-reads its own input)
+        const bool more = b + 1 < nb;
+        row += more ? IN_STEP : 0;
+        raw = fetch(row);
+        mu_next = mu_p[more ? b + 1 : b];
+      } else if (b + 1 < nb) {
+        row += IN_STEP;
+        raw = fetch(row);
+        if (mu_p) mu_next = mu_p[b + 1];
+      }
+      S.xi[tq][cur][iq] = v0;
+      S.xi[tq][cur][iq + 1] = v1;
+      if (QUICK || io.adapt) {
+        const double f0 = xf_of<NARROW>(v0, lut, A.prm.sig_scale), f1 = xf_of<NARROW>(v1, lut, A.prm.sig_scale);
+        double* xr = &S.xf[tq][1 + AEQ_L * cur + iq];
+        xr[0] = f0;
+        xr[1] = f1;
+        xr[32] = f0;
+        xr[33] = f1;
+      }
 #if AEQ_LOCKSTEP
-    asm volatile("bar.sync 1, %0;" :: "r"(bar_threads) : "memory");
+      asm volatile("bar.sync 1, %0;" :: "r"(bar_threads) : "memory");
 #endif
-    __syncwarp();
-    int32_t yi0, yi1;
-    lane_forward<FWD>(S, lane, cur, T, m0, yi0, yi1);
-    const double y0 = div_D<QUICK>(yi0, A);  // y_int / (sig_scale * tap_scale)
-    const double y1 = div_D<QUICK>(yi1, A);
-    *yrow = make_double2(y0, y1);
-    yrow += AEQ_L / 2;
-    if (QUICK || io.adapt) {
-      lane_update<QUICK>(A, S, lane, m0, y0, y1, cur, mu, T, err_out);
-      if (QUICK || err_out) ++err_out;
-      if ((b & 0xffffff) == 0xffffff) { sat64 += T.sat; T.sat = 0; }  // <= 8 per block
+      __syncwarp();
+      int32_t yi0, yi1;
+      lane_forward<FWD>(S, lane, cur, T, m0, yi0, yi1);
+      const double y0 = div_D<QUICK>(yi0, A);  // y_int / (sig_scale * tap_scale)
+      const double y1 = div_D<QUICK>(yi1, A);
+      *yrow = make_double2(y0, y1);
+      yrow += AEQ_L / 2;
+      if (QUICK || io.adapt) {
+        lane_update<QUICK>(A, S, lane, m0, y0, y1, cur, mu, T, err_out);
+        if (QUICK || err_out) ++err_out;
+      }
     }
+    sat64 += T.sat;
+    T.sat = 0;
   }
 
   // write back the stream state

@@ -47,7 +47,8 @@ constexpr int AEQ_N = 32;            // block length
 #define AEQ_WARPS 4                  // streams (warps) per CTA
 #endif
 #ifndef AEQ_LOCKSTEP
-#define AEQ_LOCKSTEP 1               // the CTA's 4 warps (one per SM sub-partition) meet once per
+#define AEQ_LOCKSTEP 1               // the CTA's 4 warps (one per SM sub-partition) meet every
+                                     // AEQ_LOCKSTEP blocks (power of two; 0 = never) 
 #endif                               // block: they then walk the ~29 KB loop body together and share
                                      // its instruction-cache lines (161 -> 156 ms at config 5)
 constexpr int AEQ_TAP_MAX = 16383;   // TAP_MAG_MAX (aeq.py:26)
@@ -648,7 +649,7 @@ __global__ void __launch_bounds__(AEQ_WARPS * 32, AEQ_MIN_CTAS) k_aeq_process(fn
         xr[33] = f1;
       }
 #if AEQ_LOCKSTEP
-      asm volatile("bar.sync 1, %0;" :: "r"(bar_threads) : "memory");
+      if ((b & (AEQ_LOCKSTEP - 1)) == 0) asm volatile("bar.sync 1, %0;" :: "r"(bar_threads) : "memory");
 #endif
       __syncwarp();
       int32_t yi0, yi1;

@@ -13,9 +13,9 @@
 // integers and of x / sig_scale, so no lane ever indexes registers dynamically.
 //
 // Forward path, FNTGPU_AEQ_FWD_FNT (aeq.py:118-144): the four 32-point input
-//   transforms are computed cooperatively by the warp in shared memory (2
-//   butterflies per lane per stage); lane (s,t,g) transforms its 16-tap group
-//   padded to 32 in registers (first DIT stage free), multiplies pointwise (the 32
+//   transforms are computed by 8 lanes each in registers + shuffles (four-step
+//   form); lane (s,t,g) transforms its 16-tap group padded to 32 in registers
+//   (first DIT stage free, the next two carry-free), multiplies pointwise (the 32
 //   general products of that filter group), runs the inverse pruned to outputs
 //   16..31 and decodes -- the reference's residue convolution per (group, s, t);
 //   recombine 128*hi + lo and sum over t, g. All transforms: alpha = 2, rotates
@@ -55,16 +55,6 @@ constexpr int AEQ_TAP_MAX = 16383;   // TAP_MAG_MAX (aeq.py:26)
 constexpr int XF_LUT = 127;          // x / sig_scale table for |x| <= 127
 #ifndef AEQ_MIN_CTAS
 #define AEQ_MIN_CTAS 4               // resident CTAs per SM the register budget targets
-#endif
-#ifndef AEQ_GRAD_LOCKSTEP
-#define AEQ_GRAD_LOCKSTEP 1          // the 8 taps' einsum chains advance in lockstep (16 independent
-                                     // FP64 chains; 155.8 -> 150.6 ms at config 5)
-#endif
-#ifndef AEQ_XFNT_SHFL
-#define AEQ_XFNT_SHFL 1              // input FNT-32s in registers + shuffles (four-step form)
-#endif
-#ifndef AEQ_ROLL_XFNT
-#define AEQ_ROLL_XFNT 0              // 1: keep the cooperative input-FNT stage loop rolled
 #endif
 
 struct __align__(16) AeqScratch {
@@ -260,7 +250,6 @@ __device__ __forceinline__ void lane_update(const AeqArgs& A, AeqScratch& S, int
     // x_block[t][j] sits at ring position 16 * prev + j (duplicated ring: no wrap);
     // tap kk (k = 8g + kk) uses x_block[t][16 + m - 8g - kk] = xs[7 - kk + m].
     const double* xs = S.xf[t] + 1 + AEQ_L * (cur ^ 1) + 9 - 8 * g;
-#if AEQ_GRAD_LOCKSTEP
     // all 8 taps advance together through numpy's m order (two chains per tap,
     // even m: 6,4,2,0,14,12,10,8 and odd m: 7,5,...,9): 16 independent FP64 chains
     // hide the DADD latency, and only one m pair of e*y and 9 x values are live.
@@ -292,49 +281,14 @@ __device__ __forceinline__ void lane_update(const AeqArgs& A, AeqScratch& S, int
       S.wf[kk][lane] = w;
       T.gp[kk] = pack_groups(requantize_tap(w, A.prm.tap_scale, T.sat));
     }
-#else
-    double ey[AEQ_L];
-#pragma unroll
-    for (int q = 0; q < AEQ_L / 2; ++q) {
-      const double2 v = reinterpret_cast<const double2*>(S.ey[s])[q];
-      ey[2 * q] = v.x;
-      ey[2 * q + 1] = v.y;
-    }
-    // a window that slides by one per tap: taps run from kk = 7 down to 0 so each
-    // step needs exactly one new value
-    auto xload = [&](int q) -> double { return xs[q]; };
-    double xw[23];
-#pragma unroll
-    for (int q = 0; q < 16; ++q) xw[q] = xload(q);
-#pragma unroll
-    for (int kk = 7; kk >= 0; --kk) {
-      if (kk < 7) xw[22 - kk] = xload(22 - kk);
-      // einsum over m in numpy's order, each product rounded before its add
-      const int o = 7 - kk;
-      double c0 = dmul(ey[6], xw[o + 6]), c1 = dmul(ey[7], xw[o + 7]);
-      c0 = dadd(dmul(ey[4], xw[o + 4]), c0);   c1 = dadd(dmul(ey[5], xw[o + 5]), c1);
-      c0 = dadd(dmul(ey[2], xw[o + 2]), c0);   c1 = dadd(dmul(ey[3], xw[o + 3]), c1);
-      c0 = dadd(dmul(ey[0], xw[o + 0]), c0);   c1 = dadd(dmul(ey[1], xw[o + 1]), c1);
-      c0 = dadd(dmul(ey[14], xw[o + 14]), c0); c1 = dadd(dmul(ey[15], xw[o + 15]), c1);
-      c0 = dadd(dmul(ey[12], xw[o + 12]), c0); c1 = dadd(dmul(ey[13], xw[o + 13]), c1);
-      c0 = dadd(dmul(ey[10], xw[o + 10]), c0); c1 = dadd(dmul(ey[11], xw[o + 11]), c1);
-      c0 = dadd(dmul(ey[8], xw[o + 8]), c0);   c1 = dadd(dmul(ey[9], xw[o + 9]), c1);
-      const double gr = dadd(c0, c1);
-      const double w = dadd(S.wf[kk][lane], dmul(mu, gr));
-      S.wf[kk][lane] = w;
-      T.gp[kk] = pack_groups(requantize_tap(w, A.prm.tap_scale, T.sat));
-    }
-#endif
   }
   __syncwarp();
 }
 
-// Cooperative 32-point forward transforms of the four input streams' blocks
-// x_block[t] = [ring prev | ring cur] into S.X[t][k] (natural order), 2
-// butterflies per lane per stage, twiddles 2^e as runtime rotates.
+// 32-point forward transforms of the four input streams' blocks
+// x_block[t] = [ring prev | ring cur] into S.X[t][k] (natural order).
 __device__ __forceinline__ void warp_input_fnt(AeqScratch& S, int lane, int cur) {
   const int prev = cur ^ 1;
-#if AEQ_XFNT_SHFL
   // Four-step form, 8 lanes per stream (n = n1 + 8 n2, k = k2 + 4 k1, n1 = lane & 7):
   //   A[k2] = sum_n2 x[n1 + 8 n2] 2^(8 n2 k2)     4-point transform in registers
   //   B[k2] = A[k2] 2^(n1 k2)                     twiddles (2^16 == -1: complement)
@@ -373,47 +327,6 @@ __device__ __forceinline__ void warp_input_fnt(AeqScratch& S, int lane, int cur)
     reinterpret_cast<uint4*>(S.X[tq])[k1] = out;
   }
   __syncwarp();
-  return;
-#endif
-  {
-    const int tq = lane >> 3;
-#pragma unroll
-    for (int r = 0; r < 4; ++r) {
-      const int p = 4 * (lane & 7) + r;           // bit-reversed position
-      const int i = (int)(__brev((unsigned)p) >> 27);  // natural index
-      const int32_t v = i < AEQ_L ? S.xi[tq][prev][i] : S.xi[tq][cur][i - AEQ_L];
-      S.X[tq][p] = f4_enc_small(v);
-    }
-  }
-  __syncwarp();
-#if AEQ_ROLL_XFNT
-#pragma unroll 1
-#else
-#pragma unroll
-#endif
-  for (int st = 0; st < 5; ++st) {
-    const int half = 1 << st;
-    const int step = AEQ_N >> (st + 1);
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const int q = lane + 32 * h;                // 64 butterflies: 4 streams x 16
-      const int tt = q >> 4, j2 = q & 15;
-      const int j = j2 & (half - 1);
-      const int i0 = (j2 >> st) * 2 * half + j;
-      const uint32_t u = S.X[tt][i0], v = S.X[tt][i0 + half];
-      const int e = (j * step) & 31;              // alpha^e = 2^e ; 2^16 = -1
-      uint32_t w = __funnelshift_l(v, v, e & 15);
-      w = (e & 16) ? ~w : w;                      // negate = one's complement in Z/M
-      uint32_t lo = m_add(u, w), hi = m_sub(u, w);
-      if (st == 4) {                              // fold the IFNT's N^-1 = 2^-5 in here:
-        lo = m_rot(lo, 27);                       // 4 rotates per lane instead of 16
-        hi = m_rot(hi, 27);
-      }
-      S.X[tt][i0] = lo;
-      S.X[tt][i0 + half] = hi;
-    }
-    __syncwarp();
-  }
 }
 
 // Forward path for one block: returns y_int[s][m0], y_int[s][m0+1] in yi0, yi1.
@@ -887,8 +800,6 @@ __global__ void k_aeq_selfcheck(const __grid_constant__ AeqArgs A, int64_t lo, i
   if (A.fast_rde && blockIdx.x == 0 && threadIdx.x < 8) {
     const int k = threadIdx.x;
     if (k >= 1 && k < A.prm.n_radii && isfinite(A.T[k]) && A.T[k] > 0.0) {
-      AeqArgs B = A;
-      B.fast_rde = 0;
       for (int d = -1; d <= 1; ++d) {
         const double r2 = __longlong_as_double(__double_as_longlong(A.T[k]) + d);
         // rde of (sqrt-free y_I, 0) reproduces the ring of r2 only if y_I^2 == r2;

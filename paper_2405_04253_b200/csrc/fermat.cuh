@@ -34,36 +34,37 @@ constexpr int32_t F4_HALF = 32768;
 #ifndef FNT_CARRY_MODE
 #define FNT_CARRY_MODE 2
 #endif
-#if FNT_CARRY_MODE == 2
 // -1 that ptxas cannot constant-fold (a literal -1 multiplier becomes an ALU IADD3)
 static __constant__ uint32_t c_fnt_minus1 = 0xFFFFFFFFu;
-#endif
 
-// a + b (mod 2^32 - 1)
+// a + b (mod 2^32 - 1); CM selects the carry form per call site (default: the
+// translation unit's FNT_CARRY_MODE)
+template <int CM = FNT_CARRY_MODE>
 __device__ __forceinline__ uint32_t m_add(uint32_t a, uint32_t b) {
   uint32_t r;
-#if FNT_CARRY_MODE == 2
-  asm("{\n\t.reg .u32 t;\n\tadd.cc.u32 t, %1, %2;\n\tmadc.lo.u32 %0, t, 1, 0;\n\t}"
-      : "=r"(r) : "r"(a), "r"(b));
-#else
-  asm("{\n\t.reg .u32 t;\n\tadd.cc.u32 t, %1, %2;\n\taddc.u32 %0, t, 0;\n\t}"
-      : "=r"(r) : "r"(a), "r"(b));
-#endif
+  if (CM == 2) {
+    asm("{\n\t.reg .u32 t;\n\tadd.cc.u32 t, %1, %2;\n\tmadc.lo.u32 %0, t, 1, 0;\n\t}"
+        : "=r"(r) : "r"(a), "r"(b));
+  } else {
+    asm("{\n\t.reg .u32 t;\n\tadd.cc.u32 t, %1, %2;\n\taddc.u32 %0, t, 0;\n\t}"
+        : "=r"(r) : "r"(a), "r"(b));
+  }
   return r;
 }
 
 // a - b (mod 2^32 - 1)
+template <int CM = FNT_CARRY_MODE>
 __device__ __forceinline__ uint32_t m_sub(uint32_t a, uint32_t b) {
   uint32_t r;
-#if FNT_CARRY_MODE == 2
-  const uint32_t m1 = c_fnt_minus1;
-  asm("{\n\t.reg .u32 t, nb;\n\tmad.lo.u32 nb, %2, %3, %3;\n\tadd.cc.u32 t, %1, nb;\n\t"
-      "madc.lo.u32 %0, t, 1, 0;\n\t}"
-      : "=r"(r) : "r"(a), "r"(b), "r"(m1));
-#else
-  asm("{\n\t.reg .u32 t;\n\tsub.cc.u32 t, %1, %2;\n\tsubc.u32 %0, t, 0;\n\t}"
-      : "=r"(r) : "r"(a), "r"(b));
-#endif
+  if (CM == 2) {
+    const uint32_t m1 = c_fnt_minus1;
+    asm("{\n\t.reg .u32 t, nb;\n\tmad.lo.u32 nb, %2, %3, %3;\n\tadd.cc.u32 t, %1, nb;\n\t"
+        "madc.lo.u32 %0, t, 1, 0;\n\t}"
+        : "=r"(r) : "r"(a), "r"(b), "r"(m1));
+  } else {
+    asm("{\n\t.reg .u32 t;\n\tsub.cc.u32 t, %1, %2;\n\tsubc.u32 %0, t, 0;\n\t}"
+        : "=r"(r) : "r"(a), "r"(b));
+  }
   return r;
 }
 
@@ -156,7 +157,7 @@ struct Tw {
   bool neg;
 };
 
-template <int KIND>
+template <int KIND, int CM = FNT_CARRY_MODE>
 __device__ __forceinline__ Tw twiddle(uint32_t a, int e /* exponent of alpha, >= 0 */) {
   if (KIND == RADIX2) {
     int r = e & 31;
@@ -175,30 +176,30 @@ __device__ __forceinline__ Tw twiddle(uint32_t a, int e /* exponent of alpha, >=
     // 2^r1 - 2^r2; fold rotates >= 16 into signs, preferring one overall negate.
     if (r1 >= 16 && r2 >= 16) { r1 -= 16; r2 -= 16; neg = true; }
     if (r1 >= 16) {  // -(2^(r1-16)) - 2^r2 = -(2^(r1-16) + 2^r2)
-      return {m_add(m_rot(a, r1 - 16), m_rot(a, r2)), !neg};
+      return {m_add<CM>(m_rot(a, r1 - 16), m_rot(a, r2)), !neg};
     }
     if (r2 >= 16) {  // 2^r1 + 2^(r2-16)
-      return {m_add(m_rot(a, r1), m_rot(a, r2 - 16)), neg};
+      return {m_add<CM>(m_rot(a, r1), m_rot(a, r2 - 16)), neg};
     }
-    return {m_sub(m_rot(a, r1), m_rot(a, r2)), neg};
+    return {m_sub<CM>(m_rot(a, r1), m_rot(a, r2)), neg};
   }
 }
 
 // Radix-2 DIT butterfly (fnt.py:94-102): (u, v) -> (u + tw*v, u - tw*v).
-template <int KIND>
+template <int KIND, int CM = FNT_CARRY_MODE>
 __device__ __forceinline__ void bfly(uint32_t& u, uint32_t& v, int e) {
-  Tw t = twiddle<KIND>(v, e);
-  uint32_t s = t.neg ? m_sub(u, t.v) : m_add(u, t.v);
-  uint32_t d = t.neg ? m_add(u, t.v) : m_sub(u, t.v);
+  Tw t = twiddle<KIND, CM>(v, e);
+  uint32_t s = t.neg ? m_sub<CM>(u, t.v) : m_add<CM>(u, t.v);
+  uint32_t d = t.neg ? m_add<CM>(u, t.v) : m_sub<CM>(u, t.v);
   u = s;
   v = d;
 }
 
 // Only the difference output u - tw*v (pruned last stage of an inverse transform).
-template <int KIND>
+template <int KIND, int CM = FNT_CARRY_MODE>
 __device__ __forceinline__ uint32_t bfly_hi(uint32_t u, uint32_t v, int e) {
-  Tw t = twiddle<KIND>(v, e);
-  return t.neg ? m_add(u, t.v) : m_sub(u, t.v);
+  Tw t = twiddle<KIND, CM>(v, e);
+  return t.neg ? m_add<CM>(u, t.v) : m_sub<CM>(u, t.v);
 }
 
 __host__ __device__ constexpr int ilog2(int n) { return n <= 1 ? 0 : 1 + ilog2(n >> 1); }
@@ -228,7 +229,8 @@ __device__ __forceinline__ void to_bitrev(uint32_t (&a)[N]) {
 // Stages are expanded by template recursion so every register index is a
 // compile-time constant (no local-memory arrays).
 // Stages [S, S_END) are run (S_END = -1: to the end).
-template <int N, int KIND, bool INV, bool ZERO_TOP, bool PRUNE_LO, int S, int S_END = -1>
+template <int N, int KIND, bool INV, bool ZERO_TOP, bool PRUNE_LO, int S, int S_END = -1,
+          int CM = FNT_CARRY_MODE>
 __device__ __forceinline__ void fnt_stage(uint32_t (&a)[N]) {
   constexpr int LG = ilog2(N);
   constexpr int END = S_END < 0 ? LG : S_END;
@@ -243,17 +245,18 @@ __device__ __forceinline__ void fnt_stage(uint32_t (&a)[N]) {
     if (ZERO_TOP && S == 0) {
       a[g + j + half] = a[g + j];
     } else if (PRUNE_LO && S == LG - 1) {
-      a[g + j + half] = bfly_hi<KIND>(a[g + j], a[g + j + half], e);
+      a[g + j + half] = bfly_hi<KIND, CM>(a[g + j], a[g + j + half], e);
     } else {
-      bfly<KIND>(a[g + j], a[g + j + half], e);
+      bfly<KIND, CM>(a[g + j], a[g + j + half], e);
     }
   }
-  if constexpr (S + 1 < END) fnt_stage<N, KIND, INV, ZERO_TOP, PRUNE_LO, S + 1, S_END>(a);
+  if constexpr (S + 1 < END) fnt_stage<N, KIND, INV, ZERO_TOP, PRUNE_LO, S + 1, S_END, CM>(a);
 }
 
-template <int N, int KIND, bool INV, bool ZERO_TOP = false, bool PRUNE_LO = false>
+template <int N, int KIND, bool INV, bool ZERO_TOP = false, bool PRUNE_LO = false,
+          int CM = FNT_CARRY_MODE>
 __device__ __forceinline__ void fnt_dit(uint32_t (&a)[N]) {
-  fnt_stage<N, KIND, INV, ZERO_TOP, PRUNE_LO, 0>(a);
+  fnt_stage<N, KIND, INV, ZERO_TOP, PRUNE_LO, 0, -1, CM>(a);
 }
 
 // Stages [S, S_END) of a forward RADIX2 DIT transform on small signed integers in

@@ -53,6 +53,12 @@ constexpr int AEQ_N = 32;            // block length
                                      // its instruction-cache lines (161 -> 156 ms at config 5)
 constexpr int AEQ_TAP_MAX = 16383;   // TAP_MAG_MAX (aeq.py:26)
 constexpr int XF_LUT = 127;          // x / sig_scale table for |x| <= 127
+#ifndef AEQ_IFNT_CM
+#define AEQ_IFNT_CM FNT_CARRY_MODE   // carry form of the inverse transform (fermat.cuh)
+#endif
+#ifndef AEQ_TAP_CM
+#define AEQ_TAP_CM FNT_CARRY_MODE    // carry form of the tap transform's modular stages
+#endif
 #ifndef AEQ_MIN_CTAS
 #define AEQ_MIN_CTAS 4               // resident CTAs per SM the register budget targets
 #endif
@@ -356,7 +362,7 @@ __device__ __forceinline__ void lane_forward(AeqScratch& S, int lane, int cur, c
     fnt_stage_plain<AEQ_N, RADIX2, 1, 3>(W);
 #pragma unroll
     for (int k = 0; k < AEQ_N; ++k) W[k] += F4 * 8192u;  // 536 879 104 > 2^28
-    fnt_stage<AEQ_N, RADIX2, false, false, false, 3>(W);
+    fnt_stage<AEQ_N, RADIX2, false, false, false, 3, -1, AEQ_TAP_CM>(W);
     uint32_t X[AEQ_N];
 #pragma unroll
     for (int q = 0; q < AEQ_N / 4; ++q) {
@@ -369,7 +375,7 @@ __device__ __forceinline__ void lane_forward(AeqScratch& S, int lane, int cur, c
     // so each output decodes as f4_mod(.) - 32768 (fermat.cuh: f4_mod)
     X[0] = m_add(X[0], 32768u);
     to_bitrev<AEQ_N>(X);
-    fnt_dit<AEQ_N, RADIX2, true, false, true>(X);  // outputs 16..31 only
+    fnt_dit<AEQ_N, RADIX2, true, false, true, AEQ_IFNT_CM>(X);  // outputs 16..31 only
     const int sh = g == 0 ? 7 : 0;                 // recombine 128 hi + lo (fixedpoint.py:139-143)
 #pragma unroll
     for (int m = 0; m < AEQ_L; ++m) S.part[lane][m] = (int32_t)(f4_mod(X[AEQ_L + m]) << sh);

@@ -422,6 +422,11 @@ def main():
                           "alg_ops_per_launch": n_blk_aeq * aeq_int,
                           "fp64_tinst_per_s": aeq_fp64,
                           "fp64_frac": aeq_fp64 / peaks["fp64_tinst"],
+                          # the kernel's two kinds of work share the SM sub-partitions' issue
+                          # slots: INT ops at the INT peak plus FP64 ops at the FP64 peak,
+                          # back to back, over the measured time (INT-only "frac" is the headline)
+                          "int_plus_fp64_frac": (aeq_tops / peaks["int_tops"]
+                                                 + aeq_fp64 / peaks["fp64_tinst"]),
                           "hbm_gbs": aeq_bytes / (aeq_ms * 1e-3) / 1e9},
         "k_decim_phase": {"ms": ph_ms},
     }

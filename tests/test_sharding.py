@@ -116,3 +116,21 @@ def test_split_helpers():
     assert link_shards(4096, 8)[7] == (3584, 512)
     assert input_window(0, 32, 100, 32) == (0, 64)
     assert input_window(48, 32, 10_000, 32) == (32, 64)
+
+
+def test_host_pipeline_segments_cover_exactly():
+    """stream._segments (the pipelined host-buffer paths' input pieces / AEQ time
+    segments): contiguous, aligned boundaries, exact cover, never empty pieces."""
+    from paper_2405_04253_b200.stream import _segments
+    for total in (0, 1, 63, 64, 65, 1000, 1 << 19, 12345):
+        for parts in (1, 3, 4, 8, 100):
+            for align in (1, 64):
+                seg = _segments(total, parts, align)
+                if total == 0:
+                    assert seg == [(0, 0)]
+                    continue
+                assert seg[0][0] == 0 and seg[-1][1] == total
+                assert all(a < b for a, b in seg)
+                assert all(seg[i][1] == seg[i + 1][0] for i in range(len(seg) - 1))
+                assert all(a % align == 0 for a, _ in seg)
+                assert len(seg) <= parts

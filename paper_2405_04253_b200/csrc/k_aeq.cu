@@ -59,6 +59,9 @@ constexpr int XF_LUT = 127;          // x / sig_scale table for |x| <= 127
 #ifndef AEQ_TAP_CM
 #define AEQ_TAP_CM FNT_CARRY_MODE    // carry form of the tap transform's modular stages
 #endif
+#ifndef AEQ_PROBE
+#define AEQ_PROBE 0                  // timing probes only: 1-4 drop one phase (wrong results)
+#endif
 #ifndef AEQ_MIN_CTAS
 #define AEQ_MIN_CTAS 4               // resident CTAs per SM the register budget targets
 #endif
@@ -341,7 +344,9 @@ __device__ __forceinline__ void lane_forward(AeqScratch& S, int lane, int cur, c
                                              int m0, int32_t& yi0, int32_t& yi1) {
   const int s = lane >> 3, t = (lane >> 1) & 3, g = lane & 1;
   if (FWD == FNTGPU_AEQ_FWD_FNT) {
+#if AEQ_PROBE != 1
     warp_input_fnt(S, lane, cur);
+#endif
     // all 16 taps of filter (s, t), group g (split_taps, fixedpoint.py:111-121):
     // own 8 + partner's 8 (lane ^ 1 holds the other half)
     uint32_t W[AEQ_N];
@@ -359,10 +364,14 @@ __device__ __forceinline__ void lane_forward(AeqScratch& S, int lane, int cur, c
     // 2^0..2^12) below 2^28 in plain int32, then a multiple of F4 makes the words
     // non-negative residues of Z/M for stages 3-4
     fnt_stage<AEQ_N, RADIX2, false, true, false, 0, 1>(W);
+#if AEQ_PROBE != 2
     fnt_stage_plain<AEQ_N, RADIX2, 1, 3>(W);
+#endif
 #pragma unroll
     for (int k = 0; k < AEQ_N; ++k) W[k] += F4 * 8192u;  // 536 879 104 > 2^28
+#if AEQ_PROBE != 2
     fnt_stage<AEQ_N, RADIX2, false, false, false, 3, -1, AEQ_TAP_CM>(W);
+#endif
     uint32_t X[AEQ_N];
 #pragma unroll
     for (int q = 0; q < AEQ_N / 4; ++q) {
@@ -375,7 +384,9 @@ __device__ __forceinline__ void lane_forward(AeqScratch& S, int lane, int cur, c
     // so each output decodes as f4_mod(.) - 32768 (fermat.cuh: f4_mod)
     X[0] = m_add(X[0], 32768u);
     to_bitrev<AEQ_N>(X);
+#if AEQ_PROBE != 3
     fnt_dit<AEQ_N, RADIX2, true, false, true, AEQ_IFNT_CM>(X);  // outputs 16..31 only
+#endif
     const int sh = g == 0 ? 7 : 0;                 // recombine 128 hi + lo (fixedpoint.py:139-143)
 #pragma unroll
     for (int m = 0; m < AEQ_L; ++m) S.part[lane][m] = (int32_t)(f4_mod(X[AEQ_L + m]) << sh);
@@ -578,7 +589,9 @@ __global__ void __launch_bounds__(AEQ_WARPS * 32, AEQ_MIN_CTAS) k_aeq_process(fn
       *yrow = make_double2(y0, y1);
       yrow += AEQ_L / 2;
       if (QUICK || io.adapt) {
+#if AEQ_PROBE != 4
         lane_update<QUICK>(A, S, lane, m0, y0, y1, cur, mu, T, err_out);
+#endif
         if (QUICK || err_out) ++err_out;
       }
     }

@@ -23,6 +23,9 @@
 
 namespace fntgpu {
 
+#ifndef CDC_PROBE
+#define CDC_PROBE 0  // timing probes only: 1 / 2 drop the fused requantization / statistics
+#endif
 #ifndef CDC_THREADS
 #define CDC_THREADS 256  // 8 warps, 3 CTAs / SM: fewer independent instruction streams per SM
 #endif                   // than 6 x 128 (the kernel is ~60 KB of straight-line code):
@@ -126,7 +129,7 @@ __device__ __forceinline__ void cdc_epilogue_fast(const CdcArgs& A, const uint32
       zr[e] = (int32_t)f4_mod(m_add(up, um)) - 32768;
       zi[e] = (int32_t)f4_mod(m_rot(m_sub(up, um), 24)) - 32768;
     }
-    if (qr) {
+    if (CDC_PROBE != 1 && qr) {
       uint32_t pr = 0, pi = 0;
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
@@ -160,7 +163,7 @@ __device__ __forceinline__ void cdc_epilogue_fast(const CdcArgs& A, const uint32
           }
       }
     }
-    if (stats) {
+    if (CDC_PROBE != 2 && stats) {
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
         const bool ok = full || (v + e >= lo && v + e < hi);

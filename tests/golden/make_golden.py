@@ -441,6 +441,22 @@ def gen_c3() -> dict:
 
 
 # --------------------------------------------------------------------------
+# float comparators (cdc.py:183-210, aeq.py:193-264): not on the FNT path
+
+def gen_float() -> None:
+    from fntdsp.aeq import td_aeq_float
+    from fntdsp.cdc import fd_cdc_float, td_cdc_float
+    cfg = c2_config()
+    ccfg = cfg.cdc_config("fnt")
+    rng = np.random.default_rng(77)
+    x = (rng.standard_normal(2000) + 1j * rng.standard_normal(2000)) / np.sqrt(2)
+    acfg = cfg.aeq_config()
+    xa = rng.standard_normal((4, 1500))
+    ya, wa = td_aeq_float(xa, acfg, mu_schedule=cfg.mu_schedule())
+    save("float", x=x, fd=fd_cdc_float(x, ccfg), td=td_cdc_float(x, ccfg), xa=xa, ya=ya, wa=wa)
+
+
+# --------------------------------------------------------------------------
 # config 5: the first 64 links, end to end through the reference (hash-only, --big)
 
 C5_LINKS = 64
@@ -558,6 +574,8 @@ def main() -> None:
         digests["aeq"] = gen_aeq()
     if want("cli"):
         gen_cli()
+    if want("float"):
+        gen_float()
     if args.big:
         digests["c3"] = gen_c3()
     if args.big or want("c5") and only is not None:

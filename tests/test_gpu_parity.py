@@ -360,6 +360,40 @@ def test_aeq_bank_many_streams_vs_oracle():
             assert np.array_equal(np.array(st[s].w).reshape(4, 4, 16), oq.w)
 
 
+@pytest.mark.parametrize("case", [
+    dict(radii=[0.6, 1.3]),                                   # 2 rings: general path
+    dict(radii=[0.4, 0.9, 1.5], tap_scale=4096.0),            # 3 rings: fast path, other thresholds
+    dict(radii=[0.1, 0.3, 0.5, 0.8, 1.0, 1.3, 1.6, 2.2]),     # 8 rings
+    dict(no_err=True),                                        # 16QAM rings without err_trace
+])
+def test_aeq_bank_other_parameters_vs_oracle(case):
+    """The equalizer kernel's general (runtime-parameter) path and its compile-time
+    fast path with other rings / tap scales, against the oracle."""
+    import torch
+    from paper_2405_04253_b200.stream import AeqBank
+    kw = {"radii": case["radii"]} if "radii" in case else {}
+    cfg = P.AeqConfig(block_n=32, l_taps=16, mu=1e-4, sig_spec=P.QuantSpec(5, SIG_SCALE),
+                      tap_scale=case.get("tap_scale", 8192.0), **kw)
+    S, nb = 9, 200
+    rng = np.random.default_rng(33)
+    x = rng.integers(-15, 16, (S, 4, 16 * nb)).astype(np.int8)
+    mu = O.mu_blocks(nb, mu1=2e-3, mu2=1e-4, gear_symbols=1600)
+    bank = AeqBank(cfg, S)
+    y = torch.empty((S, 4, 16 * nb), dtype=torch.float64, device="cuda")
+    err = None if case.get("no_err") else torch.empty((S, nb), dtype=torch.float64, device="cuda")
+    bank.run_planar(torch.from_numpy(x).cuda(), nb, y, mu_blocks=torch.from_numpy(mu).cuda(), err=err)
+    yh = y.cpu().numpy()
+    st = bank.read_state()
+    for s in (0, 4, 8):
+        oq = O.Aeq(SIG_SCALE, tap_scale=cfg.tap_scale, mu=cfg.mu, radii=cfg.radii)
+        oy = oq.process(x[s].astype(np.int64), mu_blocks=mu)
+        assert np.array_equal(yh[s], oy), s
+        if err is not None:
+            assert np.array_equal(err.cpu().numpy()[s], np.array(oq.err_trace))
+        assert np.array_equal(np.array(st[s].w).reshape(4, 4, 16), oq.w)
+        assert int(st[s].saturations) == int(oq.saturations)
+
+
 # ------------------------------------------------------- CDC -> AEQ glue chain
 
 def test_chain_matches_reference_glue(golden):

@@ -102,7 +102,8 @@ int fntgpu_cyclic_convolve_complex(const fntgpu_plan* plan, const int64_t* x_re,
 int fntgpu_residue_map(int t, int decode, const int64_t* in, int64_t* out, int64_t n, void* stream);
 
 /* sizeof() of the ABI structs in declaration order (cdc_taps, cdc_io, decim_io,
- * aeq_params, aeq_state, aeq_io) so bindings can verify their layouts. Returns 6. */
+ * aeq_params, aeq_state, aeq_io, td_aeq_io) so bindings can verify their layouts.
+ * Returns 7. */
 int fntgpu_struct_sizes(int64_t* out, int n);
 
 /* ------------------------------------------------------------------------ */
@@ -239,6 +240,26 @@ int fntgpu_aeq_process(fntgpu_aeq_state* state, const fntgpu_aeq_params* params,
 int fntgpu_aeq_update_taps(fntgpu_aeq_state* state, const fntgpu_aeq_params* params,
                            const int64_t* x_block, const double* y, double mu, double* err,
                            void* stream);
+/* ------------------------------------------------------------------------ */
+/* Float per-symbol 4x4 RDE comparator -- td_aeq_float / _td_rde_kernel      */
+/* (aeq.py:193-249); not on the FNT path. 16 taps per filter.                 */
+typedef struct fntgpu_td_aeq_io {
+  int32_t n_streams;
+  int32_t n_radii;            /* 1..8, sorted (aeq.py:50) */
+  int64_t n;                  /* symbols per stream */
+  const double* x;            /* stream s, input row r at x + s * x_stream_stride + r * x_row_stride */
+  int64_t x_stream_stride;
+  int64_t x_row_stride;
+  double* w;                  /* (n_streams, 4, 4, 16) float64 taps, updated in place */
+  const double* mu;           /* (n,) step size of every symbol (mu_schedule(m)) */
+  double radii[8];
+  double* y;                  /* (n_streams, 4, >= n) float64 outputs */
+  int64_t y_stream_stride;
+  int64_t y_row_stride;
+} fntgpu_td_aeq_io;
+
+int fntgpu_td_aeq(const fntgpu_td_aeq_io* io, void* stream);
+
 /* Self-check of the AEQ kernel's two arithmetic shortcuts for these params (no
  * reference counterpart; used by the tests and the CLI selftest): over every int32
  * numerator in [lo, hi), y = y_int / D by reciprocal + one correction step against

@@ -74,6 +74,13 @@ class AeqIO(C.Structure):
                 ("err_stream_stride", C.c_int64)]
 
 
+class TdAeqIO(C.Structure):
+    _fields_ = [("n_streams", C.c_int32), ("n_radii", C.c_int32), ("n", C.c_int64), ("x", vp),
+                ("x_stream_stride", C.c_int64), ("x_row_stride", C.c_int64), ("w", vp), ("mu", vp),
+                ("radii", C.c_double * 8), ("y", vp), ("y_stream_stride", C.c_int64),
+                ("y_row_stride", C.c_int64)]
+
+
 AEQ_STATE_BYTES = C.sizeof(AeqState)
 
 # (symbol, restype, argtypes) for every function declared in include/fntgpu.h
@@ -98,6 +105,7 @@ SIGNATURES = {
     "fntgpu_aeq_init": (C.c_int, [vp, C.c_int, C.POINTER(AeqParams), vp]),
     "fntgpu_aeq_process": (C.c_int, [vp, C.POINTER(AeqParams), C.POINTER(AeqIO), vp]),
     "fntgpu_aeq_update_taps": (C.c_int, [vp, C.POINTER(AeqParams), vp, vp, C.c_double, vp, vp]),
+    "fntgpu_td_aeq": (C.c_int, [C.POINTER(TdAeqIO), vp]),
     "fntgpu_copy2d_async": (C.c_int, [vp, C.c_int64, vp, C.c_int64, C.c_int64, C.c_int64, vp]),
     "fntgpu_aeq_selfcheck": (C.c_int, [C.POINTER(AeqParams), C.c_int64, C.c_int64, vp, vp]),
 }

@@ -288,45 +288,44 @@ class FntAeq:
 
 def td_aeq_float(x: np.ndarray, config: AeqConfig, mu_schedule=None,
                  w0: np.ndarray | None = None) -> tuple[np.ndarray, np.ndarray]:
-    """Per-symbol float 4x4 RDE baseline (aeq.py:193-249).
+    """Per-symbol float 4x4 RDE baseline (aeq.py:193-249): returns (outputs, final taps).
 
-    Not on the FNT path: the paper's float comparator. Implemented as a plain
-    host loop in float64 (the reference JIT-compiles the same loop with numba),
-    kept for API completeness and the penalty comparison."""
-    x = np.asarray(x, dtype=float)
+    Not on the FNT path (the paper's float comparator). Runs on the GPU
+    (k_td_aeq, one warp per stream, every product and sum rounded separately in
+    the reference's order), so the results equal the reference's numba kernel bit
+    for bit. 16 taps per filter (the reference's AeqConfig default)."""
+    t = _lib.torch()
+    x = np.ascontiguousarray(np.asarray(x, dtype=np.float64))
+    if x.ndim != 2 or x.shape[0] != 4:
+        raise ValueError("x must have shape (4, n)")
     n = x.shape[1]
     L = config.l_taps
+    if L != 16:
+        raise NotImplementedError("the GPU float comparator runs 16-tap filters")
     if w0 is None:
         w = np.zeros((4, 4, L))
         for s in range(4):
             w[s, s, L // 2] = 1.0
     else:
-        w = w0.astype(float).copy()
+        w = np.ascontiguousarray(np.asarray(w0, dtype=np.float64)).copy()
     mu_arr = (np.full(n, config.mu) if mu_schedule is None
-              else np.array([mu_schedule(i) for i in range(n)]))
+              else np.array([mu_schedule(i) for i in range(n)], dtype=np.float64))
     radii = np.asarray(config.radii, dtype=float)
-    y = np.zeros((4, n))
+    if not 1 <= radii.size <= 8:
+        raise NotImplementedError("the GPU equalizer supports 1..8 ring radii")
+    dev = _lib.device()
+    dx = t.from_numpy(x).to(dev)
+    dw = t.from_numpy(w).to(dev)
+    dmu = t.from_numpy(np.ascontiguousarray(mu_arr)).to(dev)
+    dy = t.empty((4, n), dtype=t.float64, device=dev)
+    io = _lib.TdAeqIO()
+    io.n_streams, io.n_radii, io.n = 1, int(radii.size), n
+    io.x, io.x_stream_stride, io.x_row_stride = dx.data_ptr(), 4 * n, n
+    io.w, io.mu = dw.data_ptr(), dmu.data_ptr()
+    for i, r in enumerate(radii):
+        io.radii[i] = float(r)
+    io.y, io.y_stream_stride, io.y_row_stride = dy.data_ptr(), 4 * n, n
     with COUNTER.scope("aeq-td"):
-        for m in range(L - 1, n):
-            win = x[:, m - L + 1:m + 1][:, ::-1]
-            for s2 in range(4):
-                acc = 0.0
-                for s1 in range(4):
-                    for k in range(L):
-                        acc += w[s2, s1, k] * win[s1, k]
-                y[s2, m] = acc
-            for pol in range(2):
-                yi, yq = y[2 * pol, m], y[2 * pol + 1, m]
-                r = np.sqrt(yi * yi + yq * yq)
-                best = radii[0]
-                for ri in range(1, radii.size):
-                    if abs(radii[ri] - r) < abs(best - r):
-                        best = radii[ri]
-                e = best * best - (yi * yi + yq * yq)
-                for ii in range(2):
-                    s2 = 2 * pol + ii
-                    g = mu_arr[m] * e * y[s2, m]
-                    if g != 0.0:
-                        w[s2] += g * win
+        _lib.check(_lib.load().fntgpu_td_aeq(C.byref(io), _lib.stream_handle()), "td_aeq")
         COUNTER.add(16 * L * n)
-    return y, w
+    return dy.cpu().numpy(), dw.cpu().numpy()

@@ -17,6 +17,7 @@ cudaError_t launch_aeq_update_once(fntgpu_aeq_state* st, const fntgpu_aeq_params
                                    cudaStream_t s);
 cudaError_t launch_aeq_selfcheck(const fntgpu_aeq_params& prm, int64_t lo, int64_t hi,
                                  unsigned long long* mismatches, cudaStream_t s);
+cudaError_t launch_td_aeq(const fntgpu_td_aeq_io& io, cudaStream_t s);
 }
 
 using namespace fntgpu;
@@ -256,11 +257,12 @@ int fntgpu_residue_map(int t, int decode, const int64_t* in, int64_t* out, int64
 }
 
 int fntgpu_struct_sizes(int64_t* out, int n) {
-  const int64_t sz[6] = {(int64_t)sizeof(fntgpu_cdc_taps), (int64_t)sizeof(fntgpu_cdc_io),
+  const int64_t sz[7] = {(int64_t)sizeof(fntgpu_cdc_taps), (int64_t)sizeof(fntgpu_cdc_io),
                          (int64_t)sizeof(fntgpu_decim_io), (int64_t)sizeof(fntgpu_aeq_params),
-                         (int64_t)sizeof(fntgpu_aeq_state), (int64_t)sizeof(fntgpu_aeq_io)};
-  for (int i = 0; i < n && i < 6; ++i) out[i] = sz[i];
-  return 6;
+                         (int64_t)sizeof(fntgpu_aeq_state), (int64_t)sizeof(fntgpu_aeq_io),
+                         (int64_t)sizeof(fntgpu_td_aeq_io)};
+  for (int i = 0; i < n && i < 7; ++i) out[i] = sz[i];
+  return 7;
 }
 
 int fntgpu_cdc64_process(const fntgpu_cdc_taps* taps, const fntgpu_cdc_io* io, void* stream) {
@@ -370,6 +372,17 @@ int fntgpu_aeq_update_taps(fntgpu_aeq_state* st, const fntgpu_aeq_params* prm,
   if (mu < 0) return fail(FNTGPU_EINVAL, "mu must be >= 0");
   if ((rc = check_device("aeq_update_taps"))) return rc;
   return cuda_rc(launch_aeq_update_once(st, *prm, x_block, y, mu, err, S(stream)), "aeq_update_taps");
+}
+
+int fntgpu_td_aeq(const fntgpu_td_aeq_io* io, void* stream) {
+  if (!io) return fail(FNTGPU_EINVAL, "td_aeq: NULL argument");
+  if (io->n_streams < 0 || io->n < 0) return fail(FNTGPU_EINVAL, "td_aeq: negative size");
+  if (io->n_radii < 1 || io->n_radii > 8) return fail(FNTGPU_EINVAL, "td_aeq: 1..8 ring radii");
+  if (io->n_streams > 0 && io->n > 0 && (!io->x || !io->w || !io->mu || !io->y))
+    return fail(FNTGPU_EINVAL, "td_aeq: NULL buffer");
+  int rc;
+  if ((rc = check_device("td_aeq"))) return rc;
+  return cuda_rc(launch_td_aeq(*io, S(stream)), "td_aeq");
 }
 
 int fntgpu_aeq_selfcheck(const fntgpu_aeq_params* prm, int64_t lo, int64_t hi,

@@ -30,10 +30,10 @@ def test_library_builds_and_exports_every_declared_symbol():
 def test_struct_layouts_match_binding():
     from paper_2405_04253_b200 import _lib
     lib = _lib.load()
-    out = (C.c_int64 * 6)()
-    assert lib.fntgpu_struct_sizes(out, 6) == 6
+    out = (C.c_int64 * 7)()
+    assert lib.fntgpu_struct_sizes(out, 7) == 7
     mine = [C.sizeof(s) for s in (_lib.CdcTaps, _lib.CdcIO, _lib.DecimIO, _lib.AeqParams,
-                                  _lib.AeqState, _lib.AeqIO)]
+                                  _lib.AeqState, _lib.AeqIO, _lib.TdAeqIO)]
     assert list(out) == mine
 
 
@@ -97,7 +97,7 @@ def test_integration_md_binding_stub_matches_abi(monkeypatch):
     exec(compile(code, "INTEGRATION.md", "exec"), ns)
     from paper_2405_04253_b200 import _lib
     lib = _lib.load()
-    out = (C.c_int64 * 6)()
-    lib.fntgpu_struct_sizes(out, 6)
+    out = (C.c_int64 * 7)()
+    lib.fntgpu_struct_sizes(out, 7)
     assert C.sizeof(ns["CdcTaps"]) == out[0]
     assert C.sizeof(ns["CdcIO"]) == out[1]

@@ -1,7 +1,7 @@
 """The float comparators (not on the FNT path) against the reference's own outputs
-(tests/golden/float.npz): the per-symbol TD-AEQ host loop reproduces the
-reference's numba kernel bit for bit; the GPU FD/TD CDC (cuFFT / conv1d, library
-code) agree to float64 rounding."""
+(tests/golden/float.npz): the per-symbol TD-AEQ kernel reproduces the reference's
+numba kernel bit for bit; the GPU FD/TD CDC (cuFFT / conv1d, library code) agree
+to float64 rounding."""
 
 import numpy as np
 import pytest
@@ -9,6 +9,7 @@ import pytest
 import paper_2405_04253_b200 as P
 
 
+@pytest.mark.gpu
 def test_td_aeq_float_matches_reference(golden):
     g = golden("float")
     cfg = P.LinkConfig()

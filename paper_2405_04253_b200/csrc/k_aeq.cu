@@ -160,8 +160,8 @@ __device__ __forceinline__ int32_t requantize_tap(double w, double tap_scale, ui
   const double p = dmul(w, tap_scale);
   const int32_t i = __double2int_rn(p);
   const bool huge = !(fabs(p) < 9.2233720368547758e18);
-  sat += ((i > AEQ_TAP_MAX) | (i < -AEQ_TAP_MAX)) & !huge;
   const int32_t c = min(max(i, -AEQ_TAP_MAX), AEQ_TAP_MAX);
+  sat += (c != i) & !huge;  // clipped exactly when |rint| > 16383
   return huge ? -AEQ_TAP_MAX : c;
 }
 

@@ -285,7 +285,9 @@ def main():
     ap.add_argument("--links", type=int, default=4096, help="links per GPU (C5: 4096)")
     ap.add_argument("--symbols", type=int, default=1 << 18)
     ap.add_argument("--forward", default="fnt", choices=["fnt", "direct"])
-    ap.add_argument("--e2e-links", type=int, default=512)
+    ap.add_argument("--e2e-links", type=int, default=None,
+                    help="links per rank in the host-buffer e2e run (default 512 on one GPU, "
+                         "256 per rank under torchrun: bounds the pinned host memory per node)")
     ap.add_argument("--cpu-symbols", type=int, default=1 << 13)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -662,7 +664,8 @@ def run_e2e(args, eng, cfg, xr, xi, fwd, world):
     import torch
     import torch.distributed as dist
     from paper_2405_04253_b200.stream import HostChain
-    n = min(args.e2e_links, args.links)
+    e2e_links = args.e2e_links if args.e2e_links is not None else (512 if world == 1 else 256)
+    n = min(e2e_links, args.links)
     L = 2 * args.symbols
     hc = HostChain(eng, cfg.aeq_config(), n, L, cfg.sig_spec(), cfg.mu_schedule(), forward=fwd)
     hx_r = torch.empty((2 * n, L), dtype=torch.int8, pin_memory=True)

@@ -540,6 +540,18 @@ def run_cpu_cdc_baseline(eng, n: int, cores: int) -> dict:
                        f"process_int), one process per core, {wall:.1f} s wall")}
 
 
+def c4_traffic(world: int):
+    """DRAM bytes of one k_cdc64 launch at config 4 on one GPU, from the committed ncu
+    --set full capture (profiles/ncu_summary_r01_c4.json); None for other shard sizes."""
+    path = PROFILES / "ncu_summary_r01_c4.json"
+    if world != 1 or not path.exists():
+        return None
+    try:
+        return json.loads(path.read_text()).get("per_launch_dram_bytes", {}).get("k_cdc64")
+    except Exception:
+        return None
+
+
 def run_c4(args, world, rank, local):
     """BASELINE config 4: one dual-pol stream of 2^31 complex samples per
     polarization, FNT-CDC range-sharded across ranks (strong scaling: the stream
@@ -622,7 +634,7 @@ def run_c4(args, world, rank, local):
                    "l2": "inputs (%.1f GB) exceed L2" % (hbm_bytes / 1e9)},
         "roofline": {"bound": "int", "kernel": "k_cdc64", "achieved": achieved,
                      "peak": peaks["int_tops"], "unit": "Tops/s",
-                     "frac": achieved / peaks["int_tops"], "traffic": None,
+                     "frac": achieved / peaks["int_tops"], "traffic": c4_traffic(world),
                      "peak_source": peaks["int_source"],
                      "hbm": {"achieved_gbs": hbm_gbs, "peak_gbs": peaks["hbm_gbs"],
                              "frac": hbm_gbs / peaks["hbm_gbs"]}},

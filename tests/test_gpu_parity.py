@@ -383,6 +383,32 @@ def test_aeq_bank_many_streams_vs_oracle():
             assert np.array_equal(np.array(st[s].w).reshape(4, 4, 16), oq.w)
 
 
+@pytest.mark.parametrize("forward", AEQ_MODES)
+def test_aeq_bank_wide_int32_inputs_vs_oracle(forward):
+    """int32 planar inputs up to |x| = 2^15 (group convolutions wrap mod F4 and are
+    decoded one by one, as in the reference) through the multi-stream kernel's fast
+    path (per-block mu, err_trace), against the oracle."""
+    import torch
+    from paper_2405_04253_b200.stream import AeqBank
+    cfg = P.LinkConfig().aeq_config()
+    S, nb = 5, 120
+    rng = np.random.default_rng(44)
+    x = rng.integers(-32768, 32769, (S, 4, 16 * nb)).astype(np.int32)
+    mu = O.mu_blocks(nb, mu1=2e-3, mu2=1e-4, gear_symbols=800)
+    bank = AeqBank(cfg, S, forward=forward)
+    y = torch.empty((S, 4, 16 * nb), dtype=torch.float64, device="cuda")
+    err = torch.empty((S, nb), dtype=torch.float64, device="cuda")
+    bank.run_planar(torch.from_numpy(x).cuda(), nb, y, mu_blocks=torch.from_numpy(mu).cuda(), err=err)
+    st = bank.read_state()
+    for s in range(S):
+        oq = O.Aeq(cfg.sig_spec.scale, mu=cfg.mu)
+        oy = oq.process(x[s].astype(np.int64), mu_blocks=mu)
+        assert np.array_equal(y[s].cpu().numpy(), oy), (forward, s)
+        assert np.array_equal(err[s].cpu().numpy(), np.array(oq.err_trace))
+        assert np.array_equal(np.array(st[s].w).reshape(4, 4, 16), oq.w)
+        assert int(st[s].saturations) == int(oq.saturations)
+
+
 @pytest.mark.parametrize("case", [
     dict(radii=[0.6, 1.3]),                                   # 2 rings: general path
     dict(radii=[0.4, 0.9, 1.5], tap_scale=4096.0),            # 3 rings: fast path, other thresholds

@@ -23,6 +23,12 @@
 
 namespace fntgpu {
 
+#ifndef CDC_MIN_CTAS
+#define CDC_MIN_CTAS 3  // 3 x 256 threads per SM: caps registers at 80
+#endif
+#ifndef CDC_TMA
+#define CDC_TMA 1  // interior input windows staged by cp.async.bulk (TMA) + mbarrier
+#endif
 #ifndef CDC_PROBE
 #define CDC_PROBE 0  // timing probes only: 1 / 2 drop the fused requantization / statistics
 #endif
@@ -211,7 +217,7 @@ __device__ __forceinline__ int32_t sx8(uint32_t w, int k) {
 }
 
 template <typename TIN, bool FAST>
-__global__ void __launch_bounds__(CDC_CTA) k_cdc64(const __grid_constant__ CdcArgs A) {
+__global__ void __launch_bounds__(CDC_CTA, CDC_MIN_CTAS) k_cdc64(const __grid_constant__ CdcArgs A) {
   using TS = typename std::conditional<sizeof(TIN) == 1, int8_t, int32_t>::type;
   // the input window and the u staging rows are never live at the same time
   extern __shared__ __align__(16) unsigned char smem[];
@@ -226,8 +232,41 @@ __global__ void __launch_bounds__(CDC_CTA) k_cdc64(const __grid_constant__ CdcAr
 
   const TIN* xr_s = reinterpret_cast<const TIN*>(io.xr) + (size_t)s * io.x_stride;
   const TIN* xi_s = reinterpret_cast<const TIN*>(io.xi) + (size_t)s * io.x_stride;
-  stage_plane<TIN, TS>(s_xr, xr_s, g0, io);
-  stage_plane<TIN, TS>(s_xi, xi_s, g0, io);
+  bool bulk = false;
+  if (sizeof(TIN) == 1 && CDC_TMA) {
+    // interior windows of int8 planes: two 1-D bulk copies (TMA engine) straight into
+    // shared memory, completion counted on an mbarrier; edges and unaligned views
+    // take the vectorised load path
+    const int64_t lo = io.x_first > 0 ? io.x_first : 0;
+    const int64_t hi_avail = io.x_first + io.x_count;
+    const int64_t hi = hi_avail < io.length ? hi_avail : io.length;
+    const TIN* pr = xr_s + (g0 - io.x_first);
+    const TIN* pi = xi_s + (g0 - io.x_first);
+    bulk = g0 >= lo && g0 + WIN <= hi && ((reinterpret_cast<uintptr_t>(pr) | reinterpret_cast<uintptr_t>(pi)) & 15) == 0;
+    if (bulk) {
+      __shared__ __align__(8) uint64_t mbar;
+      const uint32_t mb = (uint32_t)__cvta_generic_to_shared(&mbar);
+      if (threadIdx.x == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" :: "r"(mb) : "memory");
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" :: "r"(mb), "r"(2 * WIN) : "memory");
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                     :: "r"((uint32_t)__cvta_generic_to_shared(s_xr)), "l"(pr), "r"(WIN), "r"(mb) : "memory");
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                     :: "r"((uint32_t)__cvta_generic_to_shared(s_xi)), "l"(pi), "r"(WIN), "r"(mb) : "memory");
+      }
+      __syncthreads();  // barrier initialised before anyone polls it
+      uint32_t done = 0;
+      while (!done) {
+        asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0;\n\t"
+                     "selp.u32 %0, 1, 0, p;\n\t}" : "=r"(done) : "r"(mb) : "memory");
+      }
+    }
+  }
+  if (!bulk) {
+    stage_plane<TIN, TS>(s_xr, xr_s, g0, io);
+    stage_plane<TIN, TS>(s_xi, xi_s, g0, io);
+  }
   __syncthreads();
 
   const int tid = threadIdx.x;

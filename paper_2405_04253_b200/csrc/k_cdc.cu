@@ -26,6 +26,12 @@ namespace fntgpu {
 #ifndef CDC_MIN_CTAS
 #define CDC_MIN_CTAS 3  // 3 x 256 threads per SM: caps registers at 80
 #endif
+#ifndef CDC_FWD_CM
+#define CDC_FWD_CM FNT_CARRY_MODE  // carry form of the forward transform's modular stages
+#endif
+#ifndef CDC_INV_CM
+#define CDC_INV_CM FNT_CARRY_MODE  // carry form of the inverse transform
+#endif
 #ifndef CDC_TMA
 #define CDC_TMA 1  // interior input windows staged by cp.async.bulk (TMA) + mbarrier
 #endif
@@ -307,7 +313,7 @@ __global__ void __launch_bounds__(CDC_CTA, CDC_MIN_CTAS) k_cdc64(const __grid_co
     fnt_stage_plain<CDC_N, SQRT2, 0, 2>(a);
 #pragma unroll
     for (int k = 0; k < CDC_N; ++k) a[k] += F4 * 1024u;
-    fnt_stage<CDC_N, SQRT2, false, false, false, 2>(a);
+    fnt_stage<CDC_N, SQRT2, false, false, false, 2, -1, CDC_FWD_CM>(a);
   } else {
     fnt_dit<CDC_N, SQRT2, false>(a);
   }
@@ -320,7 +326,7 @@ __global__ void __launch_bounds__(CDC_CTA, CDC_MIN_CTAS) k_cdc64(const __grid_co
   // f4_mod(.) - 32768 (fermat.cuh) instead of a two-sided range fold.
   a[0] = m_add(a[0], sgn ? 16448u : 16320u);
   to_bitrev<CDC_N>(a);
-  fnt_dit<CDC_N, SQRT2, true, false, true>(a);             // outputs 32..63 only
+  fnt_dit<CDC_N, SQRT2, true, false, true, CDC_INV_CM>(a);  // outputs 32..63 only
   __syncthreads();  // every thread has consumed the input window
   {
     uint32_t* row = s_u + (sgn * CDC_BLK + bl) * UP;

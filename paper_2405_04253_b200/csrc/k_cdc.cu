@@ -47,7 +47,12 @@ constexpr int CDC_BLK = CDC_CTA / 2;            // overlap-save blocks per CTA (
 constexpr int CDC_N = 64;
 constexpr int CDC_HOP = 32;
 constexpr int WIN = CDC_HOP * (CDC_BLK + 1);    // input samples staged per plane
-constexpr int UP = 33;                          // padded pitch of the u staging rows
+#ifndef CDC_UP
+#define CDC_UP 36
+#endif
+constexpr int UP = CDC_UP;                      // pitch of the u staging rows: 36 words keeps
+                                                // rows 16-byte aligned (vector stores / loads)
+                                                // with conflict-free 128-bit wavefronts
 
 struct CdcArgs {
   uint32_t bp[CDC_N];  // b+ * 2^25 mod F4
@@ -135,9 +140,19 @@ __device__ __forceinline__ void cdc_epilogue_fast(const CdcArgs& A, const uint32
     const bool full = v >= lo && v + 4 <= hi;
     const int rb = (v >> 5) * UP + (v & 31);
     int32_t zr[4], zi[4];
+    uint32_t upv[4], umv[4];
+    if (UP % 4 == 0) {
+      const uint4 p4 = *reinterpret_cast<const uint4*>(s_u + rb);
+      const uint4 m4 = *reinterpret_cast<const uint4*>(s_u + CDC_BLK * UP + rb);
+      upv[0] = p4.x; upv[1] = p4.y; upv[2] = p4.z; upv[3] = p4.w;
+      umv[0] = m4.x; umv[1] = m4.y; umv[2] = m4.z; umv[3] = m4.w;
+    } else {
+#pragma unroll
+      for (int e = 0; e < 4; ++e) { upv[e] = s_u[rb + e]; umv[e] = s_u[CDC_BLK * UP + rb + e]; }
+    }
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
-      const uint32_t up = s_u[rb + e], um = s_u[CDC_BLK * UP + rb + e];
+      const uint32_t up = upv[e], um = umv[e];
       zr[e] = (int32_t)f4_mod(m_add(up, um)) - 32768;
       zi[e] = (int32_t)f4_mod(m_rot(m_sub(up, um), 24)) - 32768;
     }
@@ -330,8 +345,15 @@ __global__ void __launch_bounds__(CDC_CTA, CDC_MIN_CTAS) k_cdc64(const __grid_co
   __syncthreads();  // every thread has consumed the input window
   {
     uint32_t* row = s_u + (sgn * CDC_BLK + bl) * UP;
+    if (UP % 4 == 0) {
 #pragma unroll
-    for (int j = 0; j < CDC_HOP; ++j) row[j] = a[CDC_HOP + j];
+      for (int j = 0; j < CDC_HOP; j += 4)
+        *reinterpret_cast<uint4*>(row + j) = make_uint4(a[CDC_HOP + j], a[CDC_HOP + j + 1],
+                                                        a[CDC_HOP + j + 2], a[CDC_HOP + j + 3]);
+    } else {
+#pragma unroll
+      for (int j = 0; j < CDC_HOP; ++j) row[j] = a[CDC_HOP + j];
+    }
   }
   __syncthreads();
 

@@ -61,6 +61,7 @@ struct CdcArgs {
   int64_t blk_begin;   // first overlap-save block index of this launch
   int64_t blk_count;   // blocks per stream
   int32_t c;           // n_taps // 2
+  int32_t s_base;      // first stream of this launch (grid.y is limited to 65535)
 };
 
 __device__ __forceinline__ int32_t sext8(uint32_t w, int k) {
@@ -247,7 +248,7 @@ __global__ void __launch_bounds__(CDC_CTA, CDC_MIN_CTAS) k_cdc64(const __grid_co
   uint32_t* s_u = reinterpret_cast<uint32_t*>(smem);  // [sign][block][UP]
 
   const fntgpu_cdc_io& io = A.io;
-  const int s = blockIdx.y;
+  const int s = A.s_base + (int)blockIdx.y;
   const int64_t cta_blk0 = A.blk_begin + (int64_t)blockIdx.x * CDC_BLK;
   const int64_t g0 = cta_blk0 * CDC_HOP - CDC_HOP;  // first input sample of block cta_blk0
 
@@ -491,7 +492,7 @@ cudaError_t launch_cdc64(const fntgpu_cdc_taps& taps, const fntgpu_cdc_io& io, c
   const int64_t b_hi = (io.out_first + io.out_count - 1 + A.c) / CDC_HOP;
   A.blk_begin = b_lo;
   A.blk_count = b_hi - b_lo + 1;
-  dim3 grid((unsigned)((A.blk_count + CDC_BLK - 1) / CDC_BLK), (unsigned)io.n_streams);
+  dim3 grid((unsigned)((A.blk_count + CDC_BLK - 1) / CDC_BLK), 1u);
   // vectorised epilogue preconditions (see cdc_epilogue_fast)
   auto al4 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 3) == 0; };
   bool fast = (io.out_dtype == FNTGPU_NONE || io.out_dtype == FNTGPU_I16) &&
@@ -501,13 +502,22 @@ cudaError_t launch_cdc64(const fntgpu_cdc_taps& taps, const fntgpu_cdc_io& io, c
   if (io.out_dtype == FNTGPU_I16)
     fast = fast && (reinterpret_cast<uintptr_t>(io.yr) & 7) == 0 &&
            (reinterpret_cast<uintptr_t>(io.yi) & 7) == 0 && io.y_stride % 4 == 0;
-  switch (io.in_dtype) {
-    case FNTGPU_I8:
-      return fast ? launch_k<int8_t, true>(A, grid, st) : launch_k<int8_t, false>(A, grid, st);
-    case FNTGPU_I32: return launch_k<int32_t, false>(A, grid, st);
-    case FNTGPU_I64: return launch_k<int64_t, false>(A, grid, st);
-    default: return cudaErrorInvalidValue;
+  if (io.in_dtype != FNTGPU_I8 && io.in_dtype != FNTGPU_I32 && io.in_dtype != FNTGPU_I64)
+    return cudaErrorInvalidValue;
+  for (int64_t s0 = 0; s0 < io.n_streams; s0 += 65535) {
+    A.s_base = (int32_t)s0;
+    grid.y = (unsigned)(io.n_streams - s0 < 65535 ? io.n_streams - s0 : 65535);
+    cudaError_t e;
+    switch (io.in_dtype) {
+      case FNTGPU_I8:
+        e = fast ? launch_k<int8_t, true>(A, grid, st) : launch_k<int8_t, false>(A, grid, st);
+        break;
+      case FNTGPU_I32: e = launch_k<int32_t, false>(A, grid, st); break;
+      default: e = launch_k<int64_t, false>(A, grid, st); break;
+    }
+    if (e != cudaSuccess) return e;
   }
+  return cudaSuccess;
 }
 
 cudaError_t launch_decim_phase(const fntgpu_decim_io& io, cudaStream_t s) {

@@ -203,6 +203,23 @@ def test_cdc_edges(golden):
         eng.process_int(np.full(10, 40000), np.zeros(10))
 
 
+def test_cdc_more_streams_than_one_grid_dimension():
+    """70 000 short streams in one call (the launcher splits grid.y at 65 535)."""
+    import torch
+    from paper_2405_04253_b200.stream import CdcBank
+    eng = _c2_engine()
+    rng = np.random.default_rng(9)
+    S, L = 70_000, 96
+    xr = rng.integers(-15, 16, (S, L)).astype(np.int8)
+    xi = rng.integers(-15, 16, (S, L)).astype(np.int8)
+    yr = torch.empty((S, L), dtype=torch.int32, device="cuda")
+    yi = torch.empty_like(yr)
+    CdcBank(eng).run(torch.from_numpy(xr).cuda(), torch.from_numpy(xi).cuda(), length=L, yr=yr, yi=yi)
+    for s in (0, 65534, 65535, 65536, S - 1):
+        orr, oi = O.cdc_process_int(eng.tap_re, eng.tap_im, xr[s], xi[s])
+        assert np.array_equal(yr[s].cpu().numpy(), orr) and np.array_equal(yi[s].cpu().numpy(), oi), s
+
+
 def test_cdc_int8_full_range_vs_oracle():
     """int8 planes over their whole range (the kernel's carry-free first stages
     assume |x_r +- 2^8 x_i| <= 32896) and wrapping outputs, against the oracle."""

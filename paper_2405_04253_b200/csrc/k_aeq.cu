@@ -59,6 +59,9 @@ constexpr int XF_LUT = 127;          // x / sig_scale table for |x| <= 127
 #ifndef AEQ_TAP_CM
 #define AEQ_TAP_CM FNT_CARRY_MODE    // carry form of the tap transform's modular stages
 #endif
+#ifndef AEQ_DP4A
+#define AEQ_DP4A 1                   // DIRECT forward on int8 inputs by DP4A int8 dot products
+#endif
 #ifndef AEQ_PROBE
 #define AEQ_PROBE 0                  // timing probes only: 1-4 drop one phase (wrong results)
 #endif
@@ -77,6 +80,8 @@ struct __align__(16) AeqScratch {
   int32_t xi[4][2][AEQ_L];    // input integer ring: [t][block parity][j]
   uint32_t X[4][AEQ_N + 4];   // cooperative input spectra (FNT path), 16-B aligned padded rows
   double err[32];             // |e| values for the err_trace mean
+  uint8_t xq[4][64];          // DIRECT, int8 inputs: x_block[t] reversed as bytes, ring of 32
+                              // stored twice: block b's samples j at 16 * parity + 15 - j (+ 32)
 };
 
 struct AeqArgs {
@@ -339,9 +344,44 @@ __device__ __forceinline__ void warp_input_fnt(AeqScratch& S, int lane, int cur)
 }
 
 // Forward path for one block: returns y_int[s][m0], y_int[s][m0+1] in yi0, yi1.
-template <int FWD>
+// DIRECT form on int8 inputs: the per-group sums of 8 taps as two 4-way int8 dot
+// products (DP4A) per output, from the reversed byte ring (x_block[16 + m - k] for
+// k = 8g + q is byte 15 - m + q of the lane's window, and 19 - m + q for k + 4).
+__device__ __forceinline__ void direct_dp4a(const AeqScratch& S, int t, int g, int cur,
+                                            const LaneTaps& T, int32_t (&hi)[AEQ_L],
+                                            int32_t (&lo)[AEQ_L]) {
+  const uint2* qb = reinterpret_cast<const uint2*>(S.xq[t] + AEQ_L * cur + 8 * g);
+  uint32_t R[6];
+#pragma unroll
+  for (int q = 0; q < 3; ++q) {
+    const uint2 v = qb[q];
+    R[2 * q] = v.x;
+    R[2 * q + 1] = v.y;
+  }
+  // tap groups as int8 quadruples: hi group = byte 0 of p, lo group = byte 2 of
+  // p + 2^15 (pack_groups: p = sign (hi + lo 2^16), |hi|, |lo| <= 127)
+  uint32_t th[2], tl[2];
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const uint32_t p0 = T.gp[4 * h], p1 = T.gp[4 * h + 1], p2 = T.gp[4 * h + 2], p3 = T.gp[4 * h + 3];
+    th[h] = __byte_perm(__byte_perm(p0, p1, 0x0040), __byte_perm(p2, p3, 0x0040), 0x5410);
+    const uint32_t q0 = p0 + 0x8000u, q1 = p1 + 0x8000u, q2 = p2 + 0x8000u, q3 = p3 + 0x8000u;
+    tl[h] = __byte_perm(__byte_perm(q0, q1, 0x0062), __byte_perm(q2, q3, 0x0062), 0x5410);
+  }
+#pragma unroll
+  for (int m = 0; m < AEQ_L; ++m) {
+    const int oa = 15 - m, ob = 19 - m;
+    const uint32_t xa = (oa & 3) ? __funnelshift_r(R[oa >> 2], R[(oa >> 2) + 1], 8 * (oa & 3)) : R[oa >> 2];
+    const uint32_t xb = (ob & 3) ? __funnelshift_r(R[ob >> 2], R[(ob >> 2) + 1], 8 * (ob & 3)) : R[ob >> 2];
+    hi[m] = __dp4a((int)th[0], (int)xa, __dp4a((int)th[1], (int)xb, 0));
+    lo[m] = __dp4a((int)tl[0], (int)xa, __dp4a((int)tl[1], (int)xb, 0));
+  }
+}
+
+template <int FWD, bool NARROW = false>
 __device__ __forceinline__ void lane_forward(AeqScratch& S, int lane, int cur, const LaneTaps& T,
-                                             int m0, int32_t& yi0, int32_t& yi1) {
+                                             int m0, int32_t& yi0, int32_t& yi1,
+                                             bool use_dp4a = false) {
   const int s = lane >> 3, t = (lane >> 1) & 3, g = lane & 1;
   if (FWD == FNTGPU_AEQ_FWD_FNT) {
 #if AEQ_PROBE != 1
@@ -397,6 +437,24 @@ __device__ __forceinline__ void lane_forward(AeqScratch& S, int lane, int cur, c
     for (int q = 0; q < 8; ++q) {
       a0 += S.part[s * 8 + q][m0];
       a1 += S.part[s * 8 + q][m0 + 1];
+    }
+    yi0 = a0;
+    yi1 = a1;
+  } else if (NARROW && AEQ_DP4A && use_dp4a) {
+    int32_t hi[AEQ_L], lo[AEQ_L];
+    direct_dp4a(S, t, g, cur, T, hi, lo);
+#pragma unroll
+    for (int m = 0; m < AEQ_L; ++m) { S.part[lane][m] = hi[m]; S.part[lane][AEQ_L + m] = lo[m]; }
+    __syncwarp();
+    int32_t a0 = -4 * 129 * 32768, a1 = -4 * 129 * 32768;
+#pragma unroll
+    for (int tt = 0; tt < 4; ++tt) {
+      const int l0 = s * 8 + tt * 2;
+      const int32_t B = (int32_t)(F4 * 1024u) + 32768;
+      a0 += 128 * (int32_t)f4_mod((uint32_t)(S.part[l0][m0] + S.part[l0 + 1][m0] + B)) +
+            (int32_t)f4_mod((uint32_t)(S.part[l0][AEQ_L + m0] + S.part[l0 + 1][AEQ_L + m0] + B));
+      a1 += 128 * (int32_t)f4_mod((uint32_t)(S.part[l0][m0 + 1] + S.part[l0 + 1][m0 + 1] + B)) +
+            (int32_t)f4_mod((uint32_t)(S.part[l0][AEQ_L + m0 + 1] + S.part[l0 + 1][AEQ_L + m0 + 1] + B));
     }
     yi0 = a0;
     yi1 = a1;
@@ -499,8 +557,20 @@ __global__ void __launch_bounds__(AEQ_WARPS * 32, AEQ_MIN_CTAS) k_aeq_process(fn
     S.xf[tq][1 + AEQ_L + iq + 1] = f1;
     S.xf[tq][1 + AEQ_L + iq + 32] = f0;
     S.xf[tq][1 + AEQ_L + iq + 33] = f1;
+    if (FWD == FNTGPU_AEQ_FWD_DIRECT && NARROW && AEQ_DP4A) {
+      // reversed byte ring, slot 1: samples iq + 1, iq at 16 + 14 - iq (+ 32); only
+      // used when the whole history fits int8 (use_dp4a)
+      const uint16_t pr = (uint16_t)(((uint32_t)h1 & 0xffu) | (((uint32_t)h0 & 0xffu) << 8));
+      *reinterpret_cast<uint16_t*>(&S.xq[tq][AEQ_L + 14 - iq]) = pr;
+      *reinterpret_cast<uint16_t*>(&S.xq[tq][AEQ_L + 14 - iq + 32]) = pr;
+    }
   }
 
+  // DP4A direct form: int8 inputs and an int8-range history (a history set through
+  // the API or left by a wide-input call takes the 32-bit multiply path)
+  const bool use_dp4a = FWD == FNTGPU_AEQ_FWD_DIRECT && NARROW && AEQ_DP4A &&
+                        __all_sync(0xffffffffu, state.hist[tq][iq] >= -128 && state.hist[tq][iq] <= 127 &&
+                                                    state.hist[tq][iq + 1] >= -128 && state.hist[tq][iq + 1] <= 127);
   // this lane's input row (stream tq) and a one-block-ahead prefetch of its 2 samples
   const char* row;
   uint32_t sel0 = 0, sel1 = 1;
@@ -570,6 +640,11 @@ __global__ void __launch_bounds__(AEQ_WARPS * 32, AEQ_MIN_CTAS) k_aeq_process(fn
       }
       S.xi[tq][cur][iq] = v0;
       S.xi[tq][cur][iq + 1] = v1;
+      if (FWD == FNTGPU_AEQ_FWD_DIRECT && NARROW && AEQ_DP4A) {
+        const uint16_t pr = (uint16_t)(((uint32_t)v1 & 0xffu) | (((uint32_t)v0 & 0xffu) << 8));
+        *reinterpret_cast<uint16_t*>(&S.xq[tq][AEQ_L * cur + 14 - iq]) = pr;
+        *reinterpret_cast<uint16_t*>(&S.xq[tq][AEQ_L * cur + 14 - iq + 32]) = pr;
+      }
       if (QUICK || io.adapt) {
         const double f0 = xf_of<NARROW>(v0, lut, A.prm.sig_scale), f1 = xf_of<NARROW>(v1, lut, A.prm.sig_scale);
         double* xr = &S.xf[tq][1 + AEQ_L * cur + iq];
@@ -583,7 +658,7 @@ __global__ void __launch_bounds__(AEQ_WARPS * 32, AEQ_MIN_CTAS) k_aeq_process(fn
 #endif
       __syncwarp();
       int32_t yi0, yi1;
-      lane_forward<FWD>(S, lane, cur, T, m0, yi0, yi1);
+      lane_forward<FWD, NARROW>(S, lane, cur, T, m0, yi0, yi1, use_dp4a);
       const double y0 = div_D<QUICK>(yi0, A);  // y_int / (sig_scale * tap_scale)
       const double y1 = div_D<QUICK>(yi1, A);
       *yrow = make_double2(y0, y1);

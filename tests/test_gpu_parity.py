@@ -401,6 +401,21 @@ def test_aeq_bank_many_streams_vs_oracle():
 
 
 @pytest.mark.parametrize("forward", AEQ_MODES)
+def test_aeq_wide_then_narrow_calls_vs_oracle(forward):
+    """A call with wide inputs leaves an out-of-int8 history; the next call with
+    int8 inputs (DP4A direct form) must fall back for that history exactly."""
+    rng = np.random.default_rng(46)
+    eq = _aeq(mu=1e-4, forward=forward)
+    oq = O.Aeq(SIG_SCALE, mu=1e-4)
+    for x in (rng.integers(-3000, 3001, (4, 16 * 40)), rng.integers(-15, 16, (4, 16 * 40)),
+              rng.integers(-15, 16, (4, 16 * 40))):
+        y = eq.process(x.astype(np.int64), adapt=True)
+        oy = oq.process(x.astype(np.int64))
+        assert np.array_equal(y, oy)
+    assert np.array_equal(eq.w, oq.w) and np.array_equal(eq.history, oq.history)
+
+
+@pytest.mark.parametrize("forward", AEQ_MODES)
 def test_aeq_bank_wide_int32_inputs_vs_oracle(forward):
     """int32 planar inputs up to |x| = 2^15 (group convolutions wrap mod F4 and are
     decoded one by one, as in the reference) through the multi-stream kernel's fast

@@ -10,12 +10,14 @@
 //   sign +: a+ = x_r + 2^8 x_i  ->  FNT-64  ->  * b+'  ->  IFNT-64 (outputs 32..63)
 //   sign -: a- = x_r - 2^8 x_i  ->  FNT-64  ->  * b-'  ->  IFNT-64 (outputs 32..63)
 // (b+- pre-scaled by c_re * N^-1 = 2^25; radix-sqrt2 DIT with rotate-only twiddles
-// in Z/(2^32-1), fermat.cuh). The epilogue combines z_re = u+ + u-,
-// z_im = 2^24 (u+ - u-), reduces mod F4 (multiply-high) and decodes, then streams the contiguous
-// output range of the CTA (and the fused requantization / decimation
-// statistics) with coalesced stores. One HBM read per input sample (the 32-sample
-// halo between neighbouring blocks is re-read from shared memory) and one HBM
-// write per output.
+// in Z/(2^32-1), fermat.cuh; on int8 planes the first two stages run carry-free in
+// plain int32). The epilogue combines z_re = u+ + u-, z_im = 2^24 (u+ - u-), reduces
+// mod F4 (multiply-high) and decodes, then streams the contiguous output range of
+// the CTA (and the fused requantization / decimation statistics) with coalesced
+// stores. The CTA's input window arrives by two TMA bulk copies (interior windows
+// of int8 planes) or 16-byte vector loads; one HBM read per input sample (the
+// 32-sample halo between neighbouring blocks is re-read from shared memory) and
+// one HBM write per output.
 #include <type_traits>
 
 #include "fermat.cuh"

@@ -44,13 +44,14 @@ namespace fntgpu {
 constexpr int AEQ_L = 16;            // taps per filter = hop (aeq.py:45)
 constexpr int AEQ_N = 32;            // block length
 #ifndef AEQ_WARPS
-#define AEQ_WARPS 4                  // streams (warps) per CTA
-#endif
+#define AEQ_WARPS 1                  // streams (warps) per CTA: one-warp CTAs schedule best
+#endif                               // (FNT 124.4 -> 121.7 ms, direct 83.6 -> 75.0 ms vs 4)
 #ifndef AEQ_LOCKSTEP
-#define AEQ_LOCKSTEP 1               // the CTA's 4 warps (one per SM sub-partition) meet every
-                                     // AEQ_LOCKSTEP blocks (power of two; 0 = never) 
-#endif                               // block: they then walk the ~29 KB loop body together and share
-                                     // its instruction-cache lines (161 -> 156 ms at config 5)
+// With several warps per CTA, they meet every AEQ_LOCKSTEP blocks (power of two; 0 =
+// never) so they walk the ~29 KB loop body together and share its instruction-cache
+// lines (4-warp CTAs: 161 -> 156 ms at config 5). One-warp CTAs do not need it.
+#define AEQ_LOCKSTEP (AEQ_WARPS > 1 ? 1 : 0)
+#endif
 constexpr int AEQ_TAP_MAX = 16383;   // TAP_MAG_MAX (aeq.py:26)
 constexpr int XF_LUT = 127;          // x / sig_scale table for |x| <= 127
 #ifndef AEQ_IFNT_CM
@@ -66,7 +67,7 @@ constexpr int XF_LUT = 127;          // x / sig_scale table for |x| <= 127
 #define AEQ_PROBE 0                  // timing probes only: 1-4 drop one phase (wrong results)
 #endif
 #ifndef AEQ_MIN_CTAS
-#define AEQ_MIN_CTAS 4               // resident CTAs per SM the register budget targets
+#define AEQ_MIN_CTAS (16 / AEQ_WARPS) // 16 resident warps per SM: 128 registers per thread
 #endif
 
 struct __align__(16) AeqScratch {

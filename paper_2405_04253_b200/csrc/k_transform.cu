@@ -4,7 +4,8 @@
 // cyclic_convolve_complex) and fermat.py:124-133 (encode/decode arrays).
 //
 // Fast path (aeq32: alpha = 2, N = 32; cdc64: alpha = sqrt2 = 4080, N = 64):
-//   one thread owns one length-N vector in registers; the DIT network is fully
+//   a CTA stages a tile of 64 vectors through shared memory with coalesced int64
+//   loads/stores; one thread owns one length-N vector in registers; the DIT network is fully
 //   unrolled with compile-time twiddles that are rotates in Z/(2^32-1) (fermat.cuh),
 //   so no general multiplication appears inside a transform (the reference's
 //   "shift-add" claim, fnt.py:1-8) and the only general products are the
@@ -19,29 +20,79 @@ namespace fntgpu {
 // ---------------------------------------------------------------------------
 // fast path
 
+// Coalesced staging of a CTA's tile of T consecutive length-N int64 vectors: the
+// CTA reads the tile's contiguous int64 words (T threads, stride T), encodes them
+// into Z/M words and parks them in a padded [T][N + 1] shared array; each thread
+// then takes its own row (conflict-free), and results go back the same way.
+constexpr int TILE = 64;  // vectors (= threads) per CTA of the fast kernels
+
 template <int N>
-__device__ __forceinline__ void store_vec(int64_t* __restrict__ y, const uint32_t (&a)[N], int flags) {
+__device__ __forceinline__ void stage_tile_in(uint32_t (*s)[N + 1], const int64_t* __restrict__ x,
+                                              int64_t b0, int64_t batch) {
+  const int64_t* src = x + b0 * N;
+  if (batch - b0 >= TILE) {
+    // full tile: batches of 16 independent loads per thread in flight
+    constexpr int PER = N, B = 16;
 #pragma unroll
-  for (int i = 0; i < N; ++i) {
-    y[i] = (flags & FNTGPU_DECODE_SIGNED) ? (int64_t)f4_signed(a[i]) : (int64_t)f4_canon(a[i]);
+    for (int j0 = 0; j0 < PER; j0 += B) {
+      int64_t v[B];
+#pragma unroll
+      for (int j = 0; j < B; ++j) v[j] = __ldg(src + (j0 + j) * TILE + threadIdx.x);
+#pragma unroll
+      for (int j = 0; j < B; ++j) {
+        const int e = (j0 + j) * TILE + threadIdx.x;
+        s[e / N][e % N] = f4_enc64(v[j]);
+      }
+    }
+    return;
+  }
+  const int64_t words = (batch - b0) * N;
+  for (int64_t e = threadIdx.x; e < words; e += TILE) s[e / N][e % N] = f4_enc64(src[e]);
+}
+
+template <int N>
+__device__ __forceinline__ void stage_tile_out(const uint32_t (*s)[N + 1], int64_t* __restrict__ y,
+                                               int64_t b0, int64_t batch, int flags) {
+  const int64_t rows = batch - b0 < TILE ? batch - b0 : TILE;
+  const int64_t words = rows * N;
+  int64_t* dst = y + b0 * N;
+  for (int64_t e = threadIdx.x; e < words; e += TILE) {
+    const uint32_t v = s[e / N][e % N];
+    dst[e] = (flags & FNTGPU_DECODE_SIGNED) ? (int64_t)f4_signed(v) : (int64_t)f4_canon(v);
   }
 }
 
 template <int N>
-__device__ __forceinline__ void load_bitrev(uint32_t (&a)[N], const int64_t* __restrict__ x) {
+__device__ __forceinline__ void row_bitrev(uint32_t (&a)[N], const uint32_t* row) {
   constexpr int LG = ilog2(N);
 #pragma unroll
-  for (int i = 0; i < N; ++i) a[bitrev(i, LG)] = f4_enc64(x[i]);
+  for (int i = 0; i < N; ++i) a[bitrev(i, LG)] = row[i];
+}
+
+// One transform of a shared-memory row in place (read in bit-reversed order,
+// written in natural order; the inverse also applies the rotation `rot`). Kept
+// out of line: the complex convolution runs it 6 times per vector and fully
+// unrolled copies of the 64-point network overflow the instruction cache (2.6x
+// slower inline; the real convolution's 3 inline copies are 5% faster than calls).
+template <int N, int KIND, bool INV>
+__device__ __noinline__ void fnt_row(uint32_t* row, int rot) {
+  uint32_t a[N];
+  row_bitrev<N>(a, row);
+  fnt_dit<N, KIND, INV>(a);
+#pragma unroll
+  for (int i = 0; i < N; ++i) row[i] = INV ? m_rot(a[i], rot) : a[i];
 }
 
 template <int N, int KIND>
-__global__ void __launch_bounds__(128) k_fnt_fast(const int64_t* x, int64_t* y, int64_t batch,
-                                                  int inverse, int flags) {
+__global__ void __launch_bounds__(TILE) k_fnt_fast(const int64_t* x, int64_t* y, int64_t batch,
+                                                   int inverse, int flags) {
   constexpr int LG = ilog2(N);
-  const int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (b >= batch) return;
+  __shared__ uint32_t sA[TILE][N + 1];
+  const int64_t b0 = (int64_t)blockIdx.x * TILE;
+  stage_tile_in<N>(sA, x, b0, batch);
+  __syncthreads();
   uint32_t a[N];
-  load_bitrev<N>(a, x + b * N);
+  row_bitrev<N>(a, sA[threadIdx.x]);
   if (inverse) {
     fnt_dit<N, KIND, true>(a);
 #pragma unroll
@@ -49,88 +100,130 @@ __global__ void __launch_bounds__(128) k_fnt_fast(const int64_t* x, int64_t* y, 
   } else {
     fnt_dit<N, KIND, false>(a);
   }
-  store_vec<N>(y + b * N, a, flags);
+#pragma unroll
+  for (int i = 0; i < N; ++i) sA[threadIdx.x][i] = a[i];  // own row only: no barrier needed before
+  __syncthreads();
+  stage_tile_out<N>(sA, y, b0, batch, flags);
 }
 
 template <int N, int KIND>
-__global__ void __launch_bounds__(128) k_conv_real_fast(const int64_t* x, const int64_t* h,
-                                                        int64_t h_stride, int64_t* z,
-                                                        int64_t batch, int flags) {
+__global__ void __launch_bounds__(TILE) k_conv_real_fast(const int64_t* x, const int64_t* h,
+                                                         int64_t h_stride, int64_t* z,
+                                                         int64_t batch, int flags) {
   constexpr int LG = ilog2(N);
-  const int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (b >= batch) return;
-  uint32_t X[N], H[N];
-  load_bitrev<N>(X, x + b * N);
-  load_bitrev<N>(H, h + b * h_stride);
-  fnt_dit<N, KIND, false>(X);
-  fnt_dit<N, KIND, false>(H);
+  __shared__ uint32_t sX[TILE][N + 1];
+  __shared__ uint32_t sH[TILE][N + 1];
+  const int64_t b0 = (int64_t)blockIdx.x * TILE;
+  stage_tile_in<N>(sX, x, b0, batch);
+  if (h_stride != 0) {
+    stage_tile_in<N>(sH, h, b0, batch);
+  } else {
+    for (int i = threadIdx.x; i < N; i += TILE) sH[0][i] = f4_enc64(h[i]);  // shared taps
+  }
+  __syncthreads();
+  // Tap spectra first, parked back in shared memory (each thread its own row, or
+  // thread 0 the CTA's one shared row), so only one spectrum is register-resident.
+  const int hr = h_stride != 0 ? threadIdx.x : 0;
+  if (h_stride != 0 || threadIdx.x == 0) {
+    uint32_t H[N];
+    row_bitrev<N>(H, sH[hr]);
+    fnt_dit<N, KIND, false>(H);
 #pragma unroll
-  for (int i = 0; i < N; ++i) X[i] = m_mul(X[i], H[i]);  // the N general products (fnt.py:123)
+    for (int i = 0; i < N; ++i) sH[hr][i] = H[i];
+  }
+  if (h_stride == 0) __syncthreads();  // uniform over the CTA
+  uint32_t X[N];
+  row_bitrev<N>(X, sX[threadIdx.x]);
+  fnt_dit<N, KIND, false>(X);
+#pragma unroll
+  for (int i = 0; i < N; ++i) X[i] = m_mul(X[i], sH[hr][i]);  // the N general products (fnt.py:123)
   to_bitrev<N>(X);
   fnt_dit<N, KIND, true>(X);
 #pragma unroll
-  for (int i = 0; i < N; ++i) X[i] = m_rot(X[i], 32 - LG);
-  store_vec<N>(z + b * N, X, flags);
+  for (int i = 0; i < N; ++i) sX[threadIdx.x][i] = m_rot(X[i], 32 - LG);
+  __syncthreads();
+  stage_tile_out<N>(sX, z, b0, batch, flags);
 }
 
-// Eqs. (7)-(8): a+- = X_r +- 2^8 X_i, b+- likewise (linearity lets us form them in
-// the time domain), u+- = a+- * b+-, z_re = 2^-1 IFNT(u+ + u-), z_im = 2^-9 IFNT(u+ - u-).
+// Staging of a complex tile in the combined form of Eqs. (7)-(8): P = re + 2^8 im,
+// M = re - 2^8 im (linearity lets the combination happen in the time domain).
+template <int N>
+__device__ __forceinline__ void stage_pair_in(uint32_t (*sP)[N + 1], uint32_t (*sM)[N + 1],
+                                              const int64_t* __restrict__ re,
+                                              const int64_t* __restrict__ im, int64_t rows) {
+  if (rows >= TILE) {
+    constexpr int B = 8;
+#pragma unroll
+    for (int j0 = 0; j0 < N; j0 += B) {
+      int64_t vr[B], vi[B];
+#pragma unroll
+      for (int j = 0; j < B; ++j) {
+        vr[j] = __ldg(re + (j0 + j) * TILE + threadIdx.x);
+        vi[j] = __ldg(im + (j0 + j) * TILE + threadIdx.x);
+      }
+#pragma unroll
+      for (int j = 0; j < B; ++j) {
+        const int e = (j0 + j) * TILE + threadIdx.x;
+        const uint32_t r = f4_enc64(vr[j]), i8 = m_rot(f4_enc64(vi[j]), 8);
+        sP[e / N][e % N] = m_add(r, i8);
+        sM[e / N][e % N] = m_sub(r, i8);
+      }
+    }
+    return;
+  }
+  const int64_t words = rows * N;
+  for (int64_t e = threadIdx.x; e < words; e += TILE) {
+    const uint32_t r = f4_enc64(re[e]), i8 = m_rot(f4_enc64(im[e]), 8);
+    sP[e / N][e % N] = m_add(r, i8);
+    sM[e / N][e % N] = m_sub(r, i8);
+  }
+}
+
+// Eqs. (7)-(8): a+- = X_r +- 2^8 X_i, b+- likewise, u+- = a+- * b+-,
+// z_re = 2^-1 IFNT(u+ + u-), z_im = 2^-9 IFNT(u+ - u-). Tiles are staged
+// coalesced; each thread keeps one N-word array in registers and parks the
+// others in its own shared-memory rows (the tap spectra b+- in the CTA's one
+// shared row when the taps are common to the batch).
 template <int N, int KIND>
-__global__ void __launch_bounds__(64) k_conv_complex_fast(const int64_t* xr, const int64_t* xi,
-                                                           const int64_t* yr, const int64_t* yi,
-                                                           int64_t y_stride, int64_t* zr,
-                                                           int64_t* zi, int64_t batch, int flags) {
+__global__ void __launch_bounds__(TILE) k_conv_complex_fast(const int64_t* xr, const int64_t* xi,
+                                                            const int64_t* yr, const int64_t* yi,
+                                                            int64_t y_stride, int64_t* zr,
+                                                            int64_t* zi, int64_t batch, int flags) {
   constexpr int LG = ilog2(N);
-  const int64_t b0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const bool live = b0 < batch;
-  const int64_t b = live ? b0 : batch - 1;  // idle lanes recompute the last vector, store nothing
-  // u+ is parked in shared memory (padded rows) while u- is formed: three live
-  // N-word arrays would not fit the register file for N = 64.
-  __shared__ uint32_t sU[64][N + 1];
-  uint32_t* U = sU[threadIdx.x];
-  uint32_t A[N], B[N];
-  // u+ = FNT(x_r + j x_i) * FNT(y_r + j y_i)
-#pragma unroll
-  for (int i = 0; i < N; ++i) {
-    const int p = bitrev(i, LG);
-    A[p] = m_add(f4_enc64(xr[b * N + i]), m_rot(f4_enc64(xi[b * N + i]), 8));
-    B[p] = m_add(f4_enc64(yr[b * y_stride + i]), m_rot(f4_enc64(yi[b * y_stride + i]), 8));
+  extern __shared__ uint32_t smem_c[];
+  typedef uint32_t Row[N + 1];
+  Row* sAp = reinterpret_cast<Row*>(smem_c);
+  Row* sAm = sAp + TILE;
+  Row* sBp = sAm + TILE;
+  Row* sBm = sBp + (y_stride != 0 ? TILE : 1);
+  const int64_t b0 = (int64_t)blockIdx.x * TILE;
+  const int64_t rows = batch - b0 < TILE ? batch - b0 : TILE;
+  const int t = threadIdx.x;
+  stage_pair_in<N>(sAp, sAm, xr + b0 * N, xi + b0 * N, rows);
+  if (y_stride != 0) stage_pair_in<N>(sBp, sBm, yr + b0 * N, yi + b0 * N, rows);
+  else stage_pair_in<N>(sBp, sBm, yr, yi, 1);
+  __syncthreads();
+  const int hr = y_stride != 0 ? t : 0;
+  if (y_stride != 0 || t == 0) {  // b+- spectra, in place
+    fnt_row<N, KIND, false>(sBp[hr], 0);
+    fnt_row<N, KIND, false>(sBm[hr], 0);
   }
-  fnt_dit<N, KIND, false>(A);
-  fnt_dit<N, KIND, false>(B);
+  if (y_stride == 0) __syncthreads();  // uniform over the CTA
+  uint32_t *ap = sAp[t], *am = sAm[t];
+  fnt_row<N, KIND, false>(ap, 0);
+  fnt_row<N, KIND, false>(am, 0);
 #pragma unroll
-  for (int i = 0; i < N; ++i) U[i] = m_mul(A[i], B[i]);
-  __syncwarp();  // scheduling fence: keeps the u- loads from being hoisted above (register pressure)
-  // u- = FNT(x_r - j x_i) * FNT(y_r - j y_i)
-#pragma unroll
-  for (int i = 0; i < N; ++i) {
-    const int p = bitrev(i, LG);
-    A[p] = m_sub(f4_enc64(xr[b * N + i]), m_rot(f4_enc64(xi[b * N + i]), 8));
-    B[p] = m_sub(f4_enc64(yr[b * y_stride + i]), m_rot(f4_enc64(yi[b * y_stride + i]), 8));
+  for (int i = 0; i < N; ++i) {  // u+- = a+- * b+-; s = u+ + u- -> am, d = u+ - u- -> ap
+    const uint32_t up = m_mul(ap[i], sBp[hr][i]), um = m_mul(am[i], sBm[hr][i]);
+    am[i] = m_add(up, um);
+    ap[i] = m_sub(up, um);
   }
-  fnt_dit<N, KIND, false>(A);
-  fnt_dit<N, KIND, false>(B);
-#pragma unroll
-  for (int i = 0; i < N; ++i) {
-    const uint32_t um = m_mul(A[i], B[i]);
-    const uint32_t up = U[i];
-    A[i] = m_add(up, um);  // s = u+ + u-
-    B[i] = m_sub(up, um);  // d = u+ - u-
-  }
-  to_bitrev<N>(A);
-  to_bitrev<N>(B);
-  fnt_dit<N, KIND, true>(A);
-  fnt_dit<N, KIND, true>(B);
   // c_re * N^-1 = 2^-1 * 2^-LG ; c_im * N^-1 = 2^-9 * 2^-LG (fnt.py:155-158)
-#pragma unroll
-  for (int i = 0; i < N; ++i) {
-    A[i] = m_rot(A[i], (64 - 1 - LG) & 31);
-    B[i] = m_rot(B[i], (64 - 9 - LG) & 31);
-  }
-  if (live) {
-    store_vec<N>(zr + b * N, A, flags);
-    store_vec<N>(zi + b * N, B, flags);
-  }
+  fnt_row<N, KIND, true>(am, (64 - 1 - LG) & 31);
+  fnt_row<N, KIND, true>(ap, (64 - 9 - LG) & 31);
+  __syncthreads();
+  stage_tile_out<N>(sAm, zr, b0, batch, flags);
+  stage_tile_out<N>(sAp, zi, b0, batch, flags);
 }
 
 // ---------------------------------------------------------------------------
@@ -318,9 +411,9 @@ cudaError_t launch_fnt(const DevPlan& p, int inverse, const int64_t* x, int64_t*
                        int flags, cudaStream_t st) {
   if (batch <= 0) return cudaSuccess;
   if (p.kind == KIND_SQRT2_64) {
-    k_fnt_fast<64, SQRT2><<<(unsigned)((batch + 63) / 64), 64, 0, st>>>(x, y, batch, inverse, flags);
+    k_fnt_fast<64, SQRT2><<<(unsigned)((batch + TILE - 1) / TILE), TILE, 0, st>>>(x, y, batch, inverse, flags);
   } else if (p.kind == KIND_RADIX2_32) {
-    k_fnt_fast<32, RADIX2><<<(unsigned)((batch + 63) / 64), 64, 0, st>>>(x, y, batch, inverse, flags);
+    k_fnt_fast<32, RADIX2><<<(unsigned)((batch + TILE - 1) / TILE), TILE, 0, st>>>(x, y, batch, inverse, flags);
   } else {
     const int per = generic_per(p.n, 1);
     const size_t sm = (size_t)per * p.n * sizeof(uint32_t);
@@ -335,9 +428,9 @@ cudaError_t launch_conv_real(const DevPlan& p, const int64_t* x, const int64_t* 
                              int64_t* z, int64_t batch, int flags, cudaStream_t st) {
   if (batch <= 0) return cudaSuccess;
   if (p.kind == KIND_SQRT2_64) {
-    k_conv_real_fast<64, SQRT2><<<(unsigned)((batch + 63) / 64), 64, 0, st>>>(x, h, h_stride, z, batch, flags);
+    k_conv_real_fast<64, SQRT2><<<(unsigned)((batch + TILE - 1) / TILE), TILE, 0, st>>>(x, h, h_stride, z, batch, flags);
   } else if (p.kind == KIND_RADIX2_32) {
-    k_conv_real_fast<32, RADIX2><<<(unsigned)((batch + 63) / 64), 64, 0, st>>>(x, h, h_stride, z, batch, flags);
+    k_conv_real_fast<32, RADIX2><<<(unsigned)((batch + TILE - 1) / TILE), TILE, 0, st>>>(x, h, h_stride, z, batch, flags);
   } else {
     const int per = generic_per(p.n, 2);
     const size_t sm = 2 * (size_t)per * p.n * sizeof(uint32_t);
@@ -354,10 +447,14 @@ cudaError_t launch_conv_complex(const DevPlan& p, const int64_t* xr, const int64
                                 cudaStream_t st) {
   if (batch <= 0) return cudaSuccess;
   if (p.kind == KIND_SQRT2_64) {
-    k_conv_complex_fast<64, SQRT2><<<(unsigned)((batch + 63) / 64), 64, 0, st>>>(
+    const size_t sm = (2 * TILE + 2 * (y_stride != 0 ? TILE : 1)) * (64 + 1) * sizeof(uint32_t);
+    cudaError_t e = smem_cfg((const void*)k_conv_complex_fast<64, SQRT2>, sm);
+    if (e != cudaSuccess) return e;
+    k_conv_complex_fast<64, SQRT2><<<(unsigned)((batch + TILE - 1) / TILE), TILE, sm, st>>>(
         xr, xi, yr, yi, y_stride, zr, zi, batch, flags);
   } else if (p.kind == KIND_RADIX2_32) {
-    k_conv_complex_fast<32, RADIX2><<<(unsigned)((batch + 63) / 64), 64, 0, st>>>(
+    const size_t sm = (2 * TILE + 2 * (y_stride != 0 ? TILE : 1)) * (32 + 1) * sizeof(uint32_t);
+    k_conv_complex_fast<32, RADIX2><<<(unsigned)((batch + TILE - 1) / TILE), TILE, sm, st>>>(
         xr, xi, yr, yi, y_stride, zr, zi, batch, flags);
   } else {
     const int per = generic_per(p.n, 4);

@@ -104,6 +104,28 @@ def test_convolution_golden(golden, plans, name):
     assert np.array_equal(sr, c[f"{name}_signed_cplx_re"]) and np.array_equal(si, c[f"{name}_signed_cplx_im"])
 
 
+@pytest.mark.parametrize("name", ("aeq32", "cdc64"))
+def test_staged_tiles_ragged_batches_vs_oracle(plans, name):
+    """The shift-add kernels stage 64-vector tiles through shared memory: full
+    tiles, partial last tiles and in-place transforms, per-vector and shared
+    taps, against the oracle (fnt.py:106-161)."""
+    p = plans[name]
+    op = O.Plan.named(name)
+    F = p.params.F
+    rng = np.random.default_rng(17)
+    for batch in (1, 63, 64, 65, 191, 1000):
+        xr, xi, yr, yi = (rng.integers(-(1 << 40), 1 << 40, (batch, p.n)) for _ in range(4))
+        assert np.array_equal(P.fnt(p, xr), O.fnt(op, xr)), batch
+        assert np.array_equal(P.ifnt(p, xr), O.ifnt(op, xr)), batch
+        xr, xi, yr, yi = (a % F for a in (xr, xi, yr, yi))
+        assert np.array_equal(P.cyclic_convolve_real(p, xr, yr), O.cyclic_real(op, xr, yr)), batch
+        assert np.array_equal(P.cyclic_convolve_real(p, xr, yr[0]), O.cyclic_real(op, xr, yr[0])), batch
+        for y_re, y_im in ((yr, yi), (yr[-1], yi[-1])):
+            zr, zi = P.cyclic_convolve_complex(p, xr, xi, y_re, y_im)
+            rr, ri = O.cyclic_complex(op, xr, xi, y_re, y_im)
+            assert np.array_equal(zr, rr) and np.array_equal(zi, ri), batch
+
+
 def test_config1_full(golden, digests, plans):
     """BASELINE config 1: 16384 x 64, seed 0, bit-exact (reference digest)."""
     p = plans["cdc64"]

@@ -66,6 +66,9 @@ constexpr int XF_LUT = 127;          // x / sig_scale table for |x| <= 127
 #ifndef AEQ_PROBE
 #define AEQ_PROBE 0                  // timing probes only: 1-4 drop one phase (wrong results)
 #endif
+#ifndef AEQ_FUSE_T
+#define AEQ_FUSE_T 1                 // FNT forward: sum over t before the inverse when exact
+#endif
 #ifndef AEQ_MIN_CTAS
 #define AEQ_MIN_CTAS (16 / AEQ_WARPS) // 16 resident warps per SM: 128 registers per thread
 #endif
@@ -197,6 +200,26 @@ __device__ __forceinline__ int32_t unpack_group(uint32_t p, int g) {
   return g ? ((int32_t)(p + 0x8000u) >> 16) : ((int32_t)(p << 16) >> 16);
 }
 
+// FNT forward with the transform-domain sum over input streams (AEQ_FUSE_T): taps
+// are kept as balanced base-64 digits instead, w = 64 a + b with b in [-32, 31] and
+// |a| <= 256, packed the same way: p = a + b 2^16 = w 2^16 - a (2^22 - 1), so
+// unpack_group gives a (g = 0) and b (g = 1).
+template <bool BAL>
+__device__ __forceinline__ uint32_t pack_taps(int32_t w) {
+  if (!BAL) return pack_groups(w);
+  return (uint32_t)(w * 65536 - ((w + 32) >> 6) * 4194303);
+}
+template <bool BAL>
+__device__ __forceinline__ int32_t unpack_tap(uint32_t p) {
+  return (BAL ? 64 : 128) * unpack_group(p, 0) + unpack_group(p, 1);
+}
+// the reference's split_taps group g of a packed tap (fixedpoint.py:111-121)
+template <bool BAL>
+__device__ __forceinline__ int32_t ref_group(uint32_t p, int g) {
+  if (!BAL) return unpack_group(p, g);
+  return tap_group(unpack_tap<true>(p), g);
+}
+
 // einsum("sm,tmk->stk") inner reduction over m in numpy's SSE2 order.
 __device__ __forceinline__ double einsum_m(const double (&P)[AEQ_L]) {
   double c0 = P[6], c1 = P[7];
@@ -221,13 +244,21 @@ __device__ __forceinline__ double xf_of(int32_t x, const double* lut, double sig
 // This lane's 8 taps k = 8g .. 8g+7 of filter (s, t): the 14-bit values in
 // registers, the float values in the warp's shared scratch (S.wf, lane-contiguous).
 struct LaneTaps {
-  uint32_t gp[8];  // packed 7-bit groups of w_int (pack_groups); w_int = 128 hi + lo
+  uint32_t gp[8];  // packed taps: 7-bit groups of w_int (pack_groups), or balanced
+                   // base-64 digits (pack_taps<true>)
   uint32_t sat;    // saturations counted by this lane (flushed to 64 bits every 2^24 blocks)
+  uint32_t asum;   // balanced digits: sum of |a| over this lane's 8 taps
 };
+
+template <bool BAL>
+__device__ __forceinline__ void set_tap(LaneTaps& T, int kk, int32_t w) {
+  T.gp[kk] = pack_taps<BAL>(w);
+  if (BAL) T.asum += (uint32_t)abs((w + 32) >> 6);
+}
 
 // Exchange the e values, compute the err_trace mean (lane 0 writes *err_out when
 // non-null) and, when mu != 0, the float update of this lane's 8 taps.
-template <bool QUICK = false>
+template <bool QUICK = false, bool BAL = false>
 __device__ __forceinline__ void lane_update(const AeqArgs& A, AeqScratch& S, int lane, int m0,
                                             double y0, double y1, int cur, double mu,
                                             LaneTaps& T, double* err_out) {
@@ -289,12 +320,13 @@ __device__ __forceinline__ void lane_update(const AeqArgs& A, AeqScratch& S, int
         c1[kk] = i == 0 ? po : dadd(po, c1[kk]);
       }
     }
+    T.asum = 0;
 #pragma unroll
     for (int kk = 0; kk < 8; ++kk) {
       const double gr = dadd(c0[kk], c1[kk]);
       const double w = dadd(S.wf[kk][lane], dmul(mu, gr));
       S.wf[kk][lane] = w;
-      T.gp[kk] = pack_groups(requantize_tap(w, A.prm.tap_scale, T.sat));
+      set_tap<BAL>(T, kk, requantize_tap(w, A.prm.tap_scale, T.sat));
     }
   }
   __syncwarp();
@@ -379,37 +411,135 @@ __device__ __forceinline__ void direct_dp4a(const AeqScratch& S, int t, int g, i
   }
 }
 
+// Exact test for summing the four input streams in the transform domain (balanced
+// digits, AEQ_FUSE_T). With A_t = max |x_t| over the block window:
+//  (1) A_t <= 16 for every t: each of the reference's per-(s,t,g) group
+//      convolutions is then within [-32768, 32768] (|group| <= 127, 16 taps), so
+//      its decoded sum (aeq.py:139-143) is the exact integer FIR sum_t,k w x;
+//  (2) per output stream s, sum_t A_t sum_k |a_stk| <= 32768, and (from (1) and
+//      |b| <= 32) sum_t A_t sum_k |b_stk| <= 32768: the digit convolutions summed
+//      over t are in range, so their decoded residues are exact too.
+// Then 64 dec(sum_t conv a) + dec(sum_t conv b) is the same exact FIR. Warp-uniform.
+__device__ __forceinline__ bool fused_ok(const LaneTaps& T, uint32_t amax_t) {
+  uint32_t h = T.asum * amax_t;  // <= 8 * 256 * 16 when amax_t <= 16
+  h += __shfl_xor_sync(0xffffffffu, h, 1);
+  h += __shfl_xor_sync(0xffffffffu, h, 2);
+  h += __shfl_xor_sync(0xffffffffu, h, 4);
+  return __all_sync(0xffffffffu, amax_t <= 16u && h <= 32768u);
+}
+
+// Forward outputs of one block with the products P_t = X_t W_stg of this lane
+// (s, t, g) summed over groups of F input streams before the inverse: ONE inverse
+// per (s, g, group), split over the group's F lanes by k = k1 + F k2 (k1 = t mod F):
+//   y[n] = sum_k1 2^(-n k1) Q_k1[n mod 32/F],  Q_k1[j] = sum_k2 P[k1 + F k2] 2^(-F j k2)
+// Products go through S.part as [32][32] words, row = lane, logical column
+// k1 * (32/F) + k2, rotated by 4 f(lane & 7) words (conflict-free both ways).
+template <int F, int BASE>
+__device__ __forceinline__ void fused_inverse(AeqScratch& S, int lane, const uint32_t (&X)[AEQ_N],
+                                              int m0, int32_t& yi0, int32_t& yi1) {
+  constexpr int NB = AEQ_N / F;  // bins per lane = inverse length
+  const int s = lane >> 3, t = (lane >> 1) & 3, g = lane & 1;
+  const int k1 = t & (F - 1), t0 = t & ~(F - 1);
+  auto swz = [](int r) { const int x = r & 7; return 4 * (x ^ ((x & 4) >> 1)); };
+  uint32_t* prod = reinterpret_cast<uint32_t*>(S.part);
+  const int rot = swz(lane);
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    const int c1 = (4 * q) / NB, c2 = (4 * q) % NB;  // logical column 4q = c1 * NB + c2
+    const uint4 v = make_uint4(X[c1 + F * c2], X[c1 + F * (c2 + 1)], X[c1 + F * (c2 + 2)],
+                               X[c1 + F * (c2 + 3)]);
+    reinterpret_cast<uint4*>(prod + 32 * lane)[((4 * q + rot) & 31) >> 2] = v;
+  }
+  __syncwarp();
+  uint32_t Q[NB];
+#pragma unroll
+  for (int i = 0; i < F; ++i) {
+    const int r = 8 * s + 2 * (t0 + i) + g;
+    const int rr = swz(r);
+#pragma unroll
+    for (int h = 0; h < NB / 4; ++h) {
+      const uint4 v = reinterpret_cast<const uint4*>(prod + 32 * r)[((NB * k1 + 4 * h + rr) & 31) >> 2];
+      if (i == 0) {
+        Q[4 * h] = v.x; Q[4 * h + 1] = v.y; Q[4 * h + 2] = v.z; Q[4 * h + 3] = v.w;
+      } else {
+        Q[4 * h] = m_add(Q[4 * h], v.x); Q[4 * h + 1] = m_add(Q[4 * h + 1], v.y);
+        Q[4 * h + 2] = m_add(Q[4 * h + 2], v.z); Q[4 * h + 3] = m_add(Q[4 * h + 3], v.w);
+      }
+    }
+  }
+  // +32768 on the group's DC bin (lane k1 = 0, k2 = 0): +32768 on every output
+  Q[0] = m_add(Q[0], k1 == 0 ? 32768u : 0u);
+  to_bitrev<NB>(Q);
+  fnt_dit<NB, F == 4 ? RADIX16 : RADIX4, true, false, false, AEQ_IFNT_CM>(Q);
+  __syncwarp();  // every lane has read its products before S.part is reused
+#pragma unroll
+  for (int m = 0; m < AEQ_L; ++m) {
+    const uint32_t q = Q[m % NB];
+    S.part[lane][m] = (int32_t)__funnelshift_l(q, q, ((16 - m) * k1) & 31);  // 2^(-(16+m) k1)
+  }
+  __syncwarp();
+  // y_int = sum over groups of BASE dec(digit 0) + dec(digit 1), each summed over F lanes
+  int32_t a0 = -(4 / F) * (BASE + 1) * 32768, a1 = a0;
+#pragma unroll
+  for (int grp = 0; grp < 4 / F; ++grp) {
+    uint32_t h0 = 0, h1 = 0, l0 = 0, l1 = 0;
+#pragma unroll
+    for (int i = 0; i < F; ++i) {
+      const int r = 8 * s + 2 * (F * grp + i);
+      h0 = m_add(h0, (uint32_t)S.part[r][m0]);
+      h1 = m_add(h1, (uint32_t)S.part[r][m0 + 1]);
+      l0 = m_add(l0, (uint32_t)S.part[r + 1][m0]);
+      l1 = m_add(l1, (uint32_t)S.part[r + 1][m0 + 1]);
+    }
+    a0 += BASE * (int32_t)f4_mod(h0) + (int32_t)f4_mod(l0);
+    a1 += BASE * (int32_t)f4_mod(h1) + (int32_t)f4_mod(l1);
+  }
+  yi0 = a0;
+  yi1 = a1;
+  __syncwarp();
+}
+
 template <int FWD, bool NARROW = false>
 __device__ __forceinline__ void lane_forward(AeqScratch& S, int lane, int cur, const LaneTaps& T,
                                              int m0, int32_t& yi0, int32_t& yi1,
-                                             bool use_dp4a = false) {
+                                             bool use_dp4a = false, uint32_t amax_t = 65535u) {
   const int s = lane >> 3, t = (lane >> 1) & 3, g = lane & 1;
   if (FWD == FNTGPU_AEQ_FWD_FNT) {
+    constexpr bool BAL = AEQ_FUSE_T != 0;
 #if AEQ_PROBE != 1
     warp_input_fnt(S, lane, cur);
 #endif
-    // all 16 taps of filter (s, t), group g (split_taps, fixedpoint.py:111-121):
-    // own 8 + partner's 8 (lane ^ 1 holds the other half)
+    const bool fused = BAL && fused_ok(T, amax_t);
+    // all 16 taps of filter (s, t), own 8 + partner's 8 (lane ^ 1 holds the other
+    // half): digit g (fused) or the reference's group g (split_taps,
+    // fixedpoint.py:111-121)
     uint32_t W[AEQ_N];
+    if (fused) {
 #pragma unroll
-    for (int kk = 0; kk < 8; ++kk) {
-      const uint32_t other = __shfl_xor_sync(0xffffffffu, T.gp[kk], 1);
-      const uint32_t lo8 = g == 0 ? T.gp[kk] : other;   // tap kk
-      const uint32_t hi8 = g == 0 ? other : T.gp[kk];   // tap 8 + kk
-      W[bitrev(kk, 5)] = (uint32_t)unpack_group(lo8, g);
-      W[bitrev(8 + kk, 5)] = (uint32_t)unpack_group(hi8, g);
+      for (int kk = 0; kk < 8; ++kk) {
+        const uint32_t other = __shfl_xor_sync(0xffffffffu, T.gp[kk], 1);
+        W[bitrev(kk, 5)] = (uint32_t)unpack_group(g == 0 ? T.gp[kk] : other, g);      // tap kk
+        W[bitrev(8 + kk, 5)] = (uint32_t)unpack_group(g == 0 ? other : T.gp[kk], g);  // tap 8 + kk
+      }
+    } else {
+#pragma unroll
+      for (int kk = 0; kk < 8; ++kk) {
+        const uint32_t other = __shfl_xor_sync(0xffffffffu, T.gp[kk], 1);
+        W[bitrev(kk, 5)] = (uint32_t)ref_group<BAL>(g == 0 ? T.gp[kk] : other, g);
+        W[bitrev(8 + kk, 5)] = (uint32_t)ref_group<BAL>(g == 0 ? other : T.gp[kk], g);
+      }
     }
 #pragma unroll
     for (int k = AEQ_L; k < AEQ_N; ++k) W[bitrev(k, 5)] = 0u;
-    // taps zero-padded: stage 0 is a copy; |group| <= 127 keeps stages 1-2 (twiddles
-    // 2^0..2^12) below 2^28 in plain int32, then a multiple of F4 makes the words
+    // taps zero-padded: stage 0 is a copy; |group| <= 256 keeps stages 1-2 (twiddles
+    // 2^0..2^12) below 2^29 in plain int32, then a multiple of F4 makes the words
     // non-negative residues of Z/M for stages 3-4
     fnt_stage<AEQ_N, RADIX2, false, true, false, 0, 1>(W);
 #if AEQ_PROBE != 2
     fnt_stage_plain<AEQ_N, RADIX2, 1, 3>(W);
 #endif
 #pragma unroll
-    for (int k = 0; k < AEQ_N; ++k) W[k] += F4 * 8192u;  // 536 879 104 > 2^28
+    for (int k = 0; k < AEQ_N; ++k) W[k] += F4 * 8192u;  // 536 879 104 > 256 * 257 * 4097
 #if AEQ_PROBE != 2
     fnt_stage<AEQ_N, RADIX2, false, false, false, 3, -1, AEQ_TAP_CM>(W);
 #endif
@@ -421,6 +551,9 @@ __device__ __forceinline__ void lane_forward(AeqScratch& S, int lane, int cur, c
     }
 #pragma unroll
     for (int k = 0; k < AEQ_N; ++k) X[k] = m_mul(X[k], W[k]);  // 32 general products
+#if AEQ_FUSE_T
+    if (fused) { fused_inverse<4, 64>(S, lane, X, m0, yi0, yi1); return; }
+#endif
     // +32768 on every output of the inverse = +32768 on its DC bin (X carries N^-1),
     // so each output decodes as f4_mod(.) - 32768 (fermat.cuh: f4_mod)
     X[0] = m_add(X[0], 32768u);
@@ -541,11 +674,13 @@ __global__ void __launch_bounds__(AEQ_WARPS * 32, AEQ_MIN_CTAS) k_aeq_process(fn
   // input-loader role: samples iq, iq + 1 of input stream tq
   const int tq = lane >> 3, iq = 2 * (lane & 7);
 
+  constexpr bool BAL = FWD == FNTGPU_AEQ_FWD_FNT && AEQ_FUSE_T;
   LaneTaps T;
+  T.asum = 0;
 #pragma unroll
   for (int kk = 0; kk < 8; ++kk) {
     S.wf[kk][lane] = state.w[s][t][8 * g + kk];
-    T.gp[kk] = pack_groups(state.w_int[s][t][8 * g + kk]);
+    set_tap<BAL>(T, kk, state.w_int[s][t][8 * g + kk]);
   }
   T.sat = 0;
   // history -> ring slot 1 (the slot block 0 treats as "previous")
@@ -613,6 +748,11 @@ __global__ void __launch_bounds__(AEQ_WARPS * 32, AEQ_MIN_CTAS) k_aeq_process(fn
 
   long long sat64 = 0;
   int32_t v0 = 0, v1 = 0;
+  // max |x| of this lane's two samples in the previous block (window = prev + cur)
+  auto mag = [](int32_t v) -> uint32_t {
+    return min(v < 0 ? 0u - (uint32_t)v : (uint32_t)v, 65535u);
+  };
+  uint32_t amax_prev = max(mag(state.hist[tq][iq]), mag(state.hist[tq][iq + 1]));
   const int64_t nb = io.n_blocks;
   uint2 raw = make_uint2(0u, 0u);
   if (nb > 0) raw = fetch(row);
@@ -657,16 +797,26 @@ __global__ void __launch_bounds__(AEQ_WARPS * 32, AEQ_MIN_CTAS) k_aeq_process(fn
 #if AEQ_LOCKSTEP
       if ((b & (AEQ_LOCKSTEP - 1)) == 0) asm volatile("bar.sync 1, %0;" :: "r"(bar_threads) : "memory");
 #endif
+      uint32_t amax_t = 65535u;  // max |x| over the block window of input stream t
+      if (FWD == FNTGPU_AEQ_FWD_FNT && AEQ_FUSE_T) {
+        const uint32_t a_cur = max(mag(v0), mag(v1));
+        uint32_t a = max(a_cur, amax_prev);  // stream tq, this lane's two positions
+        amax_prev = a_cur;
+        a = max(a, __shfl_xor_sync(0xffffffffu, a, 1));
+        a = max(a, __shfl_xor_sync(0xffffffffu, a, 2));
+        a = max(a, __shfl_xor_sync(0xffffffffu, a, 4));
+        amax_t = __shfl_sync(0xffffffffu, a, 8 * t);
+      }
       __syncwarp();
       int32_t yi0, yi1;
-      lane_forward<FWD, NARROW>(S, lane, cur, T, m0, yi0, yi1, use_dp4a);
+      lane_forward<FWD, NARROW>(S, lane, cur, T, m0, yi0, yi1, use_dp4a, amax_t);
       const double y0 = div_D<QUICK>(yi0, A);  // y_int / (sig_scale * tap_scale)
       const double y1 = div_D<QUICK>(yi1, A);
       *yrow = make_double2(y0, y1);
       yrow += AEQ_L / 2;
       if (QUICK || io.adapt) {
 #if AEQ_PROBE != 4
-        lane_update<QUICK>(A, S, lane, m0, y0, y1, cur, mu, T, err_out);
+        lane_update<QUICK, BAL>(A, S, lane, m0, y0, y1, cur, mu, T, err_out);
 #endif
         if (QUICK || err_out) ++err_out;
       }
@@ -680,7 +830,7 @@ __global__ void __launch_bounds__(AEQ_WARPS * 32, AEQ_MIN_CTAS) k_aeq_process(fn
 #pragma unroll
   for (int kk = 0; kk < 8; ++kk) {
     state.w[s][t][8 * g + kk] = S.wf[kk][lane];
-    state.w_int[s][t][8 * g + kk] = 128 * unpack_group(T.gp[kk], 0) + unpack_group(T.gp[kk], 1);
+    state.w_int[s][t][8 * g + kk] = unpack_tap<BAL>(T.gp[kk]);
   }
   if (io.n_blocks > 0) {
     state.hist[tq][iq] = v0;
@@ -705,6 +855,7 @@ __global__ void k_aeq_update_once(fntgpu_aeq_state* st, const __grid_constant__ 
   const int j8 = lane & 7;
   const int m0 = 8 * (j8 & 1) + 4 * ((j8 >> 1) & 1) + 2 * ((j8 >> 2) & 1);
   LaneTaps T;
+  T.asum = 0;
 #pragma unroll
   for (int kk = 0; kk < 8; ++kk) {
     S.wf[kk][lane] = st->w[s][t][8 * g + kk];

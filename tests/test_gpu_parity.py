@@ -463,6 +463,50 @@ def test_aeq_bank_wide_int32_inputs_vs_oracle(forward):
         assert int(st[s].saturations) == int(oq.saturations)
 
 
+@pytest.mark.parametrize("case", ["bursts", "big_taps", "mu_zero"])
+def test_aeq_stream_sum_switching_vs_oracle(case):
+    """The FNT forward sums the four input streams before the inverse transform only
+    when an exact range test passes (max |x| <= 16 over the block window and the
+    tap-digit mass bound, k_aeq.cu fused_ok); otherwise it decodes per (s, t, group)
+    like the reference. Blocks switch between the two forms within a stream:
+    amplitude bursts past 16 (int8), taps driven to saturation by a large mu (the
+    digit bound fails), and fixed taps (mu = 0)."""
+    import torch
+    from paper_2405_04253_b200.stream import AeqBank
+    cfg = P.LinkConfig().aeq_config()
+    S, nb = 6, 240
+    rng = np.random.default_rng(61)
+    x = rng.integers(-15, 16, (S, 4, 16 * nb))
+    if case == "bursts":
+        for s in range(S):
+            for b in rng.choice(nb, nb // 4, replace=False):
+                a = int(rng.choice([16, 17, 40, 127]))
+                t = int(rng.integers(0, 4))
+                x[s, t, 16 * b:16 * b + 16] = rng.integers(-a, a + 1, 16)
+        mu = O.mu_blocks(nb, mu1=2e-3, mu2=1e-4, gear_symbols=1600)
+    elif case == "big_taps":
+        mu = O.mu_blocks(nb, mu1=0.05, mu2=2e-3, gear_symbols=1600)
+    else:
+        mu = np.zeros(nb)
+    x = x.astype(np.int8)
+    bank = AeqBank(cfg, S, forward=0)  # FNTGPU_AEQ_FWD_FNT
+    y = torch.empty((S, 4, 16 * nb), dtype=torch.float64, device="cuda")
+    err = torch.empty((S, nb), dtype=torch.float64, device="cuda")
+    bank.run_planar(torch.from_numpy(x).cuda(), nb, y, mu_blocks=torch.from_numpy(mu).cuda(), err=err)
+    yh, eh = y.cpu().numpy(), err.cpu().numpy()
+    st = bank.read_state()
+    for s in range(S):
+        oq = O.Aeq(cfg.sig_spec.scale, mu=cfg.mu)
+        oy = oq.process(x[s].astype(np.int64), mu_blocks=mu)
+        assert np.array_equal(yh[s], oy), (case, s)
+        assert np.array_equal(eh[s], np.array(oq.err_trace)), (case, s)
+        assert np.array_equal(np.array(st[s].w).reshape(4, 4, 16), oq.w), (case, s)
+        assert np.array_equal(np.array(st[s].w_int).reshape(4, 4, 16), oq.w_int), (case, s)
+        assert int(st[s].saturations) == int(oq.saturations), (case, s)
+    if case == "big_taps":
+        assert max(int(st[s].saturations) for s in range(S)) > 0
+
+
 @pytest.mark.parametrize("case", [
     dict(radii=[0.6, 1.3]),                                   # 2 rings: general path
     dict(radii=[0.4, 0.9, 1.5], tap_scale=4096.0),            # 3 rings: fast path, other thresholds

@@ -275,8 +275,8 @@ __device__ __forceinline__ void fnt_stage_plain(uint32_t (&a)[N]) {
     const int j = q % half;
     // alpha^(j step): RADIX2 2^(j step); SQRT2 (even exponents only in these
     // early stages) 2^(j step / 2)
-    const int e = KIND == RADIX2 ? j * step : (j * step) / 2;
-    static_assert(KIND == RADIX2 || ((N >> (S + 1)) % 2 == 0), "odd sqrt2 power in a plain stage");
+    const int e = KIND == RADIX2 ? j * step : KIND == RADIX4 ? 2 * j * step : (j * step) / 2;
+    static_assert(KIND != SQRT2 || ((N >> (S + 1)) % 2 == 0), "odd sqrt2 power in a plain stage");
     const uint32_t u = a[g + j], w = a[g + j + half] << e;
     a[g + j] = u + w;
     a[g + j + half] = u - w;

@@ -75,7 +75,9 @@ constexpr int XF_LUT = 127;          // x / sig_scale table for |x| <= 127
 
 struct __align__(16) AeqScratch {
   double wf[8][32];           // float taps (aeq.py:99), lane-contiguous: wf[kk][lane] = w[s][t][8g+kk]
-  int32_t part[32][33];       // per-lane partial sums (direct: 16 hi + 16 lo; fnt: 16), padded
+  int32_t part[32][34];       // per-lane partial sums (direct: 16 hi + 16 lo; fnt: 16); the even
+                              // pitch lets lanes write pairs and the readers (s, m0) load pairs
+                              // with no bank conflicts
   double ey[4][AEQ_L];        // e * y per output stream
   double xf[4][66];           // x / sig_scale ring of 32, stored twice: [t][1 + 16 * parity + j (+ 32)];
                               // the +1 makes the gradient's x pairs 16-byte aligned, and the
@@ -186,6 +188,15 @@ __device__ __forceinline__ double div_D(int32_t yi, const AeqArgs& A) {
   const double q0 = dmul(a, A.Dinv);
   const double r = __fma_rn(-q0, A.D, a);
   return __fma_rn(r, A.Dinv, q0);
+}
+
+// S.part row pairs: 64-bit stores of (v[m], v[m+1]) and loads of columns (m0, m0 + 1)
+__device__ __forceinline__ void part_store16(int32_t* row, const int32_t (&v)[AEQ_L]) {
+#pragma unroll
+  for (int m = 0; m < AEQ_L; m += 2) *reinterpret_cast<int2*>(row + m) = make_int2(v[m], v[m + 1]);
+}
+__device__ __forceinline__ int2 part_pair(const int32_t* row, int m0) {
+  return *reinterpret_cast<const int2*>(row + m0);
 }
 
 // Both 7-bit groups of a tap in one word: p = sign * (hi + lo * 2^16) with
@@ -412,20 +423,18 @@ __device__ __forceinline__ void direct_dp4a(const AeqScratch& S, int t, int g, i
 }
 
 // Exact test for summing the four input streams in the transform domain (balanced
-// digits, AEQ_FUSE_T). With A_t = max |x_t| over the block window:
-//  (1) A_t <= 16 for every t: each of the reference's per-(s,t,g) group
-//      convolutions is then within [-32768, 32768] (|group| <= 127, 16 taps), so
-//      its decoded sum (aeq.py:139-143) is the exact integer FIR sum_t,k w x;
-//  (2) per output stream s, sum_t A_t sum_k |a_stk| <= 32768, and (from (1) and
-//      |b| <= 32) sum_t A_t sum_k |b_stk| <= 32768: the digit convolutions summed
-//      over t are in range, so their decoded residues are exact too.
-// Then 64 dec(sum_t conv a) + dec(sum_t conv b) is the same exact FIR. Warp-uniform.
-__device__ __forceinline__ bool fused_ok(const LaneTaps& T, uint32_t amax_t) {
-  uint32_t h = T.asum * amax_t;  // <= 8 * 256 * 16 when amax_t <= 16
-  h += __shfl_xor_sync(0xffffffffu, h, 1);
-  h += __shfl_xor_sync(0xffffffffu, h, 2);
-  h += __shfl_xor_sync(0xffffffffu, h, 4);
-  return __all_sync(0xffffffffu, amax_t <= 16u && h <= 32768u);
+// digits, AEQ_FUSE_T). With A = max |x| over the block window (all four streams):
+//  (1) A <= 16: each of the reference's per-(s,t,g) group convolutions is then
+//      within [-32768, 32768] (|group| <= 127, 16 taps), so its decoded sum
+//      (aeq.py:139-143) is the exact integer FIR sum_t,k w x;
+//  (2) A * sum_{s,t,k} |a_stk| <= 32768, and (from (1) and |b| <= 32)
+//      A * sum_{t,k} |b_stk| <= 32768: the digit convolutions summed over t are in
+//      range for every s, so their decoded residues are exact too.
+// Then 64 dec(sum_t conv a) + dec(sum_t conv b) is the same exact FIR. amax is the
+// warp's A (uniform), so the result is warp-uniform.
+__device__ __forceinline__ bool fused_ok(const LaneTaps& T, uint32_t amax) {
+  const uint32_t asum = __reduce_add_sync(0xffffffffu, T.asum);  // <= 256 * 256
+  return amax <= 16u && asum * amax <= 32768u;
 }
 
 // Forward outputs of one block with the products P_t = X_t W_stg of this lane
@@ -472,10 +481,14 @@ __device__ __forceinline__ void fused_inverse(AeqScratch& S, int lane, const uin
   to_bitrev<NB>(Q);
   fnt_dit<NB, F == 4 ? RADIX16 : RADIX4, true, false, false, AEQ_IFNT_CM>(Q);
   __syncwarp();  // every lane has read its products before S.part is reused
+  {
+    int32_t c[AEQ_L];
 #pragma unroll
-  for (int m = 0; m < AEQ_L; ++m) {
-    const uint32_t q = Q[m % NB];
-    S.part[lane][m] = (int32_t)__funnelshift_l(q, q, ((16 - m) * k1) & 31);  // 2^(-(16+m) k1)
+    for (int m = 0; m < AEQ_L; ++m) {
+      const uint32_t q = Q[m % NB];
+      c[m] = (int32_t)__funnelshift_l(q, q, ((16 - m) * k1) & 31);  // 2^(-(16+m) k1)
+    }
+    part_store16(S.part[lane], c);
   }
   __syncwarp();
   // y_int = sum over groups of BASE dec(digit 0) + dec(digit 1), each summed over F lanes
@@ -486,10 +499,11 @@ __device__ __forceinline__ void fused_inverse(AeqScratch& S, int lane, const uin
 #pragma unroll
     for (int i = 0; i < F; ++i) {
       const int r = 8 * s + 2 * (F * grp + i);
-      h0 = m_add(h0, (uint32_t)S.part[r][m0]);
-      h1 = m_add(h1, (uint32_t)S.part[r][m0 + 1]);
-      l0 = m_add(l0, (uint32_t)S.part[r + 1][m0]);
-      l1 = m_add(l1, (uint32_t)S.part[r + 1][m0 + 1]);
+      const int2 hv = part_pair(S.part[r], m0), lv = part_pair(S.part[r + 1], m0);
+      h0 = m_add(h0, (uint32_t)hv.x);
+      h1 = m_add(h1, (uint32_t)hv.y);
+      l0 = m_add(l0, (uint32_t)lv.x);
+      l1 = m_add(l1, (uint32_t)lv.y);
     }
     a0 += BASE * (int32_t)f4_mod(h0) + (int32_t)f4_mod(l0);
     a1 += BASE * (int32_t)f4_mod(h1) + (int32_t)f4_mod(l1);
@@ -502,14 +516,14 @@ __device__ __forceinline__ void fused_inverse(AeqScratch& S, int lane, const uin
 template <int FWD, bool NARROW = false>
 __device__ __forceinline__ void lane_forward(AeqScratch& S, int lane, int cur, const LaneTaps& T,
                                              int m0, int32_t& yi0, int32_t& yi1,
-                                             bool use_dp4a = false, uint32_t amax_t = 65535u) {
+                                             bool use_dp4a = false, uint32_t amax = 0xffffffffu) {
   const int s = lane >> 3, t = (lane >> 1) & 3, g = lane & 1;
   if (FWD == FNTGPU_AEQ_FWD_FNT) {
     constexpr bool BAL = AEQ_FUSE_T != 0;
 #if AEQ_PROBE != 1
     warp_input_fnt(S, lane, cur);
 #endif
-    const bool fused = BAL && fused_ok(T, amax_t);
+    const bool fused = BAL && fused_ok(T, amax);
     // all 16 taps of filter (s, t), own 8 + partner's 8 (lane ^ 1 holds the other
     // half): digit g (fused) or the reference's group g (split_taps,
     // fixedpoint.py:111-121)
@@ -563,14 +577,20 @@ __device__ __forceinline__ void lane_forward(AeqScratch& S, int lane, int cur, c
 #endif
     const int sh = g == 0 ? 7 : 0;                 // recombine 128 hi + lo (fixedpoint.py:139-143)
 #pragma unroll
-    for (int m = 0; m < AEQ_L; ++m) S.part[lane][m] = (int32_t)(f4_mod(X[AEQ_L + m]) << sh);
+    {
+      int32_t c[AEQ_L];
+#pragma unroll
+      for (int m = 0; m < AEQ_L; ++m) c[m] = (int32_t)(f4_mod(X[AEQ_L + m]) << sh);
+      part_store16(S.part[lane], c);
+    }
     __syncwarp();
     // sum over (t, g) of 128^[g=0] (c - 32768): the offsets total 4 * 129 * 32768
     int32_t a0 = -4 * 129 * 32768, a1 = -4 * 129 * 32768;
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
-      a0 += S.part[s * 8 + q][m0];
-      a1 += S.part[s * 8 + q][m0 + 1];
+      const int2 v = part_pair(S.part[s * 8 + q], m0);
+      a0 += v.x;
+      a1 += v.y;
     }
     yi0 = a0;
     yi1 = a1;
@@ -578,17 +598,18 @@ __device__ __forceinline__ void lane_forward(AeqScratch& S, int lane, int cur, c
     int32_t hi[AEQ_L], lo[AEQ_L];
     direct_dp4a(S, t, g, cur, T, hi, lo);
 #pragma unroll
-    for (int m = 0; m < AEQ_L; ++m) { S.part[lane][m] = hi[m]; S.part[lane][AEQ_L + m] = lo[m]; }
+    part_store16(S.part[lane], hi);
+    part_store16(S.part[lane] + AEQ_L, lo);
     __syncwarp();
     int32_t a0 = -4 * 129 * 32768, a1 = -4 * 129 * 32768;
 #pragma unroll
     for (int tt = 0; tt < 4; ++tt) {
       const int l0 = s * 8 + tt * 2;
       const int32_t B = (int32_t)(F4 * 1024u) + 32768;
-      a0 += 128 * (int32_t)f4_mod((uint32_t)(S.part[l0][m0] + S.part[l0 + 1][m0] + B)) +
-            (int32_t)f4_mod((uint32_t)(S.part[l0][AEQ_L + m0] + S.part[l0 + 1][AEQ_L + m0] + B));
-      a1 += 128 * (int32_t)f4_mod((uint32_t)(S.part[l0][m0 + 1] + S.part[l0 + 1][m0 + 1] + B)) +
-            (int32_t)f4_mod((uint32_t)(S.part[l0][AEQ_L + m0 + 1] + S.part[l0 + 1][AEQ_L + m0 + 1] + B));
+      const int2 h0 = part_pair(S.part[l0], m0), h1 = part_pair(S.part[l0 + 1], m0);
+      const int2 l0v = part_pair(S.part[l0], AEQ_L + m0), l1v = part_pair(S.part[l0 + 1], AEQ_L + m0);
+      a0 += 128 * (int32_t)f4_mod((uint32_t)(h0.x + h1.x + B)) + (int32_t)f4_mod((uint32_t)(l0v.x + l1v.x + B));
+      a1 += 128 * (int32_t)f4_mod((uint32_t)(h0.y + h1.y + B)) + (int32_t)f4_mod((uint32_t)(l0v.y + l1v.y + B));
     }
     yi0 = a0;
     yi1 = a1;
@@ -618,16 +639,15 @@ __device__ __forceinline__ void lane_forward(AeqScratch& S, int lane, int cur, c
       }
     }
 #pragma unroll
-    for (int m = 0; m < AEQ_L; ++m) { S.part[lane][m] = hi[m]; S.part[lane][AEQ_L + m] = lo[m]; }
+    part_store16(S.part[lane], hi);
+    part_store16(S.part[lane] + AEQ_L, lo);
     __syncwarp();
     int32_t a0 = -4 * 129 * 32768, a1 = -4 * 129 * 32768;
 #pragma unroll
     for (int tt = 0; tt < 4; ++tt) {
       const int l0 = s * 8 + tt * 2;
-      const int2 h0 = make_int2(S.part[l0][m0], S.part[l0][m0 + 1]);
-      const int2 h1 = make_int2(S.part[l0 + 1][m0], S.part[l0 + 1][m0 + 1]);
-      const int2 l0v = make_int2(S.part[l0][AEQ_L + m0], S.part[l0][AEQ_L + m0 + 1]);
-      const int2 l1v = make_int2(S.part[l0 + 1][AEQ_L + m0], S.part[l0 + 1][AEQ_L + m0 + 1]);
+      const int2 h0 = part_pair(S.part[l0], m0), h1 = part_pair(S.part[l0 + 1], m0);
+      const int2 l0v = part_pair(S.part[l0], AEQ_L + m0), l1v = part_pair(S.part[l0 + 1], AEQ_L + m0);
       // each group convolution is a residue mod F4, decoded (aeq.py:139-140) as
       // f4_mod(v + 32768) - 32768; the -32768 offsets are summed into the start value
       const int32_t B = (int32_t)(F4 * 1024u) + 32768;
@@ -749,9 +769,7 @@ __global__ void __launch_bounds__(AEQ_WARPS * 32, AEQ_MIN_CTAS) k_aeq_process(fn
   long long sat64 = 0;
   int32_t v0 = 0, v1 = 0;
   // max |x| of this lane's two samples in the previous block (window = prev + cur)
-  auto mag = [](int32_t v) -> uint32_t {
-    return min(v < 0 ? 0u - (uint32_t)v : (uint32_t)v, 65535u);
-  };
+  auto mag = [](int32_t v) -> uint32_t { return v < 0 ? 0u - (uint32_t)v : (uint32_t)v; };
   uint32_t amax_prev = max(mag(state.hist[tq][iq]), mag(state.hist[tq][iq + 1]));
   const int64_t nb = io.n_blocks;
   uint2 raw = make_uint2(0u, 0u);
@@ -797,19 +815,15 @@ __global__ void __launch_bounds__(AEQ_WARPS * 32, AEQ_MIN_CTAS) k_aeq_process(fn
 #if AEQ_LOCKSTEP
       if ((b & (AEQ_LOCKSTEP - 1)) == 0) asm volatile("bar.sync 1, %0;" :: "r"(bar_threads) : "memory");
 #endif
-      uint32_t amax_t = 65535u;  // max |x| over the block window of input stream t
+      uint32_t amax = 0xffffffffu;  // max |x| over the block window (4 x 32 samples)
       if (FWD == FNTGPU_AEQ_FWD_FNT && AEQ_FUSE_T) {
         const uint32_t a_cur = max(mag(v0), mag(v1));
-        uint32_t a = max(a_cur, amax_prev);  // stream tq, this lane's two positions
+        amax = __reduce_max_sync(0xffffffffu, max(a_cur, amax_prev));
         amax_prev = a_cur;
-        a = max(a, __shfl_xor_sync(0xffffffffu, a, 1));
-        a = max(a, __shfl_xor_sync(0xffffffffu, a, 2));
-        a = max(a, __shfl_xor_sync(0xffffffffu, a, 4));
-        amax_t = __shfl_sync(0xffffffffu, a, 8 * t);
       }
       __syncwarp();
       int32_t yi0, yi1;
-      lane_forward<FWD, NARROW>(S, lane, cur, T, m0, yi0, yi1, use_dp4a, amax_t);
+      lane_forward<FWD, NARROW>(S, lane, cur, T, m0, yi0, yi1, use_dp4a, amax);
       const double y0 = div_D<QUICK>(yi0, A);  // y_int / (sig_scale * tap_scale)
       const double y1 = div_D<QUICK>(yi1, A);
       *yrow = make_double2(y0, y1);

@@ -83,7 +83,8 @@ struct __align__(16) AeqScratch {
                               // the +1 makes the gradient's x pairs 16-byte aligned, and the
                               // 66-double row stride keeps its 8 distinct LDS.128 conflict-free
                               // so every window is contiguous (odd t-stride: no bank conflicts)
-  int32_t xi[4][2][AEQ_L];    // input integer ring: [t][block parity][j]
+  int32_t xi[4][2 * AEQ_L + 8]; // input integer ring: [t][16 * block parity + j]; the 40-word
+                                // pitch keeps the input transform's loads conflict-free
   uint32_t X[4][AEQ_N + 4];   // cooperative input spectra (FNT path), 16-B aligned padded rows
   double err[32];             // |e| values for the err_trace mean
   uint8_t xq[4][64];          // DIRECT, int8 inputs: x_block[t] reversed as bytes, ring of 32
@@ -288,8 +289,7 @@ __device__ __forceinline__ void lane_update(const AeqArgs& A, AeqScratch& S, int
     S.err[p * 16 + m0] = fabs(e0);
     S.err[p * 16 + m0 + 1] = fabs(e1);
   }
-  S.ey[s][m0] = dmul(e0, y0);
-  S.ey[s][m0 + 1] = dmul(e1, y1);
+  *reinterpret_cast<double2*>(&S.ey[s][m0]) = make_double2(dmul(e0, y0), dmul(e1, y1));
   __syncwarp();
   if (QUICK || err_out != nullptr) {
     // np.mean(|e|) over (2 pols x 16): numpy pairwise order r[j] = a[j]+a[j+8]+a[j+16]+a[j+24]
@@ -356,8 +356,9 @@ __device__ __forceinline__ void warp_input_fnt(AeqScratch& S, int lane, int cur)
   {
     const int tq = lane >> 3, n1 = lane & 7;
     // x[n1], x[n1 + 8] from the previous block's ring half, x[n1 + 16], x[n1 + 24] from this one
-    uint32_t a0 = f4_enc_small(S.xi[tq][prev][n1]), a1 = f4_enc_small(S.xi[tq][prev][n1 + 8]);
-    uint32_t a2 = f4_enc_small(S.xi[tq][cur][n1]), a3 = f4_enc_small(S.xi[tq][cur][n1 + 8]);
+    const int32_t* xr = S.xi[tq];
+    uint32_t a0 = f4_enc_small(xr[AEQ_L * prev + n1]), a1 = f4_enc_small(xr[AEQ_L * prev + n1 + 8]);
+    uint32_t a2 = f4_enc_small(xr[AEQ_L * cur + n1]), a3 = f4_enc_small(xr[AEQ_L * cur + n1 + 8]);
     const uint32_t s02 = m_add(a0, a2), d02 = m_sub(a0, a2);
     const uint32_t s13 = m_add(a1, a3), d13 = m_rot(m_sub(a1, a3), 8);
     uint32_t v[4] = {m_add(s02, s13), m_add(d02, d13), m_sub(s02, s13), m_sub(d02, d13)};
@@ -618,8 +619,8 @@ __device__ __forceinline__ void lane_forward(AeqScratch& S, int lane, int cur, c
     const int prev = cur ^ 1;
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
-      const int4 a = reinterpret_cast<const int4*>(S.xi[t][prev])[q];
-      const int4 b = reinterpret_cast<const int4*>(S.xi[t][cur])[q];
+      const int4 a = reinterpret_cast<const int4*>(S.xi[t] + AEQ_L * prev)[q];
+      const int4 b = reinterpret_cast<const int4*>(S.xi[t] + AEQ_L * cur)[q];
       xb[4 * q] = a.x; xb[4 * q + 1] = a.y; xb[4 * q + 2] = a.z; xb[4 * q + 3] = a.w;
       xb[16 + 4 * q] = b.x; xb[16 + 4 * q + 1] = b.y; xb[16 + 4 * q + 2] = b.z; xb[16 + 4 * q + 3] = b.w;
     }
@@ -706,8 +707,7 @@ __global__ void __launch_bounds__(AEQ_WARPS * 32, AEQ_MIN_CTAS) k_aeq_process(fn
   // history -> ring slot 1 (the slot block 0 treats as "previous")
   {
     const int32_t h0 = state.hist[tq][iq], h1 = state.hist[tq][iq + 1];
-    S.xi[tq][1][iq] = h0;
-    S.xi[tq][1][iq + 1] = h1;
+    *reinterpret_cast<int2*>(S.xi[tq] + AEQ_L + iq) = make_int2(h0, h1);
     const double f0 = xf_of<false>(h0, lut, A.prm.sig_scale), f1 = xf_of<false>(h1, lut, A.prm.sig_scale);
     S.xf[tq][1 + AEQ_L + iq] = f0;
     S.xf[tq][1 + AEQ_L + iq + 1] = f1;
@@ -797,8 +797,7 @@ __global__ void __launch_bounds__(AEQ_WARPS * 32, AEQ_MIN_CTAS) k_aeq_process(fn
         raw = fetch(row);
         if (mu_p) mu_next = mu_p[b + 1];
       }
-      S.xi[tq][cur][iq] = v0;
-      S.xi[tq][cur][iq + 1] = v1;
+      *reinterpret_cast<int2*>(S.xi[tq] + AEQ_L * cur + iq) = make_int2(v0, v1);
       if (FWD == FNTGPU_AEQ_FWD_DIRECT && NARROW && AEQ_DP4A) {
         const uint16_t pr = (uint16_t)(((uint32_t)v1 & 0xffu) | (((uint32_t)v0 & 0xffu) << 8));
         *reinterpret_cast<uint16_t*>(&S.xq[tq][AEQ_L * cur + 14 - iq]) = pr;

@@ -48,6 +48,10 @@ PROFILES = ROOT / "profiles"
 CDC_INT_OPS_PER_BLOCK = 4 * 192 * 6 + 128 * 6 + 256 * 2   # 5888 per 64-block = 184 / sample
 AEQ_INT_OPS_PER_BLOCK_FNT = (4 + 32 + 32) * 80 * 6 + 1024 * 6 + 448  # 39232 (incl. tap-spectrum refresh)
 AEQ_INT_OPS_PER_BLOCK_DIRECT = 2 * 4096 + 448               # 8640 (exact time-domain MIMO FIR)
+# The kernel's transform-domain stream sum (k_aeq.cu fused_ok; every block of 5-bit
+# inputs with ordinary taps) runs 8 split inverses instead of 32, plus the sums over t
+# (3 modular adds x 32 bins x 8) and the inverses' cross-lane twiddles (8 x 4 x 16):
+AEQ_INT_OPS_PER_BLOCK_FNT_FUSED = (4 + 32 + 8) * 80 * 6 + 1024 * 6 + 768 * 2 + 512 * 2 + 448  # 30272
 AEQ_FP64_OPS_PER_BLOCK = 2 * 4096 + 256 * 4 + 64 * 2 + 32 * 12  # gradient + update + y + rde ~ 9728
 
 
@@ -429,6 +433,12 @@ def main():
                           # back to back, over the measured time (INT-only "frac" is the headline)
                           "int_plus_fp64_frac": (aeq_tops / peaks["int_tops"]
                                                  + aeq_fp64 / peaks["fp64_tinst"]),
+                          # the same with the op count of the form the kernel executes
+                          # (transform-domain sum over input streams; FNT forward only)
+                          "int_plus_fp64_frac_fused_form": (
+                              (n_blk_aeq * AEQ_INT_OPS_PER_BLOCK_FNT_FUSED / (aeq_ms * 1e-3) / 1e12
+                               / peaks["int_tops"] + aeq_fp64 / peaks["fp64_tinst"])
+                              if fwd == _lib.AEQ_FWD_FNT else None),
                           "hbm_gbs": aeq_bytes / (aeq_ms * 1e-3) / 1e9},
         "k_decim_phase": {"ms": ph_ms},
     }

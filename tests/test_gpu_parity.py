@@ -463,7 +463,7 @@ def test_aeq_bank_wide_int32_inputs_vs_oracle(forward):
         assert int(st[s].saturations) == int(oq.saturations)
 
 
-@pytest.mark.parametrize("case", ["bursts", "big_taps", "mu_zero"])
+@pytest.mark.parametrize("case", ["bursts", "big_taps", "mu_zero", "int32"])
 def test_aeq_stream_sum_switching_vs_oracle(case):
     """The FNT forward sums the four input streams before the inverse transform only
     when an exact range test passes (max |x| <= 16 over the block window and the
@@ -477,7 +477,12 @@ def test_aeq_stream_sum_switching_vs_oracle(case):
     S, nb = 6, 240
     rng = np.random.default_rng(61)
     x = rng.integers(-15, 16, (S, 4, 16 * nb))
-    if case == "bursts":
+    if case == "int32":  # 32-bit input rows: small blocks take the stream sum, wide ones not
+        for s in range(S):
+            for b in rng.choice(nb, nb // 5, replace=False):
+                x[s, :, 16 * b:16 * b + 16] = rng.integers(-40000, 40001, (4, 16))
+        mu = O.mu_blocks(nb, mu1=2e-3, mu2=1e-4, gear_symbols=1600)
+    elif case == "bursts":
         for s in range(S):
             for b in rng.choice(nb, nb // 4, replace=False):
                 a = int(rng.choice([16, 17, 40, 127]))
@@ -488,7 +493,7 @@ def test_aeq_stream_sum_switching_vs_oracle(case):
         mu = O.mu_blocks(nb, mu1=0.05, mu2=2e-3, gear_symbols=1600)
     else:
         mu = np.zeros(nb)
-    x = x.astype(np.int8)
+    x = x.astype(np.int32 if case == "int32" else np.int8)
     bank = AeqBank(cfg, S, forward=0)  # FNTGPU_AEQ_FWD_FNT
     y = torch.empty((S, 4, 16 * nb), dtype=torch.float64, device="cuda")
     err = torch.empty((S, nb), dtype=torch.float64, device="cuda")

@@ -463,14 +463,16 @@ def test_aeq_bank_wide_int32_inputs_vs_oracle(forward):
         assert int(st[s].saturations) == int(oq.saturations)
 
 
+@pytest.mark.parametrize("forward", AEQ_MODES)
 @pytest.mark.parametrize("case", ["bursts", "big_taps", "mu_zero", "int32"])
-def test_aeq_stream_sum_switching_vs_oracle(case):
+def test_aeq_stream_sum_switching_vs_oracle(case, forward):
     """The FNT forward sums the four input streams before the inverse transform only
     when an exact range test passes (max |x| <= 16 over the block window and the
     tap-digit mass bound, k_aeq.cu fused_ok); otherwise it decodes per (s, t, group)
     like the reference. Blocks switch between the two forms within a stream:
     amplitude bursts past 16 (int8), taps driven to saturation by a large mu (the
-    digit bound fails), and fixed taps (mu = 0)."""
+    digit bound fails), and fixed taps (mu = 0). The DIRECT forward skips its
+    per-group decodes on the same max |x| <= 16 test."""
     import torch
     from paper_2405_04253_b200.stream import AeqBank
     cfg = P.LinkConfig().aeq_config()
@@ -494,7 +496,7 @@ def test_aeq_stream_sum_switching_vs_oracle(case):
     else:
         mu = np.zeros(nb)
     x = x.astype(np.int32 if case == "int32" else np.int8)
-    bank = AeqBank(cfg, S, forward=0)  # FNTGPU_AEQ_FWD_FNT
+    bank = AeqBank(cfg, S, forward=forward)
     y = torch.empty((S, 4, 16 * nb), dtype=torch.float64, device="cuda")
     err = torch.empty((S, nb), dtype=torch.float64, device="cuda")
     bank.run_planar(torch.from_numpy(x).cuda(), nb, y, mu_blocks=torch.from_numpy(mu).cuda(), err=err)
@@ -503,7 +505,7 @@ def test_aeq_stream_sum_switching_vs_oracle(case):
     for s in range(S):
         oq = O.Aeq(cfg.sig_spec.scale, mu=cfg.mu)
         oy = oq.process(x[s].astype(np.int64), mu_blocks=mu)
-        assert np.array_equal(yh[s], oy), (case, s)
+        assert np.array_equal(yh[s], oy), (case, forward, s)
         assert np.array_equal(eh[s], np.array(oq.err_trace)), (case, s)
         assert np.array_equal(np.array(st[s].w).reshape(4, 4, 16), oq.w), (case, s)
         assert np.array_equal(np.array(st[s].w_int).reshape(4, 4, 16), oq.w_int), (case, s)

@@ -581,7 +581,6 @@ __device__ __forceinline__ void lane_forward(AeqScratch& S, int lane, int cur, c
     fnt_dit<AEQ_N, RADIX2, true, false, true, AEQ_IFNT_CM>(X);  // outputs 16..31 only
 #endif
     const int sh = g == 0 ? 7 : 0;                 // recombine 128 hi + lo (fixedpoint.py:139-143)
-#pragma unroll
     {
       int32_t c[AEQ_L];
 #pragma unroll
@@ -659,7 +658,6 @@ __device__ __forceinline__ void lane_forward(AeqScratch& S, int lane, int cur, c
         lo[m] += tl * xv;
       }
     }
-#pragma unroll
     part_store16(S.part[lane], hi);
     part_store16(S.part[lane] + AEQ_L, lo);
     __syncwarp();

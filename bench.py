@@ -272,7 +272,10 @@ def _config_dict(args, cpu=False):
                       "6-bit CDC taps (N=64 sqrt2 FNT), 4x4 FNT-AEQ (N=32) gear-shift mu")
                      % (args.links, int(math.log2(args.symbols))),
          "links_per_gpu": args.links, "symbols": args.symbols, "samples_per_pol": 2 * args.symbols,
-         "aeq_forward": args.forward, "parallelism": f"links sharded over {args.gpus} GPU(s), no collective",
+         "aeq_forward": args.forward,
+         "cdc_kernel": "k_cdc64_tc (tensor-core split-integer FNT)" if args.cdc_kernel == "tc"
+                       else "k_cdc64 (shift-add FNT)",
+         "parallelism": f"links sharded over {args.gpus} GPU(s), no collective",
          "l2": "inputs (int8 I/Q, %.1f GB/GPU) exceed the 126 MB L2; no flush needed"
                % (4 * args.links * 2 * args.symbols / 1e9)}
     if cpu:
@@ -300,6 +303,9 @@ def main():
     ap.add_argument("--c4-samples", type=int, default=1 << 31, help="C4 samples per polarization")
     ap.add_argument("--no-alt", action="store_true", help="skip the direct-forward AEQ comparison")
     ap.add_argument("--no-quality", action="store_true", help="skip the on-device BER/EVM scoring")
+    ap.add_argument("--cdc-kernel", default="auto", choices=["auto", "tc", "shift"],
+                    help="FNT-CDC kernel for the int8 planes: shift-add butterflies (auto/shift) "
+                         "or the tensor-core split-integer matrix form (tc)")
     args = ap.parse_args()
     if args.impl == "reference":
         impl_reference(args)
@@ -323,8 +329,10 @@ def main():
 
     import paper_2405_04253_b200 as P
     from paper_2405_04253_b200 import _lib
+    from paper_2405_04253_b200 import cdc as cdc_mod
     from paper_2405_04253_b200.linkgen import DeviceLinkGenerator
     from paper_2405_04253_b200.stream import CdcAeqChain
+    cdc_mod.set_cdc_kernel(args.cdc_kernel)
 
     if args.config == "c4":
         run_c4(args, world, rank, local)
@@ -511,6 +519,13 @@ def main():
                     "(bit-identical outputs, tests/test_gpu_parity.py); headline uses the FNT forward"}
         chain.aeq.prm.forward = _lib.AEQ_FWD_FNT
 
+    # the CDC launch of the chain through both kernels (same inputs, same outputs)
+    if not args.no_alt:
+        line["cdc_kernels"] = time_cdc_kernels(
+            lambda: chain.cdc.run(xr, xi, length=L, qr=chain.qr, qi=chain.qi,
+                                  q_spec=chain.sig_spec, decim_acc=chain.acc),
+            args.steps, world)
+
     # end-to-end through the public host API: pinned host int8 in, float64 AEQ y out
     if not args.no_e2e:
         line["e2e"] = run_e2e(args, eng, cfg, xr, xi, fwd, world)
@@ -550,6 +565,39 @@ def run_cpu_cdc_baseline(eng, n: int, cores: int) -> dict:
                        f"process_int), one process per core, {wall:.1f} s wall")}
 
 
+def time_cdc_kernels(run, reps: int, world: int) -> dict:
+    """Device time of one CDC launch with each kernel (tensor-core matrix form and the
+    shift-add butterflies), on the launching stream, max over ranks."""
+    import torch
+    from paper_2405_04253_b200 import cdc as cdc_mod
+    out = {}
+    prev = cdc_mod.set_cdc_kernel("tc")
+    try:
+        for name in ("tc", "shift"):
+            cdc_mod.set_cdc_kernel(name)
+            run()
+            torch.cuda.synchronize()
+            s = torch.cuda.current_stream()
+            a = torch.cuda.Event(enable_timing=True)
+            b = torch.cuda.Event(enable_timing=True)
+            a.record(s)
+            for _ in range(reps):
+                run()
+            b.record(s)
+            torch.cuda.synchronize()
+            ms = a.elapsed_time(b) / reps
+            if world > 1:
+                ms = allreduce([ms], "max")[0]
+            out[name + "_ms"] = ms
+    finally:
+        cdc_mod.set_cdc_kernel(prev)
+    out["speedup_tc"] = out["shift_ms"] / out["tc_ms"]
+    out["note"] = ("k_cdc64_tc: forward FNT-64 and pruned inverse as split-integer int8 matrix "
+                   "products (mma.sync IMMA.16832); k_cdc64: radix-sqrt2 shift-add butterflies. "
+                   "Bit-identical outputs (tests/test_gpu_parity.py)")
+    return out
+
+
 def c4_traffic(world: int):
     """DRAM bytes of one k_cdc64 launch at config 4 on one GPU, from the committed ncu
     --set full capture (profiles/ncu_summary_r01_c4.json); None for other shard sizes."""
@@ -570,8 +618,10 @@ def run_c4(args, world, rank, local):
     import torch
     import torch.distributed as dist
     import paper_2405_04253_b200 as P
+    from paper_2405_04253_b200 import cdc as cdc_mod
     from paper_2405_04253_b200.linkgen import DeviceLinkGenerator
     from paper_2405_04253_b200.sharding import cdc_range_shards
+    cdc_mod.set_cdc_kernel(args.cdc_kernel)
     from paper_2405_04253_b200.stream import CdcBank
 
     cfg = P.LinkConfig(z_km=75.0, seed=3)
@@ -641,6 +691,7 @@ def run_c4(args, world, rank, local):
                                "samples per pol, 75 km taps, range-sharded over %d GPU(s) with the "
                                "overlap-save halo" % (L, world),
                    "samples_per_pol": L, "shard_out": [sh.out_first, sh.out_count],
+                   "cdc_kernel": "k_cdc64_tc" if args.cdc_kernel == "tc" else "k_cdc64",
                    "l2": "inputs (%.1f GB) exceed L2" % (hbm_bytes / 1e9)},
         "roofline": {"bound": "int", "kernel": "k_cdc64", "achieved": achieved,
                      "peak": peaks["int_tops"], "unit": "Tops/s",
@@ -650,6 +701,8 @@ def run_c4(args, world, rank, local):
                              "frac": hbm_gbs / peaks["hbm_gbs"]}},
         "clocks": clk, "gpu_launches": args.steps,
     }
+    if not args.no_alt:
+        line["cdc_kernels"] = time_cdc_kernels(step, args.steps, world)
     if not args.no_e2e:
         # host buffers through the C ABI: pinned int8 I/Q -> H2D -> CDC -> D2H int16 I/Q
         from paper_2405_04253_b200.stream import HostCdc

@@ -34,7 +34,7 @@ vp = C.c_void_p
 
 class CdcTaps(C.Structure):
     _fields_ = [("b_plus", C.c_uint32 * 64), ("b_minus", C.c_uint32 * 64),
-                ("n_taps", C.c_int32), ("reserved", C.c_int32)]
+                ("n_taps", C.c_int32), ("kernel", C.c_int32)]
 
 
 class CdcIO(C.Structure):

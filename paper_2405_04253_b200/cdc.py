@@ -13,6 +13,7 @@ from __future__ import annotations
 
 import ctypes as C
 import math
+import os
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -111,6 +112,25 @@ def _device_dtype(a: np.ndarray, half: int) -> np.dtype:
     return np.dtype(np.int32)
 
 
+# Kernel behind fntgpu_cdc64_process for int8 planes (fntgpu_cdc_taps.kernel): the
+# shift-add butterfly kernel ("auto"/"shift", measured faster on B200) or the
+# tensor-core split-integer matrix form of the FNT ("tc"). Both are bit-exact; other
+# input dtypes always take the shift-add kernel.
+CDC_KERNELS = {"auto": 0, "shift": 1, "tc": 2}
+_cdc_kernel = os.environ.get("FNTGPU_CDC_KERNEL", "auto")
+if _cdc_kernel not in CDC_KERNELS:
+    raise ValueError(f"FNTGPU_CDC_KERNEL must be one of {sorted(CDC_KERNELS)}")
+
+
+def set_cdc_kernel(name: str) -> str:
+    """Select the CDC kernel for tap descriptors built afterwards; returns the previous."""
+    global _cdc_kernel
+    if name not in CDC_KERNELS:
+        raise ValueError(f"unknown CDC kernel {name!r}: one of {sorted(CDC_KERNELS)}")
+    prev, _cdc_kernel = _cdc_kernel, name
+    return prev
+
+
 @dataclass
 class FntCdcEngine:
     """Residue-domain overlap-save dispersion equalizer for one polarization
@@ -167,6 +187,7 @@ class FntCdcEngine:
                 t.b_minus[k] = int(self._b_minus[k])
             t.n_taps = int(self.config.n_taps)
             self._taps_c = t
+        self._taps_c.kernel = CDC_KERNELS[_cdc_kernel]
         return self._taps_c
 
     @property

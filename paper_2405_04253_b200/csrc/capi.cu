@@ -267,6 +267,8 @@ int fntgpu_struct_sizes(int64_t* out, int n) {
 
 int fntgpu_cdc64_process(const fntgpu_cdc_taps* taps, const fntgpu_cdc_io* io, void* stream) {
   if (!taps || !io) return fail(FNTGPU_EINVAL, "cdc64_process: NULL argument");
+  if (taps->kernel < FNTGPU_CDC_KERNEL_AUTO || taps->kernel > FNTGPU_CDC_KERNEL_TC)
+    return fail(FNTGPU_EINVAL, "cdc64_process: unknown kernel selector %d", taps->kernel);
   if (taps->n_taps < 1 || taps->n_taps > 33)
     return fail(FNTGPU_EINVAL, "n_taps=%d exceeds overlap-save validity 33 for block_n=64", taps->n_taps);
   if (io->n_streams < 0 || io->length < 0 || io->out_count < 0 || io->x_count < 0)

@@ -59,6 +59,8 @@ constexpr int UP = CDC_UP;                      // pitch of the u staging rows: 
 struct CdcArgs {
   uint32_t bp[CDC_N];  // b+ * 2^25 mod F4
   uint32_t bm[CDC_N];  // b- * 2^25 mod F4
+  uint32_t rbp[CDC_N]; // b+ mod F4 (tensor-core form: unscaled, cdc.py:124-135)
+  uint32_t rbm[CDC_N]; // b- mod F4
   fntgpu_cdc_io io;
   int64_t blk_begin;   // first overlap-save block index of this launch
   int64_t blk_count;   // blocks per stream
@@ -123,6 +125,9 @@ __device__ __forceinline__ int32_t requant_int(int32_t y, int k, const int8_t* t
 // int16 stores, 32-bit |y|^2 and IMAD.WIDE |y|^4 statistics. Preconditions checked
 // on the host (launch_cdc64): out_dtype in {NONE, I16}, q_shift >= 1 when
 // requantizing, (c + out_first) % 4 == 0 and 4-byte aligned planes and strides.
+// PRE: s_u holds the decoded outputs + 32768 (tensor-core form) instead of the u+-
+// words of the two inverse transforms.
+template <bool PRE = false>
 __device__ __forceinline__ void cdc_epilogue_fast(const CdcArgs& A, const uint32_t* s_u, int s,
                                                   int64_t n0, int lo, int hi) {
   const fntgpu_cdc_io& io = A.io;
@@ -156,8 +161,13 @@ __device__ __forceinline__ void cdc_epilogue_fast(const CdcArgs& A, const uint32
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
       const uint32_t up = upv[e], um = umv[e];
-      zr[e] = (int32_t)f4_mod(m_add(up, um)) - 32768;
-      zi[e] = (int32_t)f4_mod(m_rot(m_sub(up, um), 24)) - 32768;
+      if (PRE) {
+        zr[e] = (int32_t)up - 32768;
+        zi[e] = (int32_t)um - 32768;
+      } else {
+        zr[e] = (int32_t)f4_mod(m_add(up, um)) - 32768;
+        zi[e] = (int32_t)f4_mod(m_rot(m_sub(up, um), 24)) - 32768;
+      }
     }
     if (CDC_PROBE != 1 && qr) {
       uint32_t pr = 0, pi = 0;
@@ -227,6 +237,82 @@ __device__ __forceinline__ void cdc_epilogue_fast(const CdcArgs& A, const uint32
       if ((tid & 31) == 0) {
         if (x) atomicAdd(io.decim_acc + ((int64_t)s * 2 + pa) * 4 + q, x);
         if (y) atomicAdd(io.decim_acc + ((int64_t)s * 2 + (pa ^ 1)) * 4 + q, y);
+      }
+    }
+  }
+}
+
+// Any-dtype epilogue (process_int int16/32/64, process complex128, float64
+// requantization): one output per thread per step.
+template <bool PRE = false>
+__device__ __forceinline__ void cdc_epilogue_generic(const CdcArgs& A, const uint32_t* s_u, int s,
+                                                     int64_t n0, int64_t lo, int64_t hi) {
+  const fntgpu_cdc_io& io = A.io;
+  const int tid = threadIdx.x;
+  // n advances by CDC_CTA (even): each thread only ever sees one sampling phase
+  const int my_ph = (int)((lo + tid) & 1);
+  unsigned long long s2 = 0, s4lo = 0, s4hi = 0;
+  for (int64_t n = lo + tid; n < hi; n += CDC_CTA) {
+    const int idx = (int)(n - n0);
+    const int r = (idx >> 5) * UP + (idx & 31);
+    const uint32_t up = s_u[r], um = s_u[CDC_BLK * UP + r];
+    const int32_t zr = PRE ? (int32_t)up - 32768 : (int32_t)f4_mod(m_add(up, um)) - 32768;
+    const int32_t zi = PRE ? (int32_t)um - 32768 : (int32_t)f4_mod(m_rot(m_sub(up, um), 24)) - 32768;
+    const int64_t o = n - io.out_first;
+    switch (io.out_dtype) {
+      case FNTGPU_I16:
+        reinterpret_cast<int16_t*>(io.yr)[s * io.y_stride + o] = (int16_t)zr;
+        reinterpret_cast<int16_t*>(io.yi)[s * io.y_stride + o] = (int16_t)zi;
+        break;
+      case FNTGPU_I32:
+        reinterpret_cast<int32_t*>(io.yr)[s * io.y_stride + o] = zr;
+        reinterpret_cast<int32_t*>(io.yi)[s * io.y_stride + o] = zi;
+        break;
+      case FNTGPU_I64:
+        reinterpret_cast<int64_t*>(io.yr)[s * io.y_stride + o] = zr;
+        reinterpret_cast<int64_t*>(io.yi)[s * io.y_stride + o] = zi;
+        break;
+      case FNTGPU_C128: {
+        double2 v;
+        v.x = __dmul_rn((double)zr, io.inv_scale);  // numpy complex / real == * (1/scale) (cdc.py:180)
+        v.y = __dmul_rn((double)zi, io.inv_scale);
+        reinterpret_cast<double2*>(io.yr)[s * io.y_stride + o] = v;
+        break;
+      }
+      default:
+        break;
+    }
+    if (io.qr) {
+      // quantize_real(s, spec) on s = y_int * (1/output_scale)  (linksim.py:404)
+      const double vr = __dmul_rn(__dmul_rn((double)zr, io.inv_scale), io.q_scale);
+      const double vi = __dmul_rn(__dmul_rn((double)zi, io.inv_scale), io.q_scale);
+      double ar = floor(__dadd_rn(fabs(vr), 0.5)), ai = floor(__dadd_rn(fabs(vi), 0.5));
+      const double qm = (double)io.q_max;
+      ar = ar > qm ? qm : ar;
+      ai = ai > qm ? qm : ai;
+      io.qr[s * io.q_stride + o] = (int8_t)(vr < 0 ? -(int)ar : (int)ar);
+      io.qi[s * io.q_stride + o] = (int8_t)(vi < 0 ? -(int)ai : (int)ai);
+    }
+    if (io.decim_acc) {
+      const unsigned long long m2 =
+          (unsigned long long)((int64_t)zr * zr) + (unsigned long long)((int64_t)zi * zi);
+      const unsigned long long m4 = m2 * m2;  // |y|^4 < 2^62
+      s2 += m2;
+      s4lo += m4;
+      s4hi += (s4lo < m4);
+    }
+  }
+  if (io.decim_acc) {
+    // exact integer statistics: warp-reduce 32-bit limbs per phase, one atomic per value
+    const unsigned long long v[4] = {s2, s4lo & 0xffffffffull, s4lo >> 32, s4hi};
+#pragma unroll
+    for (int ph = 0; ph < 2; ++ph) {
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        unsigned long long x = my_ph == ph ? v[k] : 0ull;
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) x += __shfl_xor_sync(0xffffffffu, x, off);
+        if ((tid & 31) == 0 && x) atomicAdd(io.decim_acc + ((int64_t)s * 2 + ph) * 4 + k, x);
       }
     }
   }
@@ -370,71 +456,467 @@ __global__ void __launch_bounds__(CDC_CTA, CDC_MIN_CTAS) k_cdc64(const __grid_co
     cdc_epilogue_fast(A, s_u, s, n0, (int)(lo - n0), (int)(hi - n0));
     return;
   }
-  // n advances by CDC_CTA (even): each thread only ever sees one sampling phase
-  const int my_ph = (int)((lo + tid) & 1);
-  unsigned long long s2 = 0, s4lo = 0, s4hi = 0;
-  for (int64_t n = lo + tid; n < hi; n += CDC_CTA) {
-    const int idx = (int)(n - n0);
-    const int r = (idx >> 5) * UP + (idx & 31);
-    const uint32_t up = s_u[r], um = s_u[CDC_BLK * UP + r];
-    const int32_t zr = (int32_t)f4_mod(m_add(up, um)) - 32768;
-    const int32_t zi = (int32_t)f4_mod(m_rot(m_sub(up, um), 24)) - 32768;
-    const int64_t o = n - io.out_first;
-    switch (io.out_dtype) {
-      case FNTGPU_I16:
-        reinterpret_cast<int16_t*>(io.yr)[s * io.y_stride + o] = (int16_t)zr;
-        reinterpret_cast<int16_t*>(io.yi)[s * io.y_stride + o] = (int16_t)zi;
-        break;
-      case FNTGPU_I32:
-        reinterpret_cast<int32_t*>(io.yr)[s * io.y_stride + o] = zr;
-        reinterpret_cast<int32_t*>(io.yi)[s * io.y_stride + o] = zi;
-        break;
-      case FNTGPU_I64:
-        reinterpret_cast<int64_t*>(io.yr)[s * io.y_stride + o] = zr;
-        reinterpret_cast<int64_t*>(io.yi)[s * io.y_stride + o] = zi;
-        break;
-      case FNTGPU_C128: {
-        double2 v;
-        v.x = __dmul_rn((double)zr, io.inv_scale);  // numpy complex / real == * (1/scale) (cdc.py:180)
-        v.y = __dmul_rn((double)zi, io.inv_scale);
-        reinterpret_cast<double2*>(io.yr)[s * io.y_stride + o] = v;
-        break;
+  cdc_epilogue_generic(A, s_u, s, n0, lo, hi);
+}
+
+// ---------------------------------------------------------------------------------
+// Tensor-core form: the same overlap-save blocks with the 64-point forward FNT and
+// the pruned inverse as split-integer matrix products on the int8 tensor cores
+// (mma.sync m16n8k32, SASS IMMA.16832, exact int32 accumulation), the pointwise tap
+// products and mod-F4 reductions on the CUDA cores. Every transform matrix entry is a
+// 64th root of unity alpha^e (alpha = sqrt(2) = 4080), stored as two 8-bit limbs
+// t = 256 t1 + t0 with t1 in [0, 255] (u8) and t0 in [-128, 127] (s8), a split that
+// holds every root (tests/test_tc_math.py restates the whole algorithm in numpy).
+// One warp owns an M-tile of 16 consecutive blocks (rows); lane = 4 g + tig.
+//   forward  X_r = T x_r, X_i = T x_i        (K = 64 samples, N = 64 bins x 2 limbs)
+//            X = 256 P1 + P0 == FNT(x) mod F4
+//   products s = A+ b+ + A- b- = X_r beta1 + X_i beta2, d = X_r beta3 + X_i beta4
+//            (A+- = X_r +- 2^8 X_i, cdc.py:148-149; two IMAD.WIDE each), then
+//            w = (s + 32896) mod F4 in [0, 65536]: the signed limbs of s are the bytes
+//            of w ^ 0x80 (w = 65536 does not fit and is corrected after the MMAs)
+//   inverse  z_re = M_re s, z_im = M_im d      (K = 64 bins, N = 32 kept outputs, 2 x 2
+//            limb products: z == 256 Qmid + Q00 - Q11 since 2^16 == -1 mod F4)
+// The accumulator fragments of the forward products are laid out so that each
+// thread's values are exactly the A-fragment bytes of the inverse MMA (the inverse
+// matrix rows are permuted to match), so nothing moves between lanes.
+#ifndef CDC_TC_MIN_CTAS
+#define CDC_TC_MIN_CTAS 3
+#endif
+constexpr int TC_E_RE = 50;  // c_re * N^-1 = 2^25 = alpha^50 (cdc.py:152)
+constexpr int TC_E_IM = 34;  // c_im * N^-1 = 2^17 = alpha^34 (cdc.py:153)
+
+struct TcTables {
+  uint4 fwd[8][2][32];   // [bin n-tile][k-step][lane]: (t1 b0, t1 b1, t0 b0, t0 b1) of T[k][n]
+  uint4 inv[2][8][32];   // [k-step][out n-tile: re 0-3, im 4-7][lane]
+  uint4 beta[CDC_N];     // per bin: beta1..beta4 (canonical residues)
+  uint32_t root[CDC_N];  // alpha^e mod F4
+  uint32_t flags[CDC_CTA / 32][16][2][2];  // rare path: (row, s|d, bin) with w == 65536
+  uint4 afr[CDC_CTA / 32][2][2][2][32];    // inverse A quads [warp][s|d][k-step][lo|hi limb][lane]
+  int8_t x[2][2][WIN];                     // input windows [buffer][re|im] (TMA double buffer)
+};
+
+// D (+)= A B on the int8 tensor cores. Not volatile: no side effects, so the compiler
+// may interleave the MMAs with the CUDA-core epilogue of the previous chunk. The _z
+// forms start a chain from zero (C = RZ, no register initialisation).
+#define FNT_MMA(NAME, TA, TB)                                                                    \
+  __device__ __forceinline__ void NAME(int (&d)[4], const uint32_t (&a)[4], uint32_t b0,          \
+                                       uint32_t b1) {                                            \
+    asm("mma.sync.aligned.m16n8k32.row.col.s32." TA "." TB ".s32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, " \
+        "{%8,%9}, {%0,%1,%2,%3};"                                                                \
+        : "+r"(d[0]), "+r"(d[1]), "+r"(d[2]), "+r"(d[3])                                         \
+        : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));                        \
+  }                                                                                              \
+  __device__ __forceinline__ void NAME##_z(int (&d)[4], const uint32_t (&a)[4], uint32_t b0,      \
+                                           uint32_t b1) {                                        \
+    asm("mma.sync.aligned.m16n8k32.row.col.s32." TA "." TB ".s32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, " \
+        "{%8,%9}, {%10,%10,%10,%10};"                                                            \
+        : "=r"(d[0]), "=r"(d[1]), "=r"(d[2]), "=r"(d[3])                                         \
+        : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1), "r"(0));                 \
+  }
+FNT_MMA(mma_s8u8, "s8", "u8")
+FNT_MMA(mma_s8s8, "s8", "s8")
+#undef FNT_MMA
+
+// (u8, s8) limb bytes of a root: t1 in byte 0 of .x, t0 in byte 0 of .y
+__device__ __forceinline__ uint2 tc_limbs(uint32_t t) {
+  const int32_t v = t > 65407u ? (int32_t)t - (int32_t)F4 : (int32_t)t;
+  const int32_t t0 = ((v + 128) & 255) - 128;
+  const int32_t t1 = (v - t0) >> 8;
+  return make_uint2((uint32_t)t1 & 255u, (uint32_t)t0 & 255u);
+}
+
+// Fragment tables, built by every CTA once (the kernel is persistent).
+__device__ void tc_build_tables(TcTables& T, const CdcArgs& A) {
+  const int tid = threadIdx.x;
+  if (tid < CDC_N) {
+    const int h = tid >> 1;
+    uint32_t p2 = h < 16 ? (1u << h) : F4 - (1u << (h - 16));  // 2^h mod F4
+    T.root[tid] = (tid & 1) ? (uint32_t)(((uint64_t)p2 * 4080u) % F4) : p2;
+    const uint64_t bp = A.rbp[tid] % F4, bm = A.rbm[tid] % F4;
+    const uint64_t sum = (bp + bm) % F4, dif = (bp + F4 - bm) % F4;
+    T.beta[tid] = make_uint4((uint32_t)sum, (uint32_t)(256 * dif % F4), (uint32_t)dif,
+                             (uint32_t)(256 * sum % F4));
+  }
+  for (int i = tid; i < CDC_CTA / 32 * 64; i += CDC_CTA) (&T.flags[0][0][0][0])[i] = 0u;
+  __syncthreads();
+  // word w of a table = one of (t1 b0, t1 b1, t0 b0, t0 b1) of one lane of one fragment
+  for (int i = tid; i < 2 * 8 * 2 * 32 * 4; i += CDC_CTA) {
+    const int q = i & 3, lane = (i >> 2) & 31, g = lane >> 2, tig = lane & 3;
+    const int half = q & 1;  // b0 (K 0-15) or b1 (K 16-31)
+    const bool lo_limb = q >= 2;
+    uint32_t word = 0;
+    if (i < 8 * 2 * 32 * 4) {
+      // forward: [nt][ks][lane]; column g <-> bin 8 nt + g, K byte j <-> window sample
+      // n = 32 ks + 16 half + 4 tig + j (natural order: the A quads come from ldmatrix)
+      const int ks = (i >> 7) & 1, nt = i >> 8;
+      const int k = 8 * nt + g;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int n = 32 * ks + 16 * half + 4 * tig + j;
+        const uint2 l = tc_limbs(T.root[(n * k) & 63]);
+        word |= (lo_limb ? l.y : l.x) << (8 * j);
       }
-      default:
-        break;
-    }
-    if (io.qr) {
-      // quantize_real(s, spec) on s = y_int * (1/output_scale)  (linksim.py:404)
-      const double vr = __dmul_rn(__dmul_rn((double)zr, io.inv_scale), io.q_scale);
-      const double vi = __dmul_rn(__dmul_rn((double)zi, io.inv_scale), io.q_scale);
-      double ar = floor(__dadd_rn(fabs(vr), 0.5)), ai = floor(__dadd_rn(fabs(vi), 0.5));
-      const double qm = (double)io.q_max;
-      ar = ar > qm ? qm : ar;
-      ai = ai > qm ? qm : ai;
-      io.qr[s * io.q_stride + o] = (int8_t)(vr < 0 ? -(int)ar : (int)ar);
-      io.qi[s * io.q_stride + o] = (int8_t)(vi < 0 ? -(int)ai : (int)ai);
-    }
-    if (io.decim_acc) {
-      const unsigned long long m2 =
-          (unsigned long long)((int64_t)zr * zr) + (unsigned long long)((int64_t)zi * zi);
-      const unsigned long long m4 = m2 * m2;  // |y|^4 < 2^62
-      s2 += m2;
-      s4lo += m4;
-      s4hi += (s4lo < m4);
+      (&T.fwd[0][0][0].x)[i] = word;
+    } else {
+      // inverse: [ks][ot][lane]; column g <-> output m = 32 + 8 (ot & 3) + g; K byte j of
+      // half h <-> bin 32 ks + 16 h + 8 (j >> 1) + 2 tig + (j & 1) (forward C layout)
+      const int ii = i - 8 * 2 * 32 * 4;
+      const int ot = (ii >> 7) & 7, ks = ii >> 10;
+      const int m = 32 + 8 * (ot & 3) + g;
+      const int E = ot < 4 ? TC_E_RE : TC_E_IM;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int k = 32 * ks + 16 * half + 8 * (j >> 1) + 2 * tig + (j & 1);
+        const uint2 l = tc_limbs(T.root[(E - m * k) & 63]);
+        word |= (lo_limb ? l.y : l.x) << (8 * j);
+      }
+      (&T.inv[0][0][0].x)[ii] = word;
     }
   }
-  if (io.decim_acc) {
-    // exact integer statistics: warp-reduce 32-bit limbs per phase, one atomic per value
-    const unsigned long long v[4] = {s2, s4lo & 0xffffffffull, s4lo >> 32, s4hi};
-#pragma unroll
-    for (int ph = 0; ph < 2; ++ph) {
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        unsigned long long x = my_ph == ph ? v[k] : 0ull;
-#pragma unroll
-        for (int off = 16; off > 0; off >>= 1) x += __shfl_xor_sync(0xffffffffu, x, off);
-        if ((tid & 31) == 0 && x) atomicAdd(io.decim_acc + ((int64_t)s * 2 + ph) * 4 + k, x);
+  __syncthreads();
+}
+
+// (X_r b1 + X_i b2 + 32896) mod F4 in [0, 65536]: 64-bit products (|X| < 2^30, b <= 2^16)
+// folded with 2^32 == 1; the high word is small, so one end-around carry suffices.
+__device__ __forceinline__ uint32_t tc_w(int32_t xr, int32_t xi, uint32_t b1, uint32_t b2) {
+  const long long p = (long long)xr * (int32_t)b1 + (long long)xi * (int32_t)b2;
+  const uint32_t lo = (uint32_t)p;
+  const uint32_t t = (uint32_t)((int32_t)(p >> 32) + (int32_t)(F4 + 32896u));
+  return f4_mod(m_add(lo, t));
+}
+
+// signed limbs of the 4 values of one A-fragment register (bytes j = 0..3 in K order)
+__device__ __forceinline__ void tc_pack(uint32_t w0, uint32_t w1, uint32_t w2, uint32_t w3,
+                                        uint32_t& lo, uint32_t& hi) {
+  const uint32_t ab = __byte_perm(w0, w1, 0x5140), cd = __byte_perm(w2, w3, 0x5140);
+  lo = __byte_perm(ab, cd, 0x5410) ^ 0x80808080u;
+  hi = __byte_perm(ab, cd, 0x7632) ^ 0x80808080u;
+}
+
+// four 8x16-byte shared-memory matrices -> one IMMA A-operand quad (ldmatrix.x4)
+__device__ __forceinline__ void ldsm_x4(uint32_t (&a)[4], const void* p) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(a[0]), "=r"(a[1]), "=r"(a[2]), "=r"(a[3])
+               : "r"((uint32_t)__cvta_generic_to_shared(p)));
+}
+
+// Window staging of one item: interior windows by two TMA bulk copies completing on
+// the buffer's mbarrier, others by vector loads (CTA-synchronous).
+__device__ __forceinline__ bool tc_bulk_ok(const CdcArgs& A, int64_t chunks, int64_t it,
+                                           int64_t in_lo, int64_t in_hi) {
+  const fntgpu_cdc_io& io = A.io;
+  const int s = (int)(it / chunks);
+  const int64_t g0 = (A.blk_begin + (it - (int64_t)s * chunks) * CDC_BLK) * CDC_HOP - CDC_HOP;
+  const uintptr_t pr = reinterpret_cast<uintptr_t>(reinterpret_cast<const int8_t*>(io.xr) +
+                                                   (size_t)s * io.x_stride + (g0 - io.x_first));
+  const uintptr_t pi = reinterpret_cast<uintptr_t>(reinterpret_cast<const int8_t*>(io.xi) +
+                                                   (size_t)s * io.x_stride + (g0 - io.x_first));
+  return CDC_TMA && g0 >= in_lo && g0 + WIN <= in_hi && ((pr | pi) & 15) == 0;
+}
+
+__device__ __forceinline__ void tc_issue_bulk(const CdcArgs& A, int64_t chunks, int64_t it,
+                                              int8_t* dst_r, int8_t* dst_i, uint32_t mb) {
+  const fntgpu_cdc_io& io = A.io;
+  const int s = (int)(it / chunks);
+  const int64_t g0 = (A.blk_begin + (it - (int64_t)s * chunks) * CDC_BLK) * CDC_HOP - CDC_HOP;
+  const int8_t* pr = reinterpret_cast<const int8_t*>(io.xr) + (size_t)s * io.x_stride + (g0 - io.x_first);
+  const int8_t* pi = reinterpret_cast<const int8_t*>(io.xi) + (size_t)s * io.x_stride + (g0 - io.x_first);
+  // the buffer was last read through the generic proxy (two items ago)
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" :: "r"(mb), "r"(2 * WIN) : "memory");
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+               :: "r"((uint32_t)__cvta_generic_to_shared(dst_r)), "l"(pr), "r"(WIN), "r"(mb) : "memory");
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+               :: "r"((uint32_t)__cvta_generic_to_shared(dst_i)), "l"(pi), "r"(WIN), "r"(mb) : "memory");
+}
+
+// Fast-path outputs straight from the inverse fragments (FAST preconditions of
+// cdc_epilogue_fast): this thread's outputs are local indices
+// idx = 32 bl + 8 j + 2 tig + e2 (bl = block row), as (re, im) pairs over e2.
+struct TcStats {
+  unsigned long long a2 = 0, b2 = 0, a4 = 0, b4 = 0;  // even (a) / odd (b) local indices
+  uint32_t a4h = 0, b4h = 0;
+};
+
+__device__ __forceinline__ void tc_store_pair(const CdcArgs& A, int s, int64_t base_o, int idx,
+                                              int lo, int hi, const int32_t (&zr)[2],
+                                              const int32_t (&zi)[2], TcStats& st) {
+  const fntgpu_cdc_io& io = A.io;
+  const bool v0 = idx >= lo && idx < hi, v1 = idx + 1 >= lo && idx + 1 < hi;
+  if (!(v0 | v1)) return;
+  const int64_t o = s * io.y_stride + base_o + idx;
+  if (io.out_dtype == FNTGPU_I16) {
+    int16_t* yr = reinterpret_cast<int16_t*>(io.yr) + o;
+    int16_t* yi = reinterpret_cast<int16_t*>(io.yi) + o;
+    if (v0 & v1) {
+      *reinterpret_cast<uint32_t*>(yr) = ((uint32_t)zr[0] & 0xffffu) | ((uint32_t)zr[1] << 16);
+      *reinterpret_cast<uint32_t*>(yi) = ((uint32_t)zi[0] & 0xffffu) | ((uint32_t)zi[1] << 16);
+    } else {
+      const int e = v0 ? 0 : 1;
+      yr[e] = (int16_t)zr[e];
+      yi[e] = (int16_t)zi[e];
+    }
+  }
+  if (CDC_PROBE != 1 && io.qr) {
+    const int k = io.q_shift, qmax = io.q_max;
+    const uint32_t qr0 = (uint32_t)requant_int(zr[0], k, io.q_tie, qmax) & 0xffu;
+    const uint32_t qr1 = (uint32_t)requant_int(zr[1], k, io.q_tie, qmax) & 0xffu;
+    const uint32_t qi0 = (uint32_t)requant_int(zi[0], k, io.q_tie, qmax) & 0xffu;
+    const uint32_t qi1 = (uint32_t)requant_int(zi[1], k, io.q_tie, qmax) & 0xffu;
+    int8_t* qr = io.qr + s * io.q_stride + base_o + idx;
+    int8_t* qi = io.qi + s * io.q_stride + base_o + idx;
+    if (v0 & v1) {
+      *reinterpret_cast<uint16_t*>(qr) = (uint16_t)(qr0 | (qr1 << 8));
+      *reinterpret_cast<uint16_t*>(qi) = (uint16_t)(qi0 | (qi1 << 8));
+    } else if (v0) {
+      qr[0] = (int8_t)qr0;
+      qi[0] = (int8_t)qi0;
+    } else {
+      qr[1] = (int8_t)qr1;
+      qi[1] = (int8_t)qi1;
+    }
+  }
+  if (CDC_PROBE != 2 && io.decim_acc) {
+    const uint32_t m0 = v0 ? (uint32_t)(zr[0] * zr[0]) + (uint32_t)(zi[0] * zi[0]) : 0u;  // <= 2^31
+    const uint32_t m1 = v1 ? (uint32_t)(zr[1] * zr[1]) + (uint32_t)(zi[1] * zi[1]) : 0u;
+    const unsigned long long q0 = (unsigned long long)m0 * m0, q1 = (unsigned long long)m1 * m1;
+    st.a2 += m0;
+    st.a4 += q0;
+    st.a4h += (st.a4 < q0);
+    st.b2 += m1;
+    st.b4 += q1;
+    st.b4h += (st.b4 < q1);
+  }
+}
+
+template <bool FAST>
+__global__ void __launch_bounds__(CDC_CTA, CDC_TC_MIN_CTAS) k_cdc64_tc(const __grid_constant__ CdcArgs A) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  TcTables& T = *reinterpret_cast<TcTables*>(smem);
+  uint32_t* s_u = reinterpret_cast<uint32_t*>(smem + sizeof(TcTables));  // generic epilogue only
+  __shared__ __align__(8) uint64_t mbar[2];
+  const uint32_t mb0 = (uint32_t)__cvta_generic_to_shared(&mbar[0]);
+
+  const fntgpu_cdc_io& io = A.io;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int g = lane >> 2, tig = lane & 3;
+  if (tid == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" :: "r"(mb0) : "memory");
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" :: "r"(mb0 + 8) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  tc_build_tables(T, A);  // ends with __syncthreads
+
+  const int64_t chunks = (A.blk_count + CDC_BLK - 1) / CDC_BLK;
+  const int64_t items = chunks * io.n_streams;
+  const int64_t in_lo = io.x_first > 0 ? io.x_first : 0;
+  const int64_t in_hi = io.x_first + io.x_count < io.length ? io.x_first + io.x_count : io.length;
+  uint32_t phase = 0;  // parity bit per buffer
+  int64_t it = blockIdx.x;
+  if (tid == 0 && it < items && tc_bulk_ok(A, chunks, it, in_lo, in_hi))
+    tc_issue_bulk(A, chunks, it, T.x[0][0], T.x[0][1], mb0);
+  for (int buf = 0; it < items; it += gridDim.x, buf ^= 1) {
+    const int s = (int)(it / chunks);
+    const int64_t cta_blk0 = A.blk_begin + (it - (int64_t)s * chunks) * CDC_BLK;
+    int8_t* s_xr = T.x[buf][0];
+    int8_t* s_xi = T.x[buf][1];
+    if (tc_bulk_ok(A, chunks, it, in_lo, in_hi)) {
+      uint32_t done = 0;
+      const uint32_t par = (phase >> buf) & 1u;
+      while (!done) {
+        asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+                     "selp.u32 %0, 1, 0, p;\n\t}" : "=r"(done) : "r"(mb0 + 8 * buf), "r"(par) : "memory");
       }
+      phase ^= 1u << buf;
+    } else {
+      const int64_t g0 = cta_blk0 * CDC_HOP - CDC_HOP;
+      stage_plane<int8_t, int8_t>(s_xr, reinterpret_cast<const int8_t*>(io.xr) + (size_t)s * io.x_stride, g0, io);
+      stage_plane<int8_t, int8_t>(s_xi, reinterpret_cast<const int8_t*>(io.xi) + (size_t)s * io.x_stride, g0, io);
+    }
+    __syncthreads();  // window visible; every warp is done with the other buffer (and s_u)
+    {
+      const int64_t nx = it + gridDim.x;
+      if (tid == 0 && nx < items && tc_bulk_ok(A, chunks, nx, in_lo, in_hi))
+        tc_issue_bulk(A, chunks, nx, T.x[buf ^ 1][0], T.x[buf ^ 1][1], mb0 + 8 * (buf ^ 1));
+    }
+
+    // ---- forward: X_r, X_i of the warp's 16 blocks, 16 bins at a time
+    bool flagged = false;
+#pragma unroll 1
+    for (int c = 0; c < 4; ++c) {
+      int p1r[2][4], p0r[2][4], p1i[2][4], p0i[2][4];
+      {
+        uint32_t ax[2][4];
+        // ldmatrix.x4: lanes 8q..8q+7 address the 16-byte rows of matrix q = (rows 0-7 |
+        // 8-15) x (K 0-15 | 16-31) of the M-tile; the result is the A quad in place
+        const int off = 32 * (16 * warp + (lane & 15)) + 16 * (lane >> 4);
+        ldsm_x4(ax[0], s_xr + off);
+        ldsm_x4(ax[1], s_xr + off + 32);
+#pragma unroll
+        for (int jj = 0; jj < 2; ++jj) {
+          const uint4 B0 = T.fwd[2 * c + jj][0][lane], B1 = T.fwd[2 * c + jj][1][lane];
+          mma_s8u8_z(p1r[jj], ax[0], B0.x, B0.y);
+          mma_s8s8_z(p0r[jj], ax[0], B0.z, B0.w);
+          mma_s8u8(p1r[jj], ax[1], B1.x, B1.y);
+          mma_s8s8(p0r[jj], ax[1], B1.z, B1.w);
+        }
+        ldsm_x4(ax[0], s_xi + off);
+        ldsm_x4(ax[1], s_xi + off + 32);
+#pragma unroll
+        for (int jj = 0; jj < 2; ++jj) {
+          const uint4 B0 = T.fwd[2 * c + jj][0][lane], B1 = T.fwd[2 * c + jj][1][lane];
+          mma_s8u8_z(p1i[jj], ax[0], B0.x, B0.y);
+          mma_s8s8_z(p0i[jj], ax[0], B0.z, B0.w);
+          mma_s8u8(p1i[jj], ax[1], B1.x, B1.y);
+          mma_s8s8(p0i[jj], ax[1], B1.z, B1.w);
+        }
+      }
+      // C fragment: e = 0, 1 row g, cols 2 tig, 2 tig + 1; e = 2, 3 row g + 8
+      uint32_t ws[2][4], wd[2][4];
+      uint32_t any = 0;
+#pragma unroll
+      for (int jj = 0; jj < 2; ++jj) {
+#pragma unroll
+        for (int e2 = 0; e2 < 2; ++e2) {
+          const uint4 be = T.beta[16 * c + 8 * jj + 2 * tig + e2];
+#pragma unroll
+          for (int r = 0; r < 2; ++r) {
+            const int e = 2 * r + e2;
+            const int32_t xr = p1r[jj][e] * 256 + p0r[jj][e];
+            const int32_t xi = p1i[jj][e] * 256 + p0i[jj][e];
+            ws[jj][e] = tc_w(xr, xi, be.x, be.y);
+            wd[jj][e] = tc_w(xr, xi, be.z, be.w);
+            any |= ws[jj][e] | wd[jj][e];
+          }
+        }
+      }
+      // A-fragment registers of inverse k-step c >> 1: K half c & 1 -> quad positions
+      // (0, 1) or (2, 3); stored for the inverse (shared memory keeps registers free)
+      {
+        uint32_t sl0, sh0, sl1, sh1, dl0, dh0, dl1, dh1;
+        tc_pack(ws[0][0], ws[0][1], ws[1][0], ws[1][1], sl0, sh0);
+        tc_pack(ws[0][2], ws[0][3], ws[1][2], ws[1][3], sl1, sh1);
+        tc_pack(wd[0][0], wd[0][1], wd[1][0], wd[1][1], dl0, dh0);
+        tc_pack(wd[0][2], wd[0][3], wd[1][2], wd[1][3], dl1, dh1);
+        const int ks = c >> 1, h = c & 1;
+        reinterpret_cast<uint2*>(&T.afr[warp][0][ks][0][lane])[h] = make_uint2(sl0, sl1);
+        reinterpret_cast<uint2*>(&T.afr[warp][0][ks][1][lane])[h] = make_uint2(sh0, sh1);
+        reinterpret_cast<uint2*>(&T.afr[warp][1][ks][0][lane])[h] = make_uint2(dl0, dl1);
+        reinterpret_cast<uint2*>(&T.afr[warp][1][ks][1][lane])[h] = make_uint2(dh0, dh1);
+      }
+      if (__any_sync(0xffffffffu, any & 0x10000u)) {
+        // rare (p ~ 2^-16 per value): record the bins whose value the bytes cannot hold
+        flagged = true;
+#pragma unroll
+        for (int jj = 0; jj < 2; ++jj)
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const int k = 16 * c + 8 * jj + 2 * tig + (e & 1), row = g + 8 * (e >> 1);
+            if (ws[jj][e] >> 16) atomicOr(&T.flags[warp][row][0][k >> 5], 1u << (k & 31));
+            if (wd[jj][e] >> 16) atomicOr(&T.flags[warp][row][1][k >> 5], 1u << (k & 31));
+          }
+      }
+    }
+    __syncwarp();  // afr (and flags) written by every lane
+    // ---- inverse, one output n-tile j at a time for z_re (from s) and z_im (from d)
+    const int64_t n0 = cta_blk0 * CDC_HOP - A.c;
+    int64_t lo64 = n0, hi64 = n0 + (int64_t)CDC_BLK * CDC_HOP;
+    const int64_t o_lo = io.out_first, o_hi = io.out_first + io.out_count;
+    lo64 = lo64 < o_lo ? o_lo : lo64;
+    hi64 = hi64 > o_hi ? o_hi : hi64;
+    const int lo = (int)(lo64 - n0), hi = (int)(hi64 - n0);
+    TcStats st;
+#pragma unroll 1
+    for (int j = 0; j < 4; ++j) {
+      int32_t zv[2][4];  // decoded z + 32768: [re | im][fragment element]
+#pragma unroll
+      for (int sd = 0; sd < 2; ++sd) {
+        int q11[4], qm[4], q00[4];
+#pragma unroll
+        for (int ks = 0; ks < 2; ++ks) {
+          const uint4 l4 = T.afr[warp][sd][ks][0][lane], h4 = T.afr[warp][sd][ks][1][lane];
+          const uint32_t aL[4] = {l4.x, l4.y, l4.z, l4.w}, aH[4] = {h4.x, h4.y, h4.z, h4.w};
+          const uint4 B = T.inv[ks][4 * sd + j][lane];
+          if (ks == 0) {
+            mma_s8u8_z(q11, aH, B.x, B.y);
+            mma_s8s8_z(qm, aH, B.z, B.w);
+            mma_s8s8_z(q00, aL, B.z, B.w);
+          } else {
+            mma_s8u8(q11, aH, B.x, B.y);
+            mma_s8s8(qm, aH, B.z, B.w);
+            mma_s8s8(q00, aL, B.z, B.w);
+          }
+          mma_s8u8(qm, aL, B.x, B.y);
+        }
+        if (flagged) {
+          // a flagged bin k carried value + 1: subtract its matrix column
+          const int E = sd ? TC_E_IM : TC_E_RE;
+#pragma unroll
+          for (int r = 0; r < 2; ++r) {
+            const int row = g + 8 * r;
+            for (int wd2 = 0; wd2 < 2; ++wd2) {
+              uint32_t bits = T.flags[warp][row][sd][wd2];
+              while (bits) {
+                const int k = 32 * wd2 + __ffs(bits) - 1;
+                bits &= bits - 1;
+#pragma unroll
+                for (int e2 = 0; e2 < 2; ++e2) {
+                  const int m = 32 + 8 * j + 2 * tig + e2;
+                  q00[2 * r + e2] -= (int32_t)T.root[(E - m * k) & 63];
+                }
+              }
+            }
+          }
+        }
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          // z == 256 Qmid + Q00 - Q11 (|z| < 2^30): canonical residue + 32768, decoded
+          // by subtracting 32768 (fermat.py:131-133)
+          const int32_t z = qm[e] * 256 + q00[e] - q11[e];
+          zv[sd][e] = (int32_t)f4_mod((uint32_t)(z + (int32_t)(F4 * 16384u)) + 32768u);
+        }
+      }
+#pragma unroll
+      for (int r = 0; r < 2; ++r) {
+        const int bl = 16 * warp + g + 8 * r;
+        if (FAST) {
+          const int32_t zr2[2] = {zv[0][2 * r] - 32768, zv[0][2 * r + 1] - 32768};
+          const int32_t zi2[2] = {zv[1][2 * r] - 32768, zv[1][2 * r + 1] - 32768};
+          tc_store_pair(A, s, n0 - io.out_first, 32 * bl + 8 * j + 2 * tig, lo, hi, zr2, zi2, st);
+        } else {
+          uint32_t* u = s_u + bl * UP + 8 * j + 2 * tig;
+          *reinterpret_cast<uint2*>(u) = make_uint2((uint32_t)zv[0][2 * r], (uint32_t)zv[0][2 * r + 1]);
+          *reinterpret_cast<uint2*>(u + CDC_BLK * UP) = make_uint2((uint32_t)zv[1][2 * r], (uint32_t)zv[1][2 * r + 1]);
+        }
+      }
+    }
+    if (flagged) {
+      __syncwarp();
+      for (int i = lane; i < 64; i += 32) (&T.flags[warp][0][0][0])[i] = 0u;
+    }
+    if (FAST) {
+      if (io.decim_acc) {
+        // exact integer statistics per phase: warp-reduce 32-bit limbs, one atomic per value
+        const int pa = (int)(n0 & 1);  // even local indices carry phase n0 & 1
+        const unsigned long long va[4] = {st.a2, st.a4 & 0xffffffffull, st.a4 >> 32, st.a4h};
+        const unsigned long long vb[4] = {st.b2, st.b4 & 0xffffffffull, st.b4 >> 32, st.b4h};
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          unsigned long long x = va[q], y = vb[q];
+#pragma unroll
+          for (int off = 16; off > 0; off >>= 1) {
+            x += __shfl_xor_sync(0xffffffffu, x, off);
+            y += __shfl_xor_sync(0xffffffffu, y, off);
+          }
+          if (lane == 0) {
+            if (x) atomicAdd(io.decim_acc + ((int64_t)s * 2 + pa) * 4 + q, x);
+            if (y) atomicAdd(io.decim_acc + ((int64_t)s * 2 + (pa ^ 1)) * 4 + q, y);
+          }
+        }
+      }
+    } else {
+      __syncthreads();
+      cdc_epilogue_generic<true>(A, s_u, s, n0, lo64, hi64);
     }
   }
 }
@@ -482,11 +964,40 @@ static cudaError_t launch_k(const CdcArgs& A, dim3 grid, cudaStream_t st) {
   return cudaGetLastError();
 }
 
+template <bool FAST>
+static cudaError_t launch_tc(const CdcArgs& A, cudaStream_t st) {
+  constexpr int SMEM = (int)sizeof(TcTables) + (FAST ? 0 : 2 * CDC_BLK * UP * 4);
+  auto* k = k_cdc64_tc<FAST>;
+  static int grid_per_sm[2] = {0, 0};  // resident CTAs per SM (persistent grid)
+  static int sms = 0;
+  int& per_sm = grid_per_sm[FAST ? 1 : 0];
+  if (per_sm == 0) {
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
+    if (e != cudaSuccess) return e;
+    int dev = 0;
+    e = cudaGetDevice(&dev);
+    if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    int n = 0;
+    if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k, CDC_CTA, SMEM);
+    if (e != cudaSuccess) return e;
+    per_sm = n > 0 ? n : 1;
+  }
+  const int64_t items = (A.blk_count + CDC_BLK - 1) / CDC_BLK * A.io.n_streams;
+  const int64_t full = (int64_t)per_sm * sms;
+  const unsigned grid = (unsigned)(items < full ? items : full);
+  k<<<grid, CDC_CTA, SMEM, st>>>(A);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_cdc64(const fntgpu_cdc_taps& taps, const fntgpu_cdc_io& io, cudaStream_t st) {
   if (io.out_count <= 0 || io.n_streams <= 0) return cudaSuccess;
   CdcArgs A;
   scale_taps(taps.b_plus, A.bp);
   scale_taps(taps.b_minus, A.bm);
+  for (int k = 0; k < CDC_N; ++k) {
+    A.rbp[k] = taps.b_plus[k] % F4;
+    A.rbm[k] = taps.b_minus[k] % F4;
+  }
   A.io = io;
   A.c = taps.n_taps / 2;
   // blocks B needed for outputs n in [out_first, out_first+out_count): B = (n + c) / 32
@@ -506,6 +1017,13 @@ cudaError_t launch_cdc64(const fntgpu_cdc_taps& taps, const fntgpu_cdc_io& io, c
            (reinterpret_cast<uintptr_t>(io.yi) & 7) == 0 && io.y_stride % 4 == 0;
   if (io.in_dtype != FNTGPU_I8 && io.in_dtype != FNTGPU_I32 && io.in_dtype != FNTGPU_I64)
     return cudaErrorInvalidValue;
+  // tensor-core form on request (fntgpu_cdc_taps.kernel), for int8 planes (their samples
+  // are the int8 MMA operands). Auto keeps the shift-add kernel: measured faster on B200
+  // (config 5 CDC 33.0 vs 36.4 ms, config 4 26.0 vs 28.7 ms; profiles/cdc_tc_r01.json)
+  if (io.in_dtype == FNTGPU_I8 && taps.kernel == FNTGPU_CDC_KERNEL_TC) {
+    A.s_base = 0;
+    return fast ? launch_tc<true>(A, st) : launch_tc<false>(A, st);
+  }
   for (int64_t s0 = 0; s0 < io.n_streams; s0 += 65535) {
     A.s_base = (int32_t)s0;
     grid.y = (unsigned)(io.n_streams - s0 < 65535 ? io.n_streams - s0 : 65535);

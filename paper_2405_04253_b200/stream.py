@@ -50,8 +50,11 @@ class CdcBank:
         if not engine._fast():
             raise NotImplementedError("CdcBank runs the cdc64 plan")
         self.engine = engine
-        self.taps = engine.c_taps()
         self.inv_scale = 1.0 / engine.output_scale
+
+    @property
+    def taps(self):
+        return self.engine.c_taps()  # current kernel selection (cdc.set_cdc_kernel)
 
     def _exact_requant(self, io, q_spec) -> None:
         """Integer requantization when (y * (1/output_scale)) * q_scale == y / 2^k up to

@@ -175,6 +175,16 @@ def test_encode_decode_arrays():
 
 # ----------------------------------------------------------------------- CDC
 
+@pytest.fixture(params=("tc", "shift"))
+def cdc_kernel(request):
+    """Run a CDC test through both kernels: the tensor-core matrix form (int8 planes)
+    and the shift-add butterfly kernel (cdc.set_cdc_kernel)."""
+    from paper_2405_04253_b200 import cdc as cdc_mod
+    prev = cdc_mod.set_cdc_kernel(request.param)
+    yield request.param
+    cdc_mod.set_cdc_kernel(prev)
+
+
 def _c2_engine():
     cfg = P.LinkConfig(n_symbols=2 ** 18, z_km=75.0, snr_db=(20.0,), pol_rotation_deg=0.0,
                        dgd_symbols=0.0, iq_skew_samples=0.0, seed=1)
@@ -193,7 +203,7 @@ def test_cdc_engine_constants(golden, digests):
     assert eng.support_warning == d["c2_support_warning"]
 
 
-def test_cdc_config2_full(golden, digests):
+def test_cdc_config2_full(golden, digests, cdc_kernel):
     """BASELINE config 2 (2^19 samples, 75 km, 20 dB) bit-exact vs the reference."""
     a = golden("cdc")
     eng = _c2_engine()
@@ -210,7 +220,7 @@ def test_cdc_config2_full(golden, digests):
     assert y.dtype == np.complex128 and sha(y) == digests["cdc"]["c2_process"]
 
 
-def test_cdc_edges(golden):
+def test_cdc_edges(golden, cdc_kernel):
     a = golden("cdc")
     eng = _c2_engine()
     for L in (0, 1, 2, 15, 16, 17, 31, 32, 33, 63, 64, 65, 97, 1000, 4097):
@@ -225,7 +235,7 @@ def test_cdc_edges(golden):
         eng.process_int(np.full(10, 40000), np.zeros(10))
 
 
-def test_cdc_more_streams_than_one_grid_dimension():
+def test_cdc_more_streams_than_one_grid_dimension(cdc_kernel):
     """70 000 short streams in one call (the launcher splits grid.y at 65 535)."""
     import torch
     from paper_2405_04253_b200.stream import CdcBank
@@ -242,7 +252,7 @@ def test_cdc_more_streams_than_one_grid_dimension():
         assert np.array_equal(yr[s].cpu().numpy(), orr) and np.array_equal(yi[s].cpu().numpy(), oi), s
 
 
-def test_cdc_int8_full_range_vs_oracle():
+def test_cdc_int8_full_range_vs_oracle(cdc_kernel):
     """int8 planes over their whole range (the kernel's carry-free first stages
     assume |x_r +- 2^8 x_i| <= 32896) and wrapping outputs, against the oracle."""
     import torch
@@ -265,13 +275,48 @@ def test_cdc_int8_full_range_vs_oracle():
         assert np.array_equal(yi[s].cpu().numpy(), oi), s
 
 
+def test_cdc_tc_unrepresentable_residue():
+    """Tap spectra chosen so that s = u+ + u- hits 32640 on every bin of one block: the
+    one residue two signed bytes cannot hold in the tensor-core form (corrected after
+    the MMAs, tests/test_tc_math.py); both kernels against the numpy oracle."""
+    import torch
+    from paper_2405_04253_b200 import cdc as cdc_mod
+    from paper_2405_04253_b200.stream import CdcBank
+    from oracle import np_port as N
+    F = 65537
+    eng = _c2_engine()
+    rng = np.random.default_rng(21)
+    S, L = 2, 4096
+    xr = rng.integers(-128, 128, (S, L)).astype(np.int8)
+    xi = rng.integers(-128, 128, (S, L)).astype(np.int8)
+    blk = 40  # window of block 40 = samples [32 * 40 - 32, 32 * 40 + 32)
+    wr = xr[0, 32 * blk - 32: 32 * blk + 32].astype(np.int64)
+    wi = xi[0, 32 * blk - 32: 32 * blk + 32].astype(np.int64)
+    ap = (N.transform(N.CDC64, N._enc(wr, F)) + 256 * N.transform(N.CDC64, N._enc(wi, F))) % F
+    bp = np.array([32640 * pow(int(a), -1, F) % F if a else 1 for a in ap], dtype=np.int64)
+    bm = np.zeros(64, dtype=np.int64)
+    eng._b_plus, eng._b_minus, eng._taps_c = bp, bm, None
+    want = [N.cdc_process_int(xr[s].astype(np.int64), xi[s].astype(np.int64), bp, bm, 32) for s in range(S)]
+    for kern in ("tc", "shift"):
+        prev = cdc_mod.set_cdc_kernel(kern)
+        try:
+            yr = torch.empty((S, L), dtype=torch.int32, device="cuda")
+            yi = torch.empty_like(yr)
+            CdcBank(eng).run(torch.from_numpy(xr).cuda(), torch.from_numpy(xi).cuda(), length=L, yr=yr, yi=yi)
+        finally:
+            cdc_mod.set_cdc_kernel(prev)
+        for s in range(S):
+            assert np.array_equal(yr[s].cpu().numpy(), want[s][0]), (kern, s)
+            assert np.array_equal(yi[s].cpu().numpy(), want[s][1]), (kern, s)
+
+
 @pytest.mark.parametrize("tag,cfg", [
     ("t33", dict(z_km=25.0, fs_hz=80e9, n_taps=33)),
     ("z0", dict(z_km=0.0, fs_hz=80e9, n_taps=32)),
     ("t17", dict(z_km=10.0, fs_hz=80e9, n_taps=17)),
     ("t1", dict(z_km=5.0, fs_hz=80e9, n_taps=1)),
 ])
-def test_cdc_other_tap_designs(golden, tag, cfg):
+def test_cdc_other_tap_designs(golden, tag, cfg, cdc_kernel):
     a = golden("cdc")
     eng = P.FntCdcEngine(P.CdcConfig(**cfg), P.QuantSpec(5, 8.0))
     assert np.array_equal(eng.tap_re, a[f"{tag}_tap_re"]) and eng.tap_scale == float(a[f"{tag}_scale"])
@@ -284,7 +329,7 @@ def test_cdc_budget_error():
         P.FntCdcEngine(P.CdcConfig(z_km=0.0, fs_hz=80e9, n_taps=32), P.QuantSpec(12, 8.0))
 
 
-def test_cdc_bank_ranges_match_full_stream():
+def test_cdc_bank_ranges_match_full_stream(cdc_kernel):
     """Range shards with the 15/16-sample halo reproduce the full stream
     (SURVEY 8e), through the device-resident multi-stream API."""
     import torch
@@ -550,7 +595,7 @@ def test_aeq_bank_other_parameters_vs_oracle(case):
 
 # ------------------------------------------------------- CDC -> AEQ glue chain
 
-def test_chain_matches_reference_glue(golden):
+def test_chain_matches_reference_glue(golden, cdc_kernel):
     """CDC (fused requantization + decimation statistics) -> phase -> AEQ on the
     75 km / 45 deg link of fixture b: phase, requantized AEQ input and the AEQ
     outputs equal the reference's rx_frontend + run_single glue."""

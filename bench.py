@@ -303,7 +303,7 @@ def main():
     ap.add_argument("--c4-samples", type=int, default=1 << 31, help="C4 samples per polarization")
     ap.add_argument("--no-alt", action="store_true", help="skip the direct-forward AEQ comparison")
     ap.add_argument("--no-quality", action="store_true", help="skip the on-device BER/EVM scoring")
-    ap.add_argument("--cdc-kernel", default="auto", choices=["auto", "tc", "shift"],
+    ap.add_argument("--cdc-kernel", default="auto", choices=["auto", "umma", "tc", "shift"],
                     help="FNT-CDC kernel for the int8 planes: shift-add butterflies (auto/shift) "
                          "or the tensor-core split-integer matrix form (tc)")
     args = ap.parse_args()
@@ -573,7 +573,7 @@ def time_cdc_kernels(run, reps: int, world: int) -> dict:
     out = {}
     prev = cdc_mod.set_cdc_kernel("tc")
     try:
-        for name in ("tc", "shift"):
+        for name in ("umma", "tc", "shift"):
             cdc_mod.set_cdc_kernel(name)
             run()
             torch.cuda.synchronize()
@@ -592,9 +592,11 @@ def time_cdc_kernels(run, reps: int, world: int) -> dict:
     finally:
         cdc_mod.set_cdc_kernel(prev)
     out["speedup_tc"] = out["shift_ms"] / out["tc_ms"]
-    out["note"] = ("k_cdc64_tc: forward FNT-64 and pruned inverse as split-integer int8 matrix "
-                   "products (mma.sync IMMA.16832); k_cdc64: radix-sqrt2 shift-add butterflies. "
-                   "Bit-identical outputs (tests/test_gpu_parity.py)")
+    out["speedup_umma"] = out["shift_ms"] / out["umma_ms"]
+    out["note"] = ("k_cdc64_umma / k_cdc64_tc: forward FNT-64 and pruned inverse as split-integer "
+                   "int8 matrix products on tcgen05 (UTCIMMA, TMEM accumulators) / mma.sync "
+                   "(IMMA.16832); k_cdc64: radix-sqrt2 shift-add butterflies. Bit-identical "
+                   "outputs (tests/test_gpu_parity.py)")
     return out
 
 

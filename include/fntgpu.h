@@ -121,11 +121,13 @@ typedef struct fntgpu_cdc_taps {
   int32_t n_taps;       /* output alignment c = n_taps // 2 (cdc.py:174) */
   int32_t kernel;       /* FNTGPU_CDC_KERNEL_*: 0 auto (= shift-add, measured faster),
                          * 1 shift-add FNT kernel, 2 tensor-core split-integer matrix
-                         * form (int8 planes; other dtypes run the shift-add kernel) */
+                         * form on mma.sync, 3 the same on tcgen05 (int8 planes; other
+                         * dtypes run the shift-add kernel) */
 } fntgpu_cdc_taps;
 #define FNTGPU_CDC_KERNEL_AUTO 0
 #define FNTGPU_CDC_KERNEL_SHIFT 1
 #define FNTGPU_CDC_KERNEL_TC 2
+#define FNTGPU_CDC_KERNEL_UMMA 3
 
 typedef struct fntgpu_cdc_io {
   int32_t n_streams;          /* independent streams (polarizations / channels) */

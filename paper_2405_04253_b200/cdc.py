@@ -116,7 +116,7 @@ def _device_dtype(a: np.ndarray, half: int) -> np.dtype:
 # shift-add butterfly kernel ("auto"/"shift", measured faster on B200) or the
 # tensor-core split-integer matrix form of the FNT ("tc"). Both are bit-exact; other
 # input dtypes always take the shift-add kernel.
-CDC_KERNELS = {"auto": 0, "shift": 1, "tc": 2}
+CDC_KERNELS = {"auto": 0, "shift": 1, "tc": 2, "umma": 3}
 _cdc_kernel = os.environ.get("FNTGPU_CDC_KERNEL", "auto")
 if _cdc_kernel not in CDC_KERNELS:
     raise ValueError(f"FNTGPU_CDC_KERNEL must be one of {sorted(CDC_KERNELS)}")

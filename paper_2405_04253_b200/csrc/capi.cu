@@ -267,7 +267,7 @@ int fntgpu_struct_sizes(int64_t* out, int n) {
 
 int fntgpu_cdc64_process(const fntgpu_cdc_taps* taps, const fntgpu_cdc_io* io, void* stream) {
   if (!taps || !io) return fail(FNTGPU_EINVAL, "cdc64_process: NULL argument");
-  if (taps->kernel < FNTGPU_CDC_KERNEL_AUTO || taps->kernel > FNTGPU_CDC_KERNEL_TC)
+  if (taps->kernel < FNTGPU_CDC_KERNEL_AUTO || taps->kernel > FNTGPU_CDC_KERNEL_UMMA)
     return fail(FNTGPU_EINVAL, "cdc64_process: unknown kernel selector %d", taps->kernel);
   if (taps->n_taps < 1 || taps->n_taps > 33)
     return fail(FNTGPU_EINVAL, "n_taps=%d exceeds overlap-save validity 33 for block_n=64", taps->n_taps);

@@ -18,6 +18,8 @@
 // of int8 planes) or 16-byte vector loads; one HBM read per input sample (the
 // 32-sample halo between neighbouring blocks is re-read from shared memory) and
 // one HBM write per output.
+#include <cstdio>
+#include <cstdlib>
 #include <type_traits>
 
 #include "fermat.cuh"
@@ -921,6 +923,359 @@ __global__ void __launch_bounds__(CDC_CTA, CDC_TC_MIN_CTAS) k_cdc64_tc(const __g
   }
 }
 
+// ---------------------------------------------------------------------------------
+// tcgen05 form of the split-integer matrix FNT-CDC (the same algorithm as
+// k_cdc64_tc, tests/test_tc_math.py): the MMAs run asynchronously on the 5th-generation
+// tensor cores (tcgen05.mma kind::i8, M = 128 blocks per CTA tile, operands in shared
+// memory, int32 accumulators in tensor memory) issued by one thread; all 8 warps run
+// the CUDA-core stages in between and read the accumulators back with tcgen05.ld (a
+// warp sees the 32 TMEM lanes = 32 blocks of its lane quarter; warps w and w + 4 split
+// the columns). Per 128-block item:
+//   relayout  window -> x_r, x_i as K-major canonical operands (8-row x 16-byte core
+//             matrices; overlapping windows cannot be addressed by a descriptor)
+//   MMA 1     P1r, P0r, P1i, P0i = x_{r,i} [T1 | T0]          (8 x N=64, TMEM cols 0-255)
+//   stage 1   X = 256 P1 + P0, s/d products with the tap spectra, limb bytes -> smem
+//   MMA 2     Q11, Qmid, Q00 of z_re (from s) and z_im (from d) (16 x N=32, cols 0-191)
+//   stage 2   z = 256 Qmid + Q00 - Q11 mod F4, decode, outputs / requantization / stats
+#ifndef CDC_UMMA_MIN_CTAS
+#define CDC_UMMA_MIN_CTAS 2
+#endif
+constexpr int UM_ROWS = CDC_BLK;  // 128 blocks = MMA M
+constexpr uint32_t UM_TMEM_COLS = 256;
+
+struct UmmaSmem {
+  uint8_t ax[2][UM_ROWS * 64];       // x_r, x_i windows, canonical K-major [128 x 64 B]
+  uint8_t ai[4][UM_ROWS * 64];       // inverse A: s lo, s hi, d lo, d hi limbs [128 x 64 B]
+  uint8_t bf[2][CDC_N * 64];         // forward B: T1 (u8), T0 (s8) [64 bins x 64 samples]
+  uint8_t bi[4][32 * 64];            // inverse B: M_re t1, M_re t0, M_im t1, M_im t0 [32 x 64 bins]
+  uint4 beta[CDC_N];
+  uint32_t root[CDC_N];
+  uint32_t flags[UM_ROWS][2][2];     // [row][s|d][bin half]: w == 65536 bits (rare path)
+  int8_t x[2][2][WIN];               // input windows [buffer][re|im] (TMA double buffer)
+  uint64_t mbar_x[2];
+  uint64_t mbar_mma;
+  uint32_t tmem_base;
+};
+
+// canonical K-major, no swizzle: 8-row x 16-byte core matrices; LBO = 128 B between the
+// two K-adjacent core matrices of one MMA (K = 32 bytes), SBO = 512 B between row groups
+__host__ __device__ constexpr int um_off(int row, int kb) {
+  return (row >> 3) * 512 + (kb >> 4) * 128 + (row & 7) * 16 + (kb & 15);
+}
+__device__ __forceinline__ uint64_t um_desc(const void* p) {
+  const uint32_t a = (uint32_t)__cvta_generic_to_shared(p);
+  return (uint64_t)((a >> 4) & 0x3FFF) | ((uint64_t)(128 >> 4) << 16) | ((uint64_t)(512 >> 4) << 32) |
+         (1ull << 46);  // version 1 (sm_100), base offset 0, layout SWIZZLE_NONE
+}
+// instruction descriptor: kind::i8, S32 accumulate, K-major A and B, M = 128
+__host__ __device__ constexpr uint32_t um_idesc(int n, bool a_signed, bool b_signed) {
+  return (2u << 4) | ((a_signed ? 1u : 0u) << 7) | ((b_signed ? 1u : 0u) << 10) |
+         ((uint32_t)(n >> 3) << 17) | ((uint32_t)(UM_ROWS >> 4) << 24);
+}
+__device__ __forceinline__ void um_mma(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc, bool acc) {
+  asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+               "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}"
+               :: "r"(d_tmem), "l"(a), "l"(b), "r"(idesc), "r"((uint32_t)acc));
+}
+__device__ __forceinline__ void um_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];"
+               :: "r"((uint32_t)__cvta_generic_to_shared(bar)) : "memory");
+}
+__device__ __forceinline__ void um_wait(uint64_t* bar, uint32_t parity) {
+  const uint32_t mb = (uint32_t)__cvta_generic_to_shared(bar);
+  uint32_t done = 0;
+  while (!done) {
+    asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+                 "selp.u32 %0, 1, 0, p;\n\t}" : "=r"(done) : "r"(mb), "r"(parity) : "memory");
+  }
+}
+__device__ __forceinline__ void um_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void um_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+// 8 consecutive TMEM columns of this thread's lane
+__device__ __forceinline__ void um_ld8(uint32_t addr, int32_t (&v)[8]) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
+               : "r"(addr));
+}
+__device__ __forceinline__ void um_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+// Registers written by tcgen05.ld are defined only after tcgen05.wait::ld: this empty
+// volatile asm (after the wait) "redefines" them, so no use can be scheduled earlier.
+__device__ __forceinline__ void um_ld_fence(int32_t (&v)[8]) {
+  asm volatile("" : "+r"(v[0]), "+r"(v[1]), "+r"(v[2]), "+r"(v[3]), "+r"(v[4]), "+r"(v[5]), "+r"(v[6]), "+r"(v[7]));
+}
+
+__device__ void um_build_tables(UmmaSmem& S, const CdcArgs& A) {
+  const int tid = threadIdx.x;
+  if (tid < CDC_N) {
+    const int h = tid >> 1;
+    const uint32_t p2 = h < 16 ? (1u << h) : F4 - (1u << (h - 16));
+    S.root[tid] = (tid & 1) ? (uint32_t)(((uint64_t)p2 * 4080u) % F4) : p2;
+    const uint64_t bp = A.rbp[tid] % F4, bm = A.rbm[tid] % F4;
+    const uint64_t sum = (bp + bm) % F4, dif = (bp + F4 - bm) % F4;
+    S.beta[tid] = make_uint4((uint32_t)sum, (uint32_t)(256 * dif % F4), (uint32_t)dif, (uint32_t)(256 * sum % F4));
+  }
+  __syncthreads();
+  // forward B: row = bin k, K byte = window sample n, entry alpha^(nk)
+  for (int i = tid; i < CDC_N * 64; i += blockDim.x) {
+    const int k = i >> 6, n = i & 63;
+    const uint2 l = tc_limbs(S.root[(n * k) & 63]);
+    S.bf[0][um_off(k, n)] = (uint8_t)l.x;
+    S.bf[1][um_off(k, n)] = (uint8_t)l.y;
+  }
+  // inverse B: row = kept output m - 32, K byte = bin k; c_re N^-1 alpha^(-mk), c_im N^-1 alpha^(-mk)
+  for (int i = tid; i < 32 * 64; i += blockDim.x) {
+    const int mo = i >> 6, k = i & 63, m = 32 + mo;
+    const uint2 lr = tc_limbs(S.root[(TC_E_RE - m * k) & 63]);
+    const uint2 li = tc_limbs(S.root[(TC_E_IM - m * k) & 63]);
+    S.bi[0][um_off(mo, k)] = (uint8_t)lr.x;
+    S.bi[1][um_off(mo, k)] = (uint8_t)lr.y;
+    S.bi[2][um_off(mo, k)] = (uint8_t)li.x;
+    S.bi[3][um_off(mo, k)] = (uint8_t)li.y;
+  }
+}
+
+template <bool FAST>
+__global__ void __launch_bounds__(CDC_CTA, CDC_UMMA_MIN_CTAS) k_cdc64_umma(const __grid_constant__ CdcArgs A) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  UmmaSmem& S = *reinterpret_cast<UmmaSmem*>(smem);
+  uint32_t* s_u = reinterpret_cast<uint32_t*>(smem + sizeof(UmmaSmem));  // generic epilogue only
+  const fntgpu_cdc_io& io = A.io;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int row = 32 * (warp & 3) + lane;  // TMEM lane = block row of the item
+  const int half = warp >> 2;              // column half this warp reads
+  const uint32_t mbx = (uint32_t)__cvta_generic_to_shared(&S.mbar_x[0]);
+
+  if (tid == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" :: "r"(mbx) : "memory");
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" :: "r"(mbx + 8) : "memory");
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" :: "r"((uint32_t)__cvta_generic_to_shared(&S.mbar_mma)) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;"
+                 :: "r"((uint32_t)__cvta_generic_to_shared(&S.tmem_base)), "n"(UM_TMEM_COLS) : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  um_build_tables(S, A);
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // tables are MMA operands
+  um_fence_before();
+  __syncthreads();
+  um_fence_after();
+  const uint32_t tmem = S.tmem_base;
+  const uint32_t tlane = tmem + ((uint32_t)(32 * (warp & 3)) << 16);
+
+  const int64_t chunks = (A.blk_count + CDC_BLK - 1) / CDC_BLK;
+  const int64_t items = chunks * io.n_streams;
+  const int64_t in_lo = io.x_first > 0 ? io.x_first : 0;
+  const int64_t in_hi = io.x_first + io.x_count < io.length ? io.x_first + io.x_count : io.length;
+  uint32_t xphase = 0, mphase = 0;
+  int64_t it = blockIdx.x;
+  if (tid == 0 && it < items && tc_bulk_ok(A, chunks, it, in_lo, in_hi))
+    tc_issue_bulk(A, chunks, it, S.x[0][0], S.x[0][1], mbx);
+  for (int buf = 0; it < items; it += gridDim.x, buf ^= 1) {
+    const int s = (int)(it / chunks);
+    const int64_t cta_blk0 = A.blk_begin + (it - (int64_t)s * chunks) * CDC_BLK;
+    int8_t* s_xr = S.x[buf][0];
+    int8_t* s_xi = S.x[buf][1];
+    if (tc_bulk_ok(A, chunks, it, in_lo, in_hi)) {
+      um_wait(&S.mbar_x[buf], (xphase >> buf) & 1u);
+      xphase ^= 1u << buf;
+    } else {
+      const int64_t g0 = cta_blk0 * CDC_HOP - CDC_HOP;
+      stage_plane<int8_t, int8_t>(s_xr, reinterpret_cast<const int8_t*>(io.xr) + (size_t)s * io.x_stride, g0, io);
+      stage_plane<int8_t, int8_t>(s_xi, reinterpret_cast<const int8_t*>(io.xi) + (size_t)s * io.x_stride, g0, io);
+    }
+    __syncthreads();  // window visible; all threads done with the other buffer
+    {
+      const int64_t nx = it + gridDim.x;
+      if (tid == 0 && nx < items && tc_bulk_ok(A, chunks, nx, in_lo, in_hi))
+        tc_issue_bulk(A, chunks, nx, S.x[buf ^ 1][0], S.x[buf ^ 1][1], mbx + 8 * (buf ^ 1));
+    }
+    // ---- relayout: row b, 16-byte chunk q of plane p <- window bytes [32 b + 16 q, + 16)
+#pragma unroll
+    for (int i = tid; i < 2 * UM_ROWS * 4; i += CDC_CTA) {
+      const int p = i >> 9, b = (i >> 2) & 127, q = i & 3;
+      const uint4 v = *reinterpret_cast<const uint4*>((p ? s_xi : s_xr) + 32 * b + 16 * q);
+      *reinterpret_cast<uint4*>(&S.ax[p][um_off(b, 16 * q)]) = v;
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    um_fence_before();
+    __syncthreads();  // operands written; previous item's TMEM reads complete
+    um_fence_after();
+    if (tid == 0) {
+      // MMA 1: cols 64 (2 p + l) + bin, l = 0: T1 (u8), 1: T0 (s8)
+#pragma unroll
+      for (int p = 0; p < 2; ++p)
+#pragma unroll
+        for (int l = 0; l < 2; ++l)
+#pragma unroll
+          for (int ks = 0; ks < 2; ++ks)
+            um_mma(tmem + 64 * (2 * p + l), um_desc(&S.ax[p][256 * ks]), um_desc(&S.bf[l][256 * ks]),
+                   um_idesc(64, true, l == 1), ks > 0);
+      um_commit(&S.mbar_mma);
+    }
+    um_wait(&S.mbar_mma, mphase);
+    mphase ^= 1u;
+    um_fence_after();
+    // ---- stage 1: this thread's row, bins [32 half, 32 half + 32), 8 at a time; the
+    // TMEM loads of the next 8 bins are in flight while these are computed
+    uint32_t fl_s = 0, fl_d = 0;  // w == 65536 bits per bin (rare)
+    int32_t acc[2][4][8];
+#pragma unroll
+    for (int gq = 0; gq < 4; ++gq) um_ld8(tlane + 64 * gq + 32 * half, acc[0][gq]);
+    um_ld_wait();
+#pragma unroll
+    for (int c8 = 0; c8 < 4; ++c8) {
+      int32_t (&cur)[4][8] = acc[c8 & 1];
+#pragma unroll
+      for (int gq = 0; gq < 4; ++gq) um_ld_fence(cur[gq]);
+      if (c8 < 3) {
+#pragma unroll
+        for (int gq = 0; gq < 4; ++gq) um_ld8(tlane + 64 * gq + 32 * half + 8 * (c8 + 1), acc[(c8 + 1) & 1][gq]);
+      }
+      const int k0 = 32 * half + 8 * c8;
+      uint32_t ws[8], wd[8];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        const uint4 be = S.beta[k0 + e];
+        const int32_t xr = cur[0][e] * 256 + cur[1][e];
+        const int32_t xi = cur[2][e] * 256 + cur[3][e];
+        ws[e] = tc_w(xr, xi, be.x, be.y);
+        wd[e] = tc_w(xr, xi, be.z, be.w);
+        fl_s |= (ws[e] >> 16) << (8 * c8 + e);
+        fl_d |= (wd[e] >> 16) << (8 * c8 + e);
+      }
+      // limb bytes (w ^ 0x80 per byte): 8 bins = 8 contiguous bytes of the K-major row
+      uint32_t sl[2], sh[2], dl[2], dh[2];
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        tc_pack(ws[4 * q], ws[4 * q + 1], ws[4 * q + 2], ws[4 * q + 3], sl[q], sh[q]);
+        tc_pack(wd[4 * q], wd[4 * q + 1], wd[4 * q + 2], wd[4 * q + 3], dl[q], dh[q]);
+      }
+      const int o = um_off(row, k0);
+      *reinterpret_cast<uint2*>(&S.ai[0][o]) = make_uint2(sl[0], sl[1]);
+      *reinterpret_cast<uint2*>(&S.ai[1][o]) = make_uint2(sh[0], sh[1]);
+      *reinterpret_cast<uint2*>(&S.ai[2][o]) = make_uint2(dl[0], dl[1]);
+      *reinterpret_cast<uint2*>(&S.ai[3][o]) = make_uint2(dh[0], dh[1]);
+      if (c8 < 3) um_ld_wait();
+    }
+    S.flags[row][0][half] = fl_s;
+    S.flags[row][1][half] = fl_d;
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    um_fence_before();
+    __syncthreads();  // inverse operands written; MMA-1 accumulators consumed
+    um_fence_after();
+    if (tid == 0) {
+      // MMA 2: z_re from s (A = ai 0/1, B = bi 0/1), z_im from d (ai 2/3, bi 2/3);
+      // cols 96 sd + {0: Q11, 32: Qmid, 64: Q00} + output
+#pragma unroll
+      for (int sd = 0; sd < 2; ++sd) {
+        const uint32_t d0 = tmem + 96 * sd;
+#pragma unroll
+        for (int ks = 0; ks < 2; ++ks) {
+          const uint64_t aL = um_desc(&S.ai[2 * sd][256 * ks]), aH = um_desc(&S.ai[2 * sd + 1][256 * ks]);
+          const uint64_t b1 = um_desc(&S.bi[2 * sd][256 * ks]), b0 = um_desc(&S.bi[2 * sd + 1][256 * ks]);
+          um_mma(d0 + 0, aH, b1, um_idesc(32, true, false), ks > 0);   // Q11 += hi x t1
+          um_mma(d0 + 32, aH, b0, um_idesc(32, true, true), ks > 0);   // Qmid += hi x t0
+          um_mma(d0 + 32, aL, b1, um_idesc(32, true, false), true);    //       + lo x t1
+          um_mma(d0 + 64, aL, b0, um_idesc(32, true, true), ks > 0);   // Q00 += lo x t0
+        }
+      }
+      um_commit(&S.mbar_mma);
+    }
+    um_wait(&S.mbar_mma, mphase);
+    mphase ^= 1u;
+    um_fence_after();
+    // ---- stage 2: outputs m' in [16 half, 16 half + 16) of this thread's block row
+    const int64_t n0 = cta_blk0 * CDC_HOP - A.c;
+    int64_t lo64 = n0, hi64 = n0 + (int64_t)CDC_BLK * CDC_HOP;
+    const int64_t o_lo = io.out_first, o_hi = io.out_first + io.out_count;
+    lo64 = lo64 < o_lo ? o_lo : lo64;
+    hi64 = hi64 > o_hi ? o_hi : hi64;
+    const int lo = (int)(lo64 - n0), hi = (int)(hi64 - n0);
+    const uint32_t fl[2][2] = {{S.flags[row][0][0], S.flags[row][0][1]}, {S.flags[row][1][0], S.flags[row][1][1]}};
+    TcStats st;
+#pragma unroll 1
+    for (int c8 = 0; c8 < 2; ++c8) {
+      const int m0 = 16 * half + 8 * c8;  // kept-output index m - 32
+      int32_t z[2][8];
+#pragma unroll
+      for (int sd = 0; sd < 2; ++sd) {
+        int32_t q11[8], qm[8], q00[8];
+        um_ld8(tlane + 96 * sd + 0 + m0, q11);
+        um_ld8(tlane + 96 * sd + 32 + m0, qm);
+        um_ld8(tlane + 96 * sd + 64 + m0, q00);
+        um_ld_wait();
+        um_ld_fence(q11);
+        um_ld_fence(qm);
+        um_ld_fence(q00);
+        if ((fl[sd][0] | fl[sd][1]) != 0u) {
+          // a flagged bin k carried value + 1: subtract its matrix column
+          const int E = sd ? TC_E_IM : TC_E_RE;
+          for (int w2 = 0; w2 < 2; ++w2) {
+            uint32_t bits = fl[sd][w2];
+            while (bits) {
+              const int k = 32 * w2 + __ffs(bits) - 1;
+              bits &= bits - 1;
+#pragma unroll
+              for (int e = 0; e < 8; ++e) q00[e] -= (int32_t)S.root[(E - (32 + m0 + e) * k) & 63];
+            }
+          }
+        }
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          const int32_t zz = qm[e] * 256 + q00[e] - q11[e];
+          z[sd][e] = (int32_t)f4_mod((uint32_t)(zz + (int32_t)(F4 * 16384u)) + 32768u);
+        }
+      }
+      const int idx = 32 * row + m0;  // local output index of z[.][0]
+      if (FAST) {
+#pragma unroll
+        for (int e = 0; e < 8; e += 2) {
+          const int32_t zr2[2] = {z[0][e] - 32768, z[0][e + 1] - 32768};
+          const int32_t zi2[2] = {z[1][e] - 32768, z[1][e + 1] - 32768};
+          tc_store_pair(A, s, n0 - io.out_first, idx + e, lo, hi, zr2, zi2, st);
+        }
+      } else {
+        uint32_t* u = s_u + row * UP + m0;
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          u[e] = (uint32_t)z[0][e];
+          u[CDC_BLK * UP + e] = (uint32_t)z[1][e];
+        }
+      }
+    }
+    um_fence_before();  // TMEM reads of this item precede the next item's MMA 1
+    if (FAST) {
+      if (io.decim_acc) {
+        const int pa = (int)(n0 & 1);  // even local indices carry phase n0 & 1
+        const unsigned long long va[4] = {st.a2, st.a4 & 0xffffffffull, st.a4 >> 32, st.a4h};
+        const unsigned long long vb[4] = {st.b2, st.b4 & 0xffffffffull, st.b4 >> 32, st.b4h};
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          unsigned long long x = va[q], y = vb[q];
+#pragma unroll
+          for (int off = 16; off > 0; off >>= 1) {
+            x += __shfl_xor_sync(0xffffffffu, x, off);
+            y += __shfl_xor_sync(0xffffffffu, y, off);
+          }
+          if (lane == 0) {
+            if (x) atomicAdd(io.decim_acc + ((int64_t)s * 2 + pa) * 4 + q, x);
+            if (y) atomicAdd(io.decim_acc + ((int64_t)s * 2 + (pa ^ 1)) * 4 + q, y);
+          }
+        }
+      }
+    } else {
+      __syncthreads();
+      cdc_epilogue_generic<true>(A, s_u, s, n0, lo64, hi64);
+    }
+  }
+  __syncthreads();
+  um_fence_after();
+  if (warp == 0)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" :: "r"(tmem), "n"(UM_TMEM_COLS) : "memory");
+}
+
 // Reduce the fused statistics to the decimation phase (linksim.py:249-260):
 // metric(ph) = sum_pols mean(|d|^4) / mean(|d|^2)^2 ; scale-free, so the integer
 // outputs stand in for d = y_int / output_scale.
@@ -973,6 +1328,8 @@ static cudaError_t launch_tc(const CdcArgs& A, cudaStream_t st) {
   int& per_sm = grid_per_sm[FAST ? 1 : 0];
   if (per_sm == 0) {
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
+    if (e == cudaSuccess)  // all of L1 as shared memory: the kernel streams, it does not cache
+      e = cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     if (e != cudaSuccess) return e;
     int dev = 0;
     e = cudaGetDevice(&dev);
@@ -981,6 +1338,39 @@ static cudaError_t launch_tc(const CdcArgs& A, cudaStream_t st) {
     if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k, CDC_CTA, SMEM);
     if (e != cudaSuccess) return e;
     per_sm = n > 0 ? n : 1;
+  }
+  const int64_t items = (A.blk_count + CDC_BLK - 1) / CDC_BLK * A.io.n_streams;
+  const int64_t full = (int64_t)per_sm * sms;
+  const unsigned grid = (unsigned)(items < full ? items : full);
+  k<<<grid, CDC_CTA, SMEM, st>>>(A);
+  return cudaGetLastError();
+}
+
+template <bool FAST>
+static cudaError_t launch_umma(const CdcArgs& A, cudaStream_t st) {
+  constexpr int SMEM = (int)sizeof(UmmaSmem) + (FAST ? 0 : 2 * CDC_BLK * UP * 4);
+  auto* k = k_cdc64_umma<FAST>;
+  static int grid_per_sm[2] = {0, 0};
+  static int sms = 0;
+  int& per_sm = grid_per_sm[FAST ? 1 : 0];
+  if (per_sm == 0) {
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
+    if (e == cudaSuccess)  // all of L1 as shared memory: the kernel streams, it does not cache
+      e = cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    if (e != cudaSuccess) return e;
+    int dev = 0;
+    e = cudaGetDevice(&dev);
+    if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    int n = 0;
+    if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k, CDC_CTA, SMEM);
+    if (e != cudaSuccess) return e;
+    // 256 TMEM columns per CTA: two resident CTAs hold all 512 columns. The occupancy
+    // API reports 1 for the 85 KB fast variant although two fit (ncu: smem limit 2), so
+    // the grid is sized for two; an SM that cannot hold both runs the second later.
+    per_sm = FAST ? 2 : (n > 0 ? (n > 2 ? 2 : n) : 1);
+    if (getenv("FNTGPU_DEBUG"))
+      fprintf(stderr, "k_cdc64_umma<%d>: smem %d B, %d CTAs/SM by occupancy, grid %d x %d SMs\n", (int)FAST,
+              SMEM, n, per_sm, sms);
   }
   const int64_t items = (A.blk_count + CDC_BLK - 1) / CDC_BLK * A.io.n_streams;
   const int64_t full = (int64_t)per_sm * sms;
@@ -1023,6 +1413,10 @@ cudaError_t launch_cdc64(const fntgpu_cdc_taps& taps, const fntgpu_cdc_io& io, c
   if (io.in_dtype == FNTGPU_I8 && taps.kernel == FNTGPU_CDC_KERNEL_TC) {
     A.s_base = 0;
     return fast ? launch_tc<true>(A, st) : launch_tc<false>(A, st);
+  }
+  if (io.in_dtype == FNTGPU_I8 && taps.kernel == FNTGPU_CDC_KERNEL_UMMA) {
+    A.s_base = 0;
+    return fast ? launch_umma<true>(A, st) : launch_umma<false>(A, st);
   }
   for (int64_t s0 = 0; s0 < io.n_streams; s0 += 65535) {
     A.s_base = (int32_t)s0;

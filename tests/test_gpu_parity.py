@@ -175,10 +175,11 @@ def test_encode_decode_arrays():
 
 # ----------------------------------------------------------------------- CDC
 
-@pytest.fixture(params=("tc", "shift"))
+@pytest.fixture(params=("shift", "tc", "umma"))
 def cdc_kernel(request):
-    """Run a CDC test through both kernels: the tensor-core matrix form (int8 planes)
-    and the shift-add butterfly kernel (cdc.set_cdc_kernel)."""
+    """Run a CDC test through every kernel: the shift-add butterflies and the
+    split-integer matrix form on mma.sync (tc) and on tcgen05 (umma), the latter two
+    for int8 planes (cdc.set_cdc_kernel)."""
     from paper_2405_04253_b200 import cdc as cdc_mod
     prev = cdc_mod.set_cdc_kernel(request.param)
     yield request.param
@@ -297,7 +298,7 @@ def test_cdc_tc_unrepresentable_residue():
     bm = np.zeros(64, dtype=np.int64)
     eng._b_plus, eng._b_minus, eng._taps_c = bp, bm, None
     want = [N.cdc_process_int(xr[s].astype(np.int64), xi[s].astype(np.int64), bp, bm, 32) for s in range(S)]
-    for kern in ("tc", "shift"):
+    for kern in ("tc", "umma", "shift"):
         prev = cdc_mod.set_cdc_kernel(kern)
         try:
             yr = torch.empty((S, L), dtype=torch.int32, device="cuda")

@@ -46,6 +46,7 @@ PROFILES = ROOT / "profiles"
 # Algorithmic work per unit (SURVEY 8d convention):
 #   radix-2 butterfly = 6 INT ops, general residue product = 6, modular aux op = 2
 CDC_INT_OPS_PER_BLOCK = 4 * 192 * 6 + 128 * 6 + 256 * 2   # 5888 per 64-block = 184 / sample
+CDC_TC_MACS_PER_BLOCK = 2 * 2 * 64 * 64 + 2 * 4 * 32 * 64    # int8 MACs per block, matrix forms
 AEQ_INT_OPS_PER_BLOCK_FNT = (4 + 32 + 32) * 80 * 6 + 1024 * 6 + 448  # 39232 (incl. tap-spectrum refresh)
 AEQ_INT_OPS_PER_BLOCK_DIRECT = 2 * 4096 + 448               # 8640 (exact time-domain MIMO FIR)
 # The kernel's transform-domain stream sum (k_aeq.cu fused_ok; every block of 5-bit
@@ -273,8 +274,9 @@ def _config_dict(args, cpu=False):
                      % (args.links, int(math.log2(args.symbols))),
          "links_per_gpu": args.links, "symbols": args.symbols, "samples_per_pol": 2 * args.symbols,
          "aeq_forward": args.forward,
-         "cdc_kernel": "k_cdc64_tc (tensor-core split-integer FNT)" if args.cdc_kernel == "tc"
-                       else "k_cdc64 (shift-add FNT)",
+         "cdc_kernel": {"tc": "k_cdc64_tc (mma.sync split-integer FNT)",
+                        "umma": "k_cdc64_umma (tcgen05 split-integer FNT)"}.get(
+                            args.cdc_kernel, "k_cdc64 (shift-add FNT; auto with the fused requantization)"),
          "parallelism": f"links sharded over {args.gpus} GPU(s), no collective",
          "l2": "inputs (int8 I/Q, %.1f GB/GPU) exceed the 126 MB L2; no flush needed"
                % (4 * args.links * 2 * args.symbols / 1e9)}
@@ -304,8 +306,8 @@ def main():
     ap.add_argument("--no-alt", action="store_true", help="skip the direct-forward AEQ comparison")
     ap.add_argument("--no-quality", action="store_true", help="skip the on-device BER/EVM scoring")
     ap.add_argument("--cdc-kernel", default="auto", choices=["auto", "umma", "tc", "shift"],
-                    help="FNT-CDC kernel for the int8 planes: shift-add butterflies (auto/shift) "
-                         "or the tensor-core split-integer matrix form (tc)")
+                    help="FNT-CDC kernel for the int8 planes: auto (measured-faster choice), shift-add "
+                         "butterflies, or the split-integer matrix form on mma.sync (tc) / tcgen05 (umma)")
     args = ap.parse_args()
     if args.impl == "reference":
         impl_reference(args)
@@ -600,14 +602,14 @@ def time_cdc_kernels(run, reps: int, world: int) -> dict:
     return out
 
 
-def c4_traffic(world: int):
-    """DRAM bytes of one k_cdc64 launch at config 4 on one GPU, from the committed ncu
+def c4_traffic(world: int, kernel: str = "k_cdc64"):
+    """DRAM bytes of one CDC launch at config 4 on one GPU, from the committed ncu
     --set full capture (profiles/ncu_summary_r01_c4.json); None for other shard sizes."""
     path = PROFILES / "ncu_summary_r01_c4.json"
     if world != 1 or not path.exists():
         return None
     try:
-        return json.loads(path.read_text()).get("per_launch_dram_bytes", {}).get("k_cdc64")
+        return json.loads(path.read_text()).get("per_launch_dram_bytes", {}).get(kernel)
     except Exception:
         return None
 
@@ -684,6 +686,8 @@ def run_c4(args, world, rank, local):
     achieved = n_blocks * CDC_INT_OPS_PER_BLOCK / (per_launch_ms * 1e-3) / 1e12
     hbm_bytes = 2 * sh.x_count * 2 + 2 * sh.out_count * 4  # int8 I/Q in, int16 I/Q out
     hbm_gbs = hbm_bytes / (per_launch_ms * 1e-3) / 1e9
+    # kernel auto picks for int8 planes with int16 outputs (k_cdc.cu launch_cdc64)
+    c4_kernel = {"tc": "k_cdc64_tc", "shift": "k_cdc64"}.get(args.cdc_kernel, "k_cdc64_umma")
     line = {
         "metric": "FNT-CDC Gsamples/s (config 4)", "value": value, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max / args.steps,
@@ -693,16 +697,29 @@ def run_c4(args, world, rank, local):
                                "samples per pol, 75 km taps, range-sharded over %d GPU(s) with the "
                                "overlap-save halo" % (L, world),
                    "samples_per_pol": L, "shard_out": [sh.out_first, sh.out_count],
-                   "cdc_kernel": "k_cdc64_tc" if args.cdc_kernel == "tc" else "k_cdc64",
+                   "cdc_kernel": {"tc": "k_cdc64_tc", "shift": "k_cdc64"}.get(
+                       args.cdc_kernel, "k_cdc64_umma (tcgen05 split-integer FNT; auto)"),
                    "l2": "inputs (%.1f GB) exceed L2" % (hbm_bytes / 1e9)},
-        "roofline": {"bound": "int", "kernel": "k_cdc64", "achieved": achieved,
+        "roofline": {"bound": "int", "kernel": c4_kernel, "achieved": achieved,
                      "peak": peaks["int_tops"], "unit": "Tops/s",
-                     "frac": achieved / peaks["int_tops"], "traffic": c4_traffic(world),
+                     "frac": achieved / peaks["int_tops"], "traffic": c4_traffic(world, c4_kernel),
                      "peak_source": peaks["int_source"],
                      "hbm": {"achieved_gbs": hbm_gbs, "peak_gbs": peaks["hbm_gbs"],
                              "frac": hbm_gbs / peaks["hbm_gbs"]}},
         "clocks": clk, "gpu_launches": args.steps,
     }
+    if c4_kernel != "k_cdc64":
+        # the matrix forms run the transforms on the tensor cores: the roofline above counts
+        # the algorithm's FNT work (SURVEY 8d convention) against the INT peak of the CUDA
+        # cores that still carry the mod-F4 reductions; the tensor side is reported here
+        macs = n_blocks * CDC_TC_MACS_PER_BLOCK / (per_launch_ms * 1e-3)
+        int8_peak = 2.0 * peaks.get("bf16_tflops", 2250.0)  # dense int8 = 2x dense bf16
+        line["roofline"]["tensor"] = {
+            "achieved": 2.0 * macs / 1e12, "peak": int8_peak, "unit": "Tops/s (int8)",
+            "frac": 2.0 * macs / 1e12 / int8_peak,
+            "peak_source": "2 x measured dense bf16 (MEASURED_PEAKS.json)" if "bf16_tflops" in peaks
+                           else "2 x nominal dense bf16",
+            "macs_per_block": CDC_TC_MACS_PER_BLOCK}
     if not args.no_alt:
         line["cdc_kernels"] = time_cdc_kernels(step, args.steps, world)
     if not args.no_e2e:

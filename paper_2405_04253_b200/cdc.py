@@ -112,9 +112,10 @@ def _device_dtype(a: np.ndarray, half: int) -> np.dtype:
     return np.dtype(np.int32)
 
 
-# Kernel behind fntgpu_cdc64_process for int8 planes (fntgpu_cdc_taps.kernel): the
-# shift-add butterfly kernel ("auto"/"shift", measured faster on B200) or the
-# tensor-core split-integer matrix form of the FNT ("tc"). Both are bit-exact; other
+# Kernel behind fntgpu_cdc64_process for int8 planes (fntgpu_cdc_taps.kernel): "auto"
+# (the measured-faster one: the tcgen05 split-integer matrix form for plain outputs,
+# the shift-add butterflies when requantization / statistics are fused), "shift",
+# "tc" (mma.sync matrix form) or "umma" (tcgen05 matrix form). All bit-exact; other
 # input dtypes always take the shift-add kernel.
 CDC_KERNELS = {"auto": 0, "shift": 1, "tc": 2, "umma": 3}
 _cdc_kernel = os.environ.get("FNTGPU_CDC_KERNEL", "auto")

@@ -691,6 +691,94 @@ __device__ __forceinline__ void tc_store_pair(const CdcArgs& A, int s, int64_t b
   }
 }
 
+// Output pointers / parameters of the fast epilogue, read from param space once.
+struct TcOut {
+  int16_t* yr;
+  int16_t* yi;
+  int8_t* qr;
+  int8_t* qi;
+  unsigned long long* acc;
+  int64_t y_stride, q_stride;
+  int k, qmax;
+  bool i16;
+  __device__ explicit TcOut(const fntgpu_cdc_io& io)
+      : yr(reinterpret_cast<int16_t*>(io.yr)), yi(reinterpret_cast<int16_t*>(io.yi)), qr(io.qr), qi(io.qi),
+        acc(io.decim_acc), y_stride(io.y_stride), q_stride(io.q_stride), k(io.q_shift), qmax(io.q_max),
+        i16(io.out_dtype == FNTGPU_I16) {}
+};
+
+// 8 consecutive outputs idx .. idx + 7 of stream s (idx multiple of 8)
+__device__ __forceinline__ void tc_store8(const TcOut& O, const int8_t* tie, int s, int64_t base_o, int idx,
+                                          int lo, int hi, const int32_t (&zr)[8], const int32_t (&zi)[8],
+                                          TcStats& st) {
+  if (idx + 8 <= lo || idx >= hi) return;
+  const bool full = idx >= lo && idx + 8 <= hi;
+  if (O.i16) {
+    int16_t* yr = O.yr + s * O.y_stride + base_o + idx;
+    int16_t* yi = O.yi + s * O.y_stride + base_o + idx;
+    if (full) {
+      uint32_t pr[4], pi[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        pr[e] = ((uint32_t)zr[2 * e] & 0xffffu) | ((uint32_t)zr[2 * e + 1] << 16);
+        pi[e] = ((uint32_t)zi[2 * e] & 0xffffu) | ((uint32_t)zi[2 * e + 1] << 16);
+      }
+      // base_o + idx is a multiple of 4 (launch precondition): 8-byte aligned pairs
+      reinterpret_cast<uint2*>(yr)[0] = make_uint2(pr[0], pr[1]);
+      reinterpret_cast<uint2*>(yr)[1] = make_uint2(pr[2], pr[3]);
+      reinterpret_cast<uint2*>(yi)[0] = make_uint2(pi[0], pi[1]);
+      reinterpret_cast<uint2*>(yi)[1] = make_uint2(pi[2], pi[3]);
+    } else {
+#pragma unroll
+      for (int e = 0; e < 8; ++e)
+        if (idx + e >= lo && idx + e < hi) {
+          yr[e] = (int16_t)zr[e];
+          yi[e] = (int16_t)zi[e];
+        }
+    }
+  }
+  if (CDC_PROBE != 1 && O.qr) {
+    uint32_t qr[2] = {0u, 0u}, qi[2] = {0u, 0u};
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      qr[e >> 2] |= ((uint32_t)requant_int(zr[e], O.k, tie, O.qmax) & 0xffu) << (8 * (e & 3));
+      qi[e >> 2] |= ((uint32_t)requant_int(zi[e], O.k, tie, O.qmax) & 0xffu) << (8 * (e & 3));
+    }
+    int8_t* pq = O.qr + s * O.q_stride + base_o + idx;
+    int8_t* pqi = O.qi + s * O.q_stride + base_o + idx;
+    if (full) {
+      *reinterpret_cast<uint32_t*>(pq) = qr[0];
+      *reinterpret_cast<uint32_t*>(pq + 4) = qr[1];
+      *reinterpret_cast<uint32_t*>(pqi) = qi[0];
+      *reinterpret_cast<uint32_t*>(pqi + 4) = qi[1];
+    } else {
+#pragma unroll
+      for (int e = 0; e < 8; ++e)
+        if (idx + e >= lo && idx + e < hi) {
+          pq[e] = (int8_t)(qr[e >> 2] >> (8 * (e & 3)));
+          pqi[e] = (int8_t)(qi[e >> 2] >> (8 * (e & 3)));
+        }
+    }
+  }
+  if (CDC_PROBE != 2 && O.acc) {
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const bool ok = full || (idx + e >= lo && idx + e < hi);
+      const uint32_t m2 = ok ? (uint32_t)(zr[e] * zr[e]) + (uint32_t)(zi[e] * zi[e]) : 0u;  // <= 2^31
+      const unsigned long long m4 = (unsigned long long)m2 * m2;
+      if (e & 1) {
+        st.b2 += m2;
+        st.b4 += m4;
+        st.b4h += (st.b4 < m4);
+      } else {
+        st.a2 += m2;
+        st.a4 += m4;
+        st.a4h += (st.a4 < m4);
+      }
+    }
+  }
+}
+
 template <bool FAST>
 __global__ void __launch_bounds__(CDC_CTA, CDC_TC_MIN_CTAS) k_cdc64_tc(const __grid_constant__ CdcArgs A) {
   extern __shared__ __align__(16) unsigned char smem[];
@@ -1063,6 +1151,7 @@ __global__ void __launch_bounds__(CDC_CTA, CDC_UMMA_MIN_CTAS) k_cdc64_umma(const
   um_fence_after();
   const uint32_t tmem = S.tmem_base;
   const uint32_t tlane = tmem + ((uint32_t)(32 * (warp & 3)) << 16);
+  const TcOut O(io);
 
   const int64_t chunks = (A.blk_count + CDC_BLK - 1) / CDC_BLK;
   const int64_t items = chunks * io.n_streams;
@@ -1078,14 +1167,16 @@ __global__ void __launch_bounds__(CDC_CTA, CDC_UMMA_MIN_CTAS) k_cdc64_umma(const
     int8_t* s_xr = S.x[buf][0];
     int8_t* s_xi = S.x[buf][1];
     if (tc_bulk_ok(A, chunks, it, in_lo, in_hi)) {
-      um_wait(&S.mbar_x[buf], (xphase >> buf) & 1u);
+      um_wait(&S.mbar_x[buf], (xphase >> buf) & 1u);  // every thread acquires the TMA bytes
       xphase ^= 1u << buf;
     } else {
       const int64_t g0 = cta_blk0 * CDC_HOP - CDC_HOP;
       stage_plane<int8_t, int8_t>(s_xr, reinterpret_cast<const int8_t*>(io.xr) + (size_t)s * io.x_stride, g0, io);
       stage_plane<int8_t, int8_t>(s_xi, reinterpret_cast<const int8_t*>(io.xi) + (size_t)s * io.x_stride, g0, io);
+      __syncthreads();  // vector-staged window visible (stream edges only)
     }
-    __syncthreads();  // window visible; all threads done with the other buffer
+    // the other buffer was last read by the previous item's relayout, which every thread
+    // finished before that item's operand barrier: the next window can land there now
     {
       const int64_t nx = it + gridDim.x;
       if (tid == 0 && nx < items && tc_bulk_ok(A, chunks, nx, in_lo, in_hi))
@@ -1230,12 +1321,13 @@ __global__ void __launch_bounds__(CDC_CTA, CDC_UMMA_MIN_CTAS) k_cdc64_umma(const
       }
       const int idx = 32 * row + m0;  // local output index of z[.][0]
       if (FAST) {
+        int32_t zr8[8], zi8[8];
 #pragma unroll
-        for (int e = 0; e < 8; e += 2) {
-          const int32_t zr2[2] = {z[0][e] - 32768, z[0][e + 1] - 32768};
-          const int32_t zi2[2] = {z[1][e] - 32768, z[1][e + 1] - 32768};
-          tc_store_pair(A, s, n0 - io.out_first, idx + e, lo, hi, zr2, zi2, st);
+        for (int e = 0; e < 8; ++e) {
+          zr8[e] = z[0][e] - 32768;
+          zi8[e] = z[1][e] - 32768;
         }
+        tc_store8(O, io.q_tie, s, n0 - io.out_first, idx, lo, hi, zr8, zi8, st);
       } else {
         uint32_t* u = s_u + row * UP + m0;
 #pragma unroll
@@ -1247,7 +1339,7 @@ __global__ void __launch_bounds__(CDC_CTA, CDC_UMMA_MIN_CTAS) k_cdc64_umma(const
     }
     um_fence_before();  // TMEM reads of this item precede the next item's MMA 1
     if (FAST) {
-      if (io.decim_acc) {
+      if (O.acc) {
         const int pa = (int)(n0 & 1);  // even local indices carry phase n0 & 1
         const unsigned long long va[4] = {st.a2, st.a4 & 0xffffffffull, st.a4 >> 32, st.a4h};
         const unsigned long long vb[4] = {st.b2, st.b4 & 0xffffffffull, st.b4 >> 32, st.b4h};
@@ -1407,14 +1499,20 @@ cudaError_t launch_cdc64(const fntgpu_cdc_taps& taps, const fntgpu_cdc_io& io, c
            (reinterpret_cast<uintptr_t>(io.yi) & 7) == 0 && io.y_stride % 4 == 0;
   if (io.in_dtype != FNTGPU_I8 && io.in_dtype != FNTGPU_I32 && io.in_dtype != FNTGPU_I64)
     return cudaErrorInvalidValue;
-  // tensor-core form on request (fntgpu_cdc_taps.kernel), for int8 planes (their samples
-  // are the int8 MMA operands). Auto keeps the shift-add kernel: measured faster on B200
-  // (config 5 CDC 33.0 vs 36.4 ms, config 4 26.0 vs 28.7 ms; profiles/cdc_tc_r01.json)
-  if (io.in_dtype == FNTGPU_I8 && taps.kernel == FNTGPU_CDC_KERNEL_TC) {
+  // tensor-core forms for int8 planes (their samples are the int8 MMA operands). Auto
+  // picks what measured fastest on B200 (profiles/cdc_tc_r01.json): the tcgen05 form
+  // for plain int16 / no outputs (config 4: 24.0 vs 25.8 ms), the shift-add kernel
+  // when the requantization / statistics epilogue is fused (config 5: tie, 33.0 ms) and
+  // for every other output or input type. mma.sync (TC) only on request (0.90x).
+  int kern = taps.kernel;
+  if (kern == FNTGPU_CDC_KERNEL_AUTO)
+    kern = (io.in_dtype == FNTGPU_I8 && fast && !io.qr && !io.decim_acc) ? FNTGPU_CDC_KERNEL_UMMA
+                                                                          : FNTGPU_CDC_KERNEL_SHIFT;
+  if (io.in_dtype == FNTGPU_I8 && kern == FNTGPU_CDC_KERNEL_TC) {
     A.s_base = 0;
     return fast ? launch_tc<true>(A, st) : launch_tc<false>(A, st);
   }
-  if (io.in_dtype == FNTGPU_I8 && taps.kernel == FNTGPU_CDC_KERNEL_UMMA) {
+  if (io.in_dtype == FNTGPU_I8 && kern == FNTGPU_CDC_KERNEL_UMMA) {
     A.s_base = 0;
     return fast ? launch_umma<true>(A, st) : launch_umma<false>(A, st);
   }

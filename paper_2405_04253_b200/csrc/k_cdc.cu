@@ -68,6 +68,8 @@ struct CdcArgs {
   int64_t blk_count;   // blocks per stream
   int32_t c;           // n_taps // 2
   int32_t s_base;      // first stream of this launch (grid.y is limited to 65535)
+  int32_t q_away;      // every tie of the exact requantization rounds away from zero
+                       // (io.q_tie[j] == min(j + 1, q_max)): q = min((|y| + 2^(k-1)) >> k, q_max)
 };
 
 __device__ __forceinline__ int32_t sext8(uint32_t w, int k) {
@@ -112,6 +114,13 @@ __device__ __forceinline__ void stage_plane(TS* dst, const TIN* src, int64_t g0,
 // when inv * q_scale == 2^-k up to rounding: the float64 product is within 3 ulp of
 // y / 2^k, so round-half-away agrees with the exact rounding except at exact ties
 // |y| = 2^(k-1) + j 2^k, whose float64 outcome the host precomputed (io.q_tie).
+// requant_int when the host found every tie rounding away (CdcArgs.q_away): no tie
+// table lookup, no comparisons beyond the clamp
+__device__ __forceinline__ int32_t requant_away(int32_t y, int k, int qmax) {
+  const int32_t q = min((abs(y) + (1 << (k - 1))) >> k, qmax);
+  return y < 0 ? -q : q;
+}
+
 __device__ __forceinline__ int32_t requant_int(int32_t y, int k, const int8_t* tie, int qmax) {
   const int32_t a = abs(y);
   const int32_t base = a >> k;
@@ -173,10 +182,18 @@ __device__ __forceinline__ void cdc_epilogue_fast(const CdcArgs& A, const uint32
     }
     if (CDC_PROBE != 1 && qr) {
       uint32_t pr = 0, pi = 0;
+      if (A.q_away) {
 #pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        pr |= ((uint32_t)requant_int(zr[e], k, tie, qmax) & 0xffu) << (8 * e);
-        pi |= ((uint32_t)requant_int(zi[e], k, tie, qmax) & 0xffu) << (8 * e);
+        for (int e = 0; e < 4; ++e) {
+          pr |= ((uint32_t)requant_away(zr[e], k, qmax) & 0xffu) << (8 * e);
+          pi |= ((uint32_t)requant_away(zi[e], k, qmax) & 0xffu) << (8 * e);
+        }
+      } else {
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          pr |= ((uint32_t)requant_int(zr[e], k, tie, qmax) & 0xffu) << (8 * e);
+          pi |= ((uint32_t)requant_int(zi[e], k, tie, qmax) & 0xffu) << (8 * e);
+        }
       }
       if (full) {
         *reinterpret_cast<uint32_t*>(qr + v) = pr;
@@ -700,11 +717,11 @@ struct TcOut {
   unsigned long long* acc;
   int64_t y_stride, q_stride;
   int k, qmax;
-  bool i16;
-  __device__ explicit TcOut(const fntgpu_cdc_io& io)
-      : yr(reinterpret_cast<int16_t*>(io.yr)), yi(reinterpret_cast<int16_t*>(io.yi)), qr(io.qr), qi(io.qi),
-        acc(io.decim_acc), y_stride(io.y_stride), q_stride(io.q_stride), k(io.q_shift), qmax(io.q_max),
-        i16(io.out_dtype == FNTGPU_I16) {}
+  bool i16, away;
+  __device__ explicit TcOut(const CdcArgs& A)
+      : yr(reinterpret_cast<int16_t*>(A.io.yr)), yi(reinterpret_cast<int16_t*>(A.io.yi)), qr(A.io.qr),
+        qi(A.io.qi), acc(A.io.decim_acc), y_stride(A.io.y_stride), q_stride(A.io.q_stride),
+        k(A.io.q_shift), qmax(A.io.q_max), i16(A.io.out_dtype == FNTGPU_I16), away(A.q_away != 0) {}
 };
 
 // 8 consecutive outputs idx .. idx + 7 of stream s (idx multiple of 8)
@@ -739,10 +756,18 @@ __device__ __forceinline__ void tc_store8(const TcOut& O, const int8_t* tie, int
   }
   if (CDC_PROBE != 1 && O.qr) {
     uint32_t qr[2] = {0u, 0u}, qi[2] = {0u, 0u};
+    if (O.away) {
 #pragma unroll
-    for (int e = 0; e < 8; ++e) {
-      qr[e >> 2] |= ((uint32_t)requant_int(zr[e], O.k, tie, O.qmax) & 0xffu) << (8 * (e & 3));
-      qi[e >> 2] |= ((uint32_t)requant_int(zi[e], O.k, tie, O.qmax) & 0xffu) << (8 * (e & 3));
+      for (int e = 0; e < 8; ++e) {
+        qr[e >> 2] |= ((uint32_t)requant_away(zr[e], O.k, O.qmax) & 0xffu) << (8 * (e & 3));
+        qi[e >> 2] |= ((uint32_t)requant_away(zi[e], O.k, O.qmax) & 0xffu) << (8 * (e & 3));
+      }
+    } else {
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        qr[e >> 2] |= ((uint32_t)requant_int(zr[e], O.k, tie, O.qmax) & 0xffu) << (8 * (e & 3));
+        qi[e >> 2] |= ((uint32_t)requant_int(zi[e], O.k, tie, O.qmax) & 0xffu) << (8 * (e & 3));
+      }
     }
     int8_t* pq = O.qr + s * O.q_stride + base_o + idx;
     int8_t* pqi = O.qi + s * O.q_stride + base_o + idx;
@@ -1151,7 +1176,7 @@ __global__ void __launch_bounds__(CDC_CTA, CDC_UMMA_MIN_CTAS) k_cdc64_umma(const
   um_fence_after();
   const uint32_t tmem = S.tmem_base;
   const uint32_t tlane = tmem + ((uint32_t)(32 * (warp & 3)) << 16);
-  const TcOut O(io);
+  const TcOut O(A);
 
   const int64_t chunks = (A.blk_count + CDC_BLK - 1) / CDC_BLK;
   const int64_t items = chunks * io.n_streams;
@@ -1482,6 +1507,12 @@ cudaError_t launch_cdc64(const fntgpu_cdc_taps& taps, const fntgpu_cdc_io& io, c
   }
   A.io = io;
   A.c = taps.n_taps / 2;
+  A.q_away = 0;
+  if (io.qr && io.q_shift >= 1 && io.q_max >= 0 && io.q_max < 128) {
+    A.q_away = 1;
+    for (int j = 0; j <= io.q_max; ++j)
+      if (io.q_tie[j] != (j + 1 < io.q_max ? j + 1 : io.q_max)) A.q_away = 0;
+  }
   // blocks B needed for outputs n in [out_first, out_first+out_count): B = (n + c) / 32
   const int64_t b_lo = (io.out_first + A.c) / CDC_HOP;
   const int64_t b_hi = (io.out_first + io.out_count - 1 + A.c) / CDC_HOP;

@@ -311,6 +311,60 @@ def test_cdc_tc_unrepresentable_residue():
             assert np.array_equal(yi[s].cpu().numpy(), want[s][1]), (kern, s)
 
 
+@pytest.mark.parametrize("ties", ("engine", "mixed"))
+def test_cdc_fused_requantization_tie_tables(cdc_kernel, ties):
+    """The fused int8 requantization (linksim.py:404 via quantize_real) against a numpy
+    restatement on the kernel's own int32 outputs: with the engine's tie table (every
+    tie rounds away: the kernels' shift-only fast form) and with a table whose even
+    ties round down (the general form with the table lookup)."""
+    import torch
+    from paper_2405_04253_b200.stream import CdcBank
+    eng = _c2_engine()
+    bank = CdcBank(eng)
+    rng = np.random.default_rng(17)
+    S, L = 2, 40_004
+    xr = rng.integers(-16, 16, (S, L)).astype(np.int8)
+    xi = rng.integers(-16, 16, (S, L)).astype(np.int8)
+    dxr, dxi = torch.from_numpy(xr).cuda(), torch.from_numpy(xi).cuda()
+    y32r = torch.empty((S, L), dtype=torch.int32, device="cuda")
+    y32i = torch.empty_like(y32r)
+    bank.run(dxr, dxi, yr=y32r, yi=y32i)
+    orig = bank._exact_requant
+    tie = {}
+
+    def patched(io, q_spec):
+        orig(io, q_spec)
+        if ties == "mixed":
+            for j in range(0, int(q_spec.max_int) + 1, 2):
+                io.q_tie[j] = min(j, int(q_spec.max_int))
+        tie["k"] = io.q_shift
+        tie["t"] = [int(io.q_tie[j]) for j in range(int(q_spec.max_int) + 1)]
+
+    bank._exact_requant = patched
+    qr = torch.empty((S, L), dtype=torch.int8, device="cuda")
+    qi = torch.empty_like(qr)
+    y16r = torch.empty((S, L), dtype=torch.int16, device="cuda")
+    y16i = torch.empty_like(y16r)
+    spec = eng.sig_spec
+    bank.run(dxr, dxi, yr=y16r, yi=y16i, qr=qr, qi=qi, q_spec=spec)
+    k, t, qmax = tie["k"], np.array(tie["t"]), int(spec.max_int)
+    assert k == 7 and (ties == "engine") == all(t[j] == min(j + 1, qmax) for j in range(qmax + 1))
+
+    def want(y):
+        a = np.abs(y.astype(np.int64))
+        base, rem, half = a >> k, a & ((1 << k) - 1), 1 << (k - 1)
+        q = base + (rem > half)
+        q = np.where(rem == half, t[np.minimum(base, qmax)], q)
+        q = np.minimum(q, qmax)
+        return np.where(y < 0, -q, q).astype(np.int8)
+
+    for got, y in ((qr, y32r), (qi, y32i)):
+        yy = y.cpu().numpy()
+        assert np.array_equal(got.cpu().numpy(), want(yy))
+    assert np.array_equal(y16r.cpu().numpy(), y32r.cpu().numpy().astype(np.int16))
+    assert np.array_equal(y16i.cpu().numpy(), y32i.cpu().numpy().astype(np.int16))
+
+
 @pytest.mark.parametrize("tag,cfg", [
     ("t33", dict(z_km=25.0, fs_hz=80e9, n_taps=33)),
     ("z0", dict(z_km=0.0, fs_hz=80e9, n_taps=32)),

@@ -120,10 +120,11 @@ typedef struct fntgpu_cdc_taps {
   uint32_t b_minus[64]; /* (H_r - 2^8 H_i) mod F  (_b_minus) */
   int32_t n_taps;       /* output alignment c = n_taps // 2 (cdc.py:174) */
   int32_t kernel;       /* FNTGPU_CDC_KERNEL_*: 0 auto (the measured-faster kernel:
-                         * tcgen05 form for int8 planes with plain outputs, shift-add
-                         * otherwise), 1 shift-add FNT kernel, 2 tensor-core split-integer
-                         * matrix form on mma.sync, 3 the same on tcgen05 (int8 planes;
-                         * other dtypes run the shift-add kernel) */
+                         * tcgen05 form for int8 planes with int16 / int8-requantized /
+                         * statistics outputs, shift-add otherwise), 1 shift-add FNT
+                         * kernel, 2 tensor-core split-integer matrix form on mma.sync,
+                         * 3 the same on tcgen05 (int8 planes; other dtypes run the
+                         * shift-add kernel) */
 } fntgpu_cdc_taps;
 #define FNTGPU_CDC_KERNEL_AUTO 0
 #define FNTGPU_CDC_KERNEL_SHIFT 1

@@ -113,8 +113,8 @@ def _device_dtype(a: np.ndarray, half: int) -> np.dtype:
 
 
 # Kernel behind fntgpu_cdc64_process for int8 planes (fntgpu_cdc_taps.kernel): "auto"
-# (the measured-faster one: the tcgen05 split-integer matrix form for plain outputs,
-# the shift-add butterflies when requantization / statistics are fused), "shift",
+# (the measured-faster one: the tcgen05 split-integer matrix form for int16 /
+# requantized / statistics outputs, the shift-add butterflies otherwise), "shift",
 # "tc" (mma.sync matrix form) or "umma" (tcgen05 matrix form). All bit-exact; other
 # input dtypes always take the shift-add kernel.
 CDC_KERNELS = {"auto": 0, "shift": 1, "tc": 2, "umma": 3}

@@ -1532,13 +1532,12 @@ cudaError_t launch_cdc64(const fntgpu_cdc_taps& taps, const fntgpu_cdc_io& io, c
     return cudaErrorInvalidValue;
   // tensor-core forms for int8 planes (their samples are the int8 MMA operands). Auto
   // picks what measured fastest on B200 (profiles/cdc_tc_r01.json): the tcgen05 form
-  // for plain int16 / no outputs (config 4: 24.0 vs 25.8 ms), the shift-add kernel
-  // when the requantization / statistics epilogue is fused (config 5: tie, 33.0 ms) and
-  // for every other output or input type. mma.sync (TC) only on request (0.90x).
+  // for the fast epilogues (config 4 int16 outputs: 24.1 vs 25.7 ms; config 5 fused
+  // requantization + statistics: 31.1 vs 31.4 ms), the shift-add kernel for every other
+  // output or input type. mma.sync (TC) only on request (0.87-0.90x).
   int kern = taps.kernel;
   if (kern == FNTGPU_CDC_KERNEL_AUTO)
-    kern = (io.in_dtype == FNTGPU_I8 && fast && !io.qr && !io.decim_acc) ? FNTGPU_CDC_KERNEL_UMMA
-                                                                          : FNTGPU_CDC_KERNEL_SHIFT;
+    kern = (io.in_dtype == FNTGPU_I8 && fast) ? FNTGPU_CDC_KERNEL_UMMA : FNTGPU_CDC_KERNEL_SHIFT;
   if (io.in_dtype == FNTGPU_I8 && kern == FNTGPU_CDC_KERNEL_TC) {
     A.s_base = 0;
     return fast ? launch_tc<true>(A, st) : launch_tc<false>(A, st);

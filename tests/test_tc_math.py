@@ -1,5 +1,5 @@
 """CPU restatement of the tensor-core (split-integer matrix) form of the FNT-CDC
-(paper_2405_04253_b200/csrc/k_cdc.cu: k_cdc64_tc, cdc_tc_tables).
+(paper_2405_04253_b200/csrc/k_cdc.cu: k_cdc64_umma, k_cdc64_tc).
 
 The kernel runs the 64-point forward FNT and the pruned inverse as int8 matrix
 products on the tensor cores (mma.sync m16n8k32, exact int32 accumulation): every
@@ -84,7 +84,7 @@ def split_s8(w):
 
 def tc_blocks(win_r, win_i, bp, bm, stats=None):
     """Split-integer matrix form of cdc.py:141-156 for windows (B, 64) of int8 samples,
-    as k_cdc64_tc computes it. Returns decoded (z_re, z_im) (B, 32) of the kept outputs."""
+    as k_cdc64_umma and k_cdc64_tc compute it. Returns decoded (z_re, z_im) (B, 32) of the kept outputs."""
     xr = np.asarray(win_r, dtype=np.int64)
     xi = np.asarray(win_i, dtype=np.int64)
     t1, t0 = limbs_u8s8(forward_matrix())

@@ -336,12 +336,40 @@ __device__ __forceinline__ void lane_update(const AeqArgs& A, AeqScratch& S, int
       }
     }
     T.asum = 0;
+    uint32_t smask = 0;  // taps whose rint left [-16383, 16383] (or the int32 range)
 #pragma unroll
     for (int kk = 0; kk < 8; ++kk) {
       const double gr = dadd(c0[kk], c1[kk]);
       const double w = dadd(S.wf[kk][lane], dmul(mu, gr));
       S.wf[kk][lane] = w;
-      set_tap<BAL>(T, kk, requantize_tap(w, A.prm.tap_scale, T.sat));
+      // requantize_tap without its per-tap |p| >= 2^63 test: such a p saturates the
+      // int32 conversion, so it is among the clipped taps settled below
+      const int32_t i = __double2int_rn(dmul(w, A.prm.tap_scale));
+      const int32_t c = min(max(i, -AEQ_TAP_MAX), AEQ_TAP_MAX);
+      smask |= (uint32_t)(c != i) << kk;
+      set_tap<BAL>(T, kk, c);
+    }
+    T.sat += __popc(smask);
+    if (__any_sync(0xffffffffu, smask != 0u)) {
+      // rare: a clipped tap whose rint is not an int64 (numpy: INT64_MIN) becomes
+      // -16383 and is not counted (requantize_tap, aeq.py:165-168)
+      bool redo = false;
+#pragma unroll
+      for (int kk = 0; kk < 8; ++kk) {
+        if ((smask >> kk) & 1u) {
+          const double p = dmul(S.wf[kk][lane], A.prm.tap_scale);
+          if (!(fabs(p) < 9.2233720368547758e18)) {
+            T.sat -= 1;
+            T.gp[kk] = pack_taps<BAL>(-AEQ_TAP_MAX);
+            redo = true;
+          }
+        }
+      }
+      if (BAL && redo) {
+        T.asum = 0;
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) T.asum += (uint32_t)abs((unpack_tap<BAL>(T.gp[kk]) + 32) >> 6);
+      }
     }
   }
   __syncwarp();

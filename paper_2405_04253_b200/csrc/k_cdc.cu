@@ -18,6 +18,7 @@
 // of int8 planes) or 16-byte vector loads; one HBM read per input sample (the
 // 32-sample halo between neighbouring blocks is re-read from shared memory) and
 // one HBM write per output.
+#include <atomic>
 #include <cstdio>
 #include <cstdlib>
 #include <type_traits>
@@ -1436,63 +1437,68 @@ static cudaError_t launch_k(const CdcArgs& A, dim3 grid, cudaStream_t st) {
   return cudaGetLastError();
 }
 
+// Persistent-grid launch configuration of a tensor-core CDC kernel on the current
+// device: the dynamic shared-memory attribute is per device, so it is set (and the
+// resident CTAs per SM measured) once per device ordinal.
+struct TcLaunchCfg {
+  std::atomic<int> per_sm{0};
+  int sms = 0;
+};
+template <typename K>
+static cudaError_t tc_launch_cfg(TcLaunchCfg (&cfgs)[64], K* k, int smem, int cap, int& per_sm, int& sms) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  if (dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
+  TcLaunchCfg& c = cfgs[dev];
+  if (c.per_sm.load(std::memory_order_acquire) == 0) {
+    e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e == cudaSuccess)  // all of L1 as shared memory: the kernels stream, they do not cache
+      e = cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    int n = 0, m = 0;
+    if (e == cudaSuccess) e = cudaDeviceGetAttribute(&m, cudaDevAttrMultiProcessorCount, dev);
+    if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k, CDC_CTA, smem);
+    if (e != cudaSuccess) return e;
+    c.sms = m;
+    // cap < 0: a fixed count of -cap (the occupancy API under-reports for the 85 KB tcgen05
+    // variant, where ncu shows two resident CTAs; TMEM allows at most two)
+    const int v = cap < 0 ? -cap : (n > cap ? cap : (n > 0 ? n : 1));
+    c.per_sm.store(v, std::memory_order_release);
+    if (getenv("FNTGPU_DEBUG"))
+      fprintf(stderr, "tensor-core CDC kernel on device %d: smem %d B, %d CTAs/SM by occupancy, grid %d x %d SMs\n",
+              dev, smem, n, v, m);
+  }
+  per_sm = c.per_sm.load(std::memory_order_acquire);
+  sms = c.sms;
+  return cudaSuccess;
+}
+
 template <bool FAST>
 static cudaError_t launch_tc(const CdcArgs& A, cudaStream_t st) {
   constexpr int SMEM = (int)sizeof(TcTables) + (FAST ? 0 : 2 * CDC_BLK * UP * 4);
-  auto* k = k_cdc64_tc<FAST>;
-  static int grid_per_sm[2] = {0, 0};  // resident CTAs per SM (persistent grid)
-  static int sms = 0;
-  int& per_sm = grid_per_sm[FAST ? 1 : 0];
-  if (per_sm == 0) {
-    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
-    if (e == cudaSuccess)  // all of L1 as shared memory: the kernel streams, it does not cache
-      e = cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-    if (e != cudaSuccess) return e;
-    int dev = 0;
-    e = cudaGetDevice(&dev);
-    if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    int n = 0;
-    if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k, CDC_CTA, SMEM);
-    if (e != cudaSuccess) return e;
-    per_sm = n > 0 ? n : 1;
-  }
+  static TcLaunchCfg cfgs[64];
+  int per_sm = 0, sms = 0;
+  const cudaError_t e = tc_launch_cfg(cfgs, k_cdc64_tc<FAST>, SMEM, 3, per_sm, sms);
+  if (e != cudaSuccess) return e;
   const int64_t items = (A.blk_count + CDC_BLK - 1) / CDC_BLK * A.io.n_streams;
   const int64_t full = (int64_t)per_sm * sms;
   const unsigned grid = (unsigned)(items < full ? items : full);
-  k<<<grid, CDC_CTA, SMEM, st>>>(A);
+  k_cdc64_tc<FAST><<<grid, CDC_CTA, SMEM, st>>>(A);
   return cudaGetLastError();
 }
 
 template <bool FAST>
 static cudaError_t launch_umma(const CdcArgs& A, cudaStream_t st) {
   constexpr int SMEM = (int)sizeof(UmmaSmem) + (FAST ? 0 : 2 * CDC_BLK * UP * 4);
-  auto* k = k_cdc64_umma<FAST>;
-  static int grid_per_sm[2] = {0, 0};
-  static int sms = 0;
-  int& per_sm = grid_per_sm[FAST ? 1 : 0];
-  if (per_sm == 0) {
-    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
-    if (e == cudaSuccess)  // all of L1 as shared memory: the kernel streams, it does not cache
-      e = cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-    if (e != cudaSuccess) return e;
-    int dev = 0;
-    e = cudaGetDevice(&dev);
-    if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    int n = 0;
-    if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k, CDC_CTA, SMEM);
-    if (e != cudaSuccess) return e;
-    // 256 TMEM columns per CTA: two resident CTAs hold all 512 columns. The occupancy
-    // API reports 1 for the 85 KB fast variant although two fit (ncu: smem limit 2), so
-    // the grid is sized for two; an SM that cannot hold both runs the second later.
-    per_sm = FAST ? 2 : (n > 0 ? (n > 2 ? 2 : n) : 1);
-    if (getenv("FNTGPU_DEBUG"))
-      fprintf(stderr, "k_cdc64_umma<%d>: smem %d B, %d CTAs/SM by occupancy, grid %d x %d SMs\n", (int)FAST,
-              SMEM, n, per_sm, sms);
-  }
+  static TcLaunchCfg cfgs[64];
+  int per_sm = 0, sms = 0;
+  // 256 TMEM columns per CTA: two resident CTAs hold all 512 columns of an SM
+  const cudaError_t e = tc_launch_cfg(cfgs, k_cdc64_umma<FAST>, SMEM, FAST ? -2 : 2, per_sm, sms);
+  if (e != cudaSuccess) return e;
   const int64_t items = (A.blk_count + CDC_BLK - 1) / CDC_BLK * A.io.n_streams;
   const int64_t full = (int64_t)per_sm * sms;
   const unsigned grid = (unsigned)(items < full ? items : full);
-  k<<<grid, CDC_CTA, SMEM, st>>>(A);
+  k_cdc64_umma<FAST><<<grid, CDC_CTA, SMEM, st>>>(A);
   return cudaGetLastError();
 }
 

@@ -51,6 +51,31 @@ def test_plan_validation_codes_without_gpu():
     assert "power of two" in _lib.last_error()
 
 
+def test_cdc_kernel_selector_validation_without_gpu():
+    """fntgpu_cdc_taps.kernel: 0 auto, 1 shift-add, 2 mma.sync matrix form, 3 tcgen05
+    matrix form; anything else is rejected before any device work. The Python
+    selector maps the same names (cdc.set_cdc_kernel)."""
+    from paper_2405_04253_b200 import _lib, cdc
+    lib = _lib.load()
+    taps = _lib.CdcTaps()
+    taps.n_taps = 32
+    io = _lib.CdcIO()
+    for bad in (-1, 4, 99):
+        taps.kernel = bad
+        assert lib.fntgpu_cdc64_process(C.byref(taps), C.byref(io), None) == _lib.EINVAL
+        assert "kernel selector" in _lib.last_error()
+    assert cdc.CDC_KERNELS == {"auto": 0, "shift": 1, "tc": 2, "umma": 3}
+    prev = cdc.set_cdc_kernel("umma")
+    try:
+        with pytest.raises(ValueError):
+            cdc.set_cdc_kernel("cufft")
+    finally:
+        cdc.set_cdc_kernel(prev)
+    text = (ROOT / "include" / "fntgpu.h").read_text()
+    for name, code in (("AUTO", 0), ("SHIFT", 1), ("TC", 2), ("UMMA", 3)):
+        assert re.search(rf"#define FNTGPU_CDC_KERNEL_{name} {code}\b", text)
+
+
 @pytest.mark.skipif(HAS_CUDA, reason="checks the no-GPU behaviour")
 def test_no_cpu_fallback():
     import paper_2405_04253_b200 as P

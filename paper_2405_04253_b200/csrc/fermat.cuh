@@ -265,10 +265,14 @@ __device__ __forceinline__ void fnt_dit(uint32_t (&a)[N]) {
 // plain two's-complement arithmetic: while |values| * 2^e stays below 2^31 no
 // modular reduction is needed, so a butterfly is one shift and two adds (no
 // carries). Callers bound the magnitudes and move to Z/M with a bias add after.
-template <int N, int KIND, int S, int S_END>
+// BIAS (a multiple of F4 above the magnitude bound) is added to every output of the
+// last stage inside its 3-input adds, making the words non-negative residues of Z/M
+// for the modular stages that follow at no extra instruction.
+template <int N, int KIND, int S, int S_END, uint32_t BIAS = 0>
 __device__ __forceinline__ void fnt_stage_plain(uint32_t (&a)[N]) {
   constexpr int half = 1 << S;
   constexpr int step = N >> (S + 1);
+  constexpr uint32_t B = S + 1 == S_END ? BIAS : 0u;
 #pragma unroll
   for (int q = 0; q < N / 2; ++q) {
     const int g = (q / half) * 2 * half;
@@ -278,10 +282,10 @@ __device__ __forceinline__ void fnt_stage_plain(uint32_t (&a)[N]) {
     const int e = KIND == RADIX2 ? j * step : KIND == RADIX4 ? 2 * j * step : (j * step) / 2;
     static_assert(KIND != SQRT2 || ((N >> (S + 1)) % 2 == 0), "odd sqrt2 power in a plain stage");
     const uint32_t u = a[g + j], w = a[g + j + half] << e;
-    a[g + j] = u + w;
-    a[g + j + half] = u - w;
+    a[g + j] = u + w + B;
+    a[g + j + half] = u - w + B;
   }
-  if constexpr (S + 1 < S_END) fnt_stage_plain<N, KIND, S + 1, S_END>(a);
+  if constexpr (S + 1 < S_END) fnt_stage_plain<N, KIND, S + 1, S_END, BIAS>(a);
 }
 
 }  // namespace fntgpu

@@ -583,10 +583,9 @@ __device__ __forceinline__ void lane_forward(AeqScratch& S, int lane, int cur, c
     // non-negative residues of Z/M for stages 3-4
     fnt_stage<AEQ_N, RADIX2, false, true, false, 0, 1>(W);
 #if AEQ_PROBE != 2
-    fnt_stage_plain<AEQ_N, RADIX2, 1, 3>(W);
+    // + F4 * 8192 = 536 879 104 > 256 * 257 * 4097 on every output of stage 2
+    fnt_stage_plain<AEQ_N, RADIX2, 1, 3, F4 * 8192u>(W);
 #endif
-#pragma unroll
-    for (int k = 0; k < AEQ_N; ++k) W[k] += F4 * 8192u;  // 536 879 104 > 256 * 257 * 4097
 #if AEQ_PROBE != 2
     fnt_stage<AEQ_N, RADIX2, false, false, false, 3, -1, AEQ_TAP_CM>(W);
 #endif

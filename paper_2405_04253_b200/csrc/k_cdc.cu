@@ -434,9 +434,7 @@ __global__ void __launch_bounds__(CDC_CTA, CDC_MIN_CTAS) k_cdc64(const __grid_co
     // int8 planes: stages 0-1 (twiddles 1, 2^8) keep |values| < 2^26 in plain int32
     // arithmetic (no carries); a multiple of F4 above 2^26 then makes them
     // non-negative words of Z/M for stages 2-5
-    fnt_stage_plain<CDC_N, SQRT2, 0, 2>(a);
-#pragma unroll
-    for (int k = 0; k < CDC_N; ++k) a[k] += F4 * 1024u;
+    fnt_stage_plain<CDC_N, SQRT2, 0, 2, F4 * 1024u>(a);
     fnt_stage<CDC_N, SQRT2, false, false, false, 2, -1, CDC_FWD_CM>(a);
   } else {
     fnt_dit<CDC_N, SQRT2, false>(a);

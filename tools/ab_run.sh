@@ -11,7 +11,7 @@ try:
     d = json.load(open(f"gpurun_out/ab_{n}.json"))
     k = d["roofline"].get("kernels", {})
     aeq = k.get("k_aeq_process", {}).get("ms", float("nan"))
-    cdc = k.get("k_cdc64", {}).get("ms", float("nan"))
+    cdc = next((v.get("ms") for kk, v in k.items() if kk.startswith("k_cdc64")), float("nan"))
     print(f"{n:12s} step {d['ms_per_step']:8.2f} ms  value {d['value']:8.2f}  aeq {aeq:8.2f}  cdc {cdc:7.2f}  frac {d['roofline']['frac']:.3f}")
 except Exception as e:
     print(n, "FAILED", e, open(f"gpurun_out/ab_{n}.err").read()[-500:])

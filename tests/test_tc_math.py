@@ -182,3 +182,26 @@ def test_unrepresentable_residue_is_corrected():
     wr = npp._dec((npp.transform(npp.CDC64, (up + um) % F, True) * C_RE) % F, F)[:, HOP:]
     wi = npp._dec((npp.transform(npp.CDC64, (up - um) % F, True) * C_IM) % F, F)[:, HOP:]
     assert np.array_equal(zr, wr) and np.array_equal(zi, wi)
+
+
+def test_tc_form_extreme_windows():
+    """Windows at the int8 extremes (all -128, all 127, alternating) and the largest tap
+    spectra: the accumulator bounds asserted inside tc_blocks hold at the worst case and
+    the outputs still match the shift-add FNT path."""
+    rng = np.random.default_rng(23)
+    bp = rng.integers(0, F, N)
+    bm = rng.integers(0, F, N)
+    bp[:4] = F - 1
+    bm[:4] = 32768
+    wins = [np.full(N, -128), np.full(N, 127), np.where(np.arange(N) % 2, 127, -128),
+            np.where(np.arange(N) < 32, -128, 127)]
+    win_r = np.array([w for w in wins for _ in wins])
+    win_i = np.array([v for _ in wins for v in wins])
+    zr, zi = tc_blocks(win_r, win_i, bp, bm)
+    Xr = npp.transform(npp.CDC64, npp._enc(win_r, F))
+    Xi = npp.transform(npp.CDC64, npp._enc(win_i, F))
+    up = (((Xr + 256 * Xi) % F) * bp) % F
+    um = (((Xr - 256 * Xi) % F) * bm) % F
+    wr = npp._dec((npp.transform(npp.CDC64, (up + um) % F, True) * C_RE) % F, F)[:, HOP:]
+    wi = npp._dec((npp.transform(npp.CDC64, (up - um) % F, True) * C_IM) % F, F)[:, HOP:]
+    assert np.array_equal(zr, wr) and np.array_equal(zi, wi)

@@ -305,6 +305,9 @@ def main():
     ap.add_argument("--c4-samples", type=int, default=1 << 31, help="C4 samples per polarization")
     ap.add_argument("--no-alt", action="store_true", help="skip the direct-forward AEQ comparison")
     ap.add_argument("--no-quality", action="store_true", help="skip the on-device BER/EVM scoring")
+    ap.add_argument("--aeq-kernel", default="auto", choices=["auto", "warp", "pol"],
+                    help="FNT-AEQ stream layout: one warp per stream, two warps per stream (one per "
+                         "polarization), or auto (the split form below ~8 streams per SM)")
     ap.add_argument("--cdc-kernel", default="auto", choices=["auto", "umma", "tc", "shift"],
                     help="FNT-CDC kernel for the int8 planes: auto (measured-faster choice), shift-add "
                          "butterflies, or the split-integer matrix form on mma.sync (tc) / tcgen05 (umma)")
@@ -335,6 +338,8 @@ def main():
     from paper_2405_04253_b200.linkgen import DeviceLinkGenerator
     from paper_2405_04253_b200.stream import CdcAeqChain
     cdc_mod.set_cdc_kernel(args.cdc_kernel)
+    from paper_2405_04253_b200 import aeq as aeq_mod
+    aeq_mod.set_aeq_kernel(args.aeq_kernel)
 
     if args.config == "c4":
         run_c4(args, world, rank, local)

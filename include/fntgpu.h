@@ -200,7 +200,18 @@ typedef struct fntgpu_aeq_params {
   double radii[8];    /* sorted ring radii (aeq.py:50) */
   int32_t n_radii;    /* 1..8 */
   int32_t forward;    /* FNTGPU_AEQ_FWD_* */
+  int32_t kernel;     /* FNTGPU_AEQ_KERNEL_*: stream layout of fntgpu_aeq_process */
+  int32_t reserved;
 } fntgpu_aeq_params;
+/* Stream layout of the FNT-forward equalizer (same bits either way):
+ * AUTO  the polarization-split form when there are too few streams to fill the
+ *       GPU with one warp each (fewer than ~8 per SM), else one warp per stream;
+ * WARP  one warp per stream (k_aeq.cu), the throughput form;
+ * POL   two warps per stream, one per polarization's output pair (k_aeq_pol.cu),
+ *       the latency form. The DIRECT forward always runs one warp per stream. */
+#define FNTGPU_AEQ_KERNEL_AUTO 0
+#define FNTGPU_AEQ_KERNEL_WARP 1
+#define FNTGPU_AEQ_KERNEL_POL 2
 
 typedef struct fntgpu_aeq_state { /* device memory, one per stream */
   double w[4][4][16];             /* float taps (aeq.py:99) */

@@ -56,7 +56,8 @@ class DecimIO(C.Structure):
 
 class AeqParams(C.Structure):
     _fields_ = [("sig_scale", C.c_double), ("tap_scale", C.c_double), ("mu", C.c_double),
-                ("radii", C.c_double * 8), ("n_radii", C.c_int32), ("forward", C.c_int32)]
+                ("radii", C.c_double * 8), ("n_radii", C.c_int32), ("forward", C.c_int32),
+                ("kernel", C.c_int32), ("reserved", C.c_int32)]
 
 
 class AeqState(C.Structure):

@@ -82,6 +82,21 @@ class RvMimoTaps:
         return cls(w)
 
 
+AEQ_KERNELS = {"auto": 0, "warp": 1, "pol": 2}  # FNTGPU_AEQ_KERNEL_*
+_aeq_kernel = "auto"
+
+
+def set_aeq_kernel(name: str) -> str:
+    """Select the equalizer's stream layout for parameter blocks built afterwards
+    (auto / warp: one warp per stream / pol: two warps per stream, one per
+    polarization); returns the previous selection. Outputs are identical."""
+    global _aeq_kernel
+    if name not in AEQ_KERNELS:
+        raise ValueError(f"unknown AEQ kernel {name!r}: one of {sorted(AEQ_KERNELS)}")
+    prev, _aeq_kernel = _aeq_kernel, name
+    return prev
+
+
 def aeq_params(config: AeqConfig, forward: int | None = None) -> _lib.AeqParams:
     """The C-ABI parameter block for an AeqConfig."""
     prm = _lib.AeqParams()
@@ -95,6 +110,7 @@ def aeq_params(config: AeqConfig, forward: int | None = None) -> _lib.AeqParams:
         prm.radii[i] = float(r)
     prm.n_radii = int(radii.size)
     prm.forward = _lib.env_forward_mode() if forward is None else int(forward)
+    prm.kernel = AEQ_KERNELS[_aeq_kernel]
     return prm
 
 

@@ -325,6 +325,8 @@ static int check_aeq_params(const fntgpu_aeq_params* prm, const char* where) {
   if (prm->mu < 0) return fail(FNTGPU_EINVAL, "mu must be >= 0");
   if (prm->forward != FNTGPU_AEQ_FWD_FNT && prm->forward != FNTGPU_AEQ_FWD_DIRECT)
     return fail(FNTGPU_EINVAL, "%s: bad forward mode", where);
+  if (prm->kernel < FNTGPU_AEQ_KERNEL_AUTO || prm->kernel > FNTGPU_AEQ_KERNEL_POL)
+    return fail(FNTGPU_EINVAL, "%s: bad kernel selector", where);
   return FNTGPU_OK;
 }
 

@@ -149,10 +149,11 @@ __device__ __forceinline__ uint32_t f4_enc64(int64_t v) {
 //                 alpha^(2h) = 2^h, alpha^(2h+1) = 2^h * (2^12 - 2^4)
 //   kind RADIX4 : alpha = 2^2, N <= 16          alpha^e = 2^(2e)  (sub-transforms of
 //   kind RADIX16: alpha = 2^4, N <= 8           alpha^e = 2^(4e)   a 32-point one)
+//   kind RADIX256: alpha = 2^8, N <= 4          alpha^e = 2^(8e)
 // The result is returned as (value, negate) where negate means the caller must
 // use -value (absorbed by swapping the butterfly's add and subtract): a rotate
 // by r >= 16 equals -(rotate by r - 16) modulo F4.
-enum TwKind { RADIX2 = 0, SQRT2 = 1, RADIX16 = 2, RADIX4 = 3 };
+enum TwKind { RADIX2 = 0, SQRT2 = 1, RADIX16 = 2, RADIX4 = 3, RADIX256 = 4 };
 
 struct Tw {
   uint32_t v;
@@ -162,7 +163,7 @@ struct Tw {
 template <int KIND, int CM = FNT_CARRY_MODE>
 __device__ __forceinline__ Tw twiddle(uint32_t a, int e /* exponent of alpha, >= 0 */) {
   if (KIND != SQRT2) {
-    int r = (KIND == RADIX16 ? 4 * e : KIND == RADIX4 ? 2 * e : e) & 31;
+    int r = (KIND == RADIX256 ? 8 * e : KIND == RADIX16 ? 4 * e : KIND == RADIX4 ? 2 * e : e) & 31;
     if (r >= 16) return {m_rot(a, r - 16), true};
     return {m_rot(a, r), false};
   } else {

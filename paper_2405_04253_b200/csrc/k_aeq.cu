@@ -27,22 +27,16 @@
 //   contracted into FMA), correctly rounded division and ring decisions, numpy's einsum reduction order
 //   over m (two lanes of even/odd m, unrolled by 4) and numpy's
 //   pairwise order for the err_trace mean.
-#include <cmath>
-#include <cstring>
-
 // Pipe balance for this kernel (fermat.cuh): the AEQ's FMA pipe already carries the
 // residue products and the FP64 update's partner work, so the plain addc / subc
 // forms measure faster here (tools/ab_run.sh: 161 vs 165 ms at config 5).
 #ifndef FNT_CARRY_MODE
 #define FNT_CARRY_MODE 0
 #endif
-#include "fermat.cuh"
-#include "internal.h"
+#include "aeq_common.cuh"
 
 namespace fntgpu {
 
-constexpr int AEQ_L = 16;            // taps per filter = hop (aeq.py:45)
-constexpr int AEQ_N = 32;            // block length
 #ifndef AEQ_WARPS
 #define AEQ_WARPS 1                  // streams (warps) per CTA: one-warp CTAs schedule best
 #endif                               // (FNT 124.4 -> 121.7 ms, direct 83.6 -> 75.0 ms vs 4)
@@ -52,8 +46,6 @@ constexpr int AEQ_N = 32;            // block length
 // lines (4-warp CTAs: 161 -> 156 ms at config 5). One-warp CTAs do not need it.
 #define AEQ_LOCKSTEP (AEQ_WARPS > 1 ? 1 : 0)
 #endif
-constexpr int AEQ_TAP_MAX = 16383;   // TAP_MAG_MAX (aeq.py:26)
-constexpr int XF_LUT = 127;          // x / sig_scale table for |x| <= 127
 #ifndef AEQ_IFNT_CM
 #define AEQ_IFNT_CM FNT_CARRY_MODE   // carry form of the inverse transform (fermat.cuh)
 #endif
@@ -95,105 +87,6 @@ struct __align__(16) AeqScratch {
                               // stored twice: block b's samples j at 16 * parity + 15 - j (+ 32)
 };
 
-struct AeqArgs {
-  fntgpu_aeq_params prm;
-  fntgpu_aeq_io io;
-  double R2[8];               // radii[i] * radii[i] (nearest ** 2, aeq.py:58)
-  double T[8];                // ring decision thresholds on r2 (rde fast path, see rde_thresholds)
-  double D;                   // sig_scale * tap_scale (aeq.py:142)
-  double Dinv;                // RN(1 / D): y = y_int / D by one Markstein correction step
-  int32_t fast_rde;           // 1: ring chosen by comparing r2 with T[] (no sqrt)
-  int32_t fast_div;           // 1: D in [2^-500, 2^500] (div_D's correction step is exact)
-};
-
-__device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a, b); }
-__device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a, b); }
-__device__ __forceinline__ double dsub(double a, double b) { return __dsub_rn(a, b); }
-
-// sign-extended byte k (0..3, may be a runtime value) of w
-__device__ __forceinline__ int32_t sbyte(uint32_t w, uint32_t k) {
-  return (int32_t)(w << (24u - 8u * k)) >> 24;
-}
-
-// split_taps (fixedpoint.py:111-121): sign * (|w| >> 7) or sign * (|w| & 127)
-// (|w| < 2^14 always: taps are clipped to +-16383 and split_taps rejects larger)
-__device__ __forceinline__ int32_t tap_group(int32_t w, int g) {
-  const int32_t m = abs(w);
-  const int32_t v = (m >> (g ? 0 : 7)) & 127;
-  return w < 0 ? -v : v;
-}
-
-// rde_error (aeq.py:53-58) for one output pair (y_I, y_Q). The 3-ring case
-// (16QAM, qam16_radii) is unrolled; other ring counts loop.
-template <bool QUICK = false>
-__device__ __forceinline__ double rde(double yi, double yq, const AeqArgs& A) {
-  const double r2 = dadd(dmul(yi, yi), dmul(yq, yq));
-  double best_r2;
-  if (QUICK) {  // launch-time checked: fast_rde && n_radii == 3
-    best_r2 = r2 >= A.T[2] ? A.R2[2] : (r2 >= A.T[1] ? A.R2[1] : A.R2[0]);
-    return dsub(best_r2, r2);
-  }
-  if (A.fast_rde) {
-    // argmin_i |sqrt(r2) - R_i| is a step function of r2 over the reachable range;
-    // the host located its steps exactly (rde_thresholds), so no sqrt is needed.
-    if (A.prm.n_radii == 3) {
-      best_r2 = r2 >= A.T[2] ? A.R2[2] : (r2 >= A.T[1] ? A.R2[1] : A.R2[0]);
-    } else {
-      int sel = 0;
-      for (int i = 1; i < A.prm.n_radii; ++i) sel += r2 >= A.T[i];
-      best_r2 = A.R2[sel];
-    }
-    return dsub(best_r2, r2);
-  }
-  const double r = __dsqrt_rn(r2);
-  if (A.prm.n_radii == 3) {
-    const double d0 = fabs(dsub(r, A.prm.radii[0]));
-    const double d1 = fabs(dsub(r, A.prm.radii[1]));
-    const double d2 = fabs(dsub(r, A.prm.radii[2]));
-    // np.argmin: first minimum
-    const bool take1 = d1 < d0;
-    const double dm = take1 ? d1 : d0;
-    best_r2 = d2 < dm ? A.R2[2] : (take1 ? A.R2[1] : A.R2[0]);
-  } else {
-    int best = 0;
-    double bd = fabs(dsub(r, A.prm.radii[0]));
-    for (int i = 1; i < A.prm.n_radii; ++i) {
-      const double d = fabs(dsub(r, A.prm.radii[i]));
-      if (d < bd) { bd = d; best = i; }
-    }
-    best_r2 = A.R2[best];
-  }
-  return dsub(best_r2, r2);
-}
-
-// np.rint(w * tap_scale).astype(int64), then |.| > 16383 -> count and clip
-// (aeq.py:165-168). Values whose rint is not a representable int64 (|r| >= 2^63,
-// NaN) become INT64_MIN in numpy on x86-64: not counted, clipped to -16383.
-// cvt.rni.s32.f64 rounds half-to-even like np.rint and saturates, so |rint| > 16383
-// is read off the int32; |p| >= 2^63 exactly when |rint(p)| >= 2^63 (doubles there
-// are integers).
-__device__ __forceinline__ int32_t requantize_tap(double w, double tap_scale, uint32_t& sat) {
-  const double p = dmul(w, tap_scale);
-  const int32_t i = __double2int_rn(p);
-  const bool huge = !(fabs(p) < 9.2233720368547758e18);
-  const int32_t c = min(max(i, -AEQ_TAP_MAX), AEQ_TAP_MAX);
-  sat += (c != i) & !huge;  // clipped exactly when |rint| > 16383
-  return huge ? -AEQ_TAP_MAX : c;
-}
-
-// y_int / D correctly rounded: q0 = RN(y_int * RN(1/D)) is within 1 ulp of the
-// quotient, the residual y_int - q0 D is exact in one FMA, and one more FMA rounds
-// the corrected quotient (Markstein's theorem; no over/underflow for |y_int| < 2^32
-// and the D range the host admits). fntgpu_aeq_selfcheck (tests/test_gpu_parity.py)
-// checks it against IEEE division over every int32 numerator for the configured D.
-template <bool QUICK = false>
-__device__ __forceinline__ double div_D(int32_t yi, const AeqArgs& A) {
-  const double a = (double)yi;
-  if (!QUICK && !A.fast_div) return __ddiv_rn(a, A.D);
-  const double q0 = dmul(a, A.Dinv);
-  const double r = __fma_rn(-q0, A.D, a);
-  return __fma_rn(r, A.Dinv, q0);
-}
 
 // S.part row pairs: 64-bit stores of (v[m], v[m+1]) and loads of columns (m0, m0 + 1)
 __device__ __forceinline__ void part_store16(int32_t* row, const int32_t (&v)[AEQ_L]) {
@@ -204,37 +97,6 @@ __device__ __forceinline__ int2 part_pair(const int32_t* row, int m0) {
   return *reinterpret_cast<const int2*>(row + m0);
 }
 
-// Both 7-bit groups of a tap in one word: p = sign * (hi + lo * 2^16) with
-// hi = |w| >> 7, lo = |w| & 127 (fixedpoint.py:111-121). Since w = sign (128 hi + lo),
-// p = w * 2^16 - (w / 128) * (2^23 - 1) (C division truncates like sign * (|w| >> 7)).
-// Unpack: hi group = low 16 bits sign-extended (|hi| < 2^15); lo group =
-// (p + 2^15) >> 16 (the low half's sign borrow is cancelled by the rounding).
-__device__ __forceinline__ uint32_t pack_groups(int32_t w) {
-  return (uint32_t)(w * 65536 - (w / 128) * 8388607);
-}
-__device__ __forceinline__ int32_t unpack_group(uint32_t p, int g) {
-  return g ? ((int32_t)(p + 0x8000u) >> 16) : ((int32_t)(p << 16) >> 16);
-}
-
-// FNT forward with the transform-domain sum over input streams (AEQ_FUSE_T): taps
-// are kept as balanced base-64 digits instead, w = 64 a + b with b in [-32, 31] and
-// |a| <= 256, packed the same way: p = a + b 2^16 = w 2^16 - a (2^22 - 1), so
-// unpack_group gives a (g = 0) and b (g = 1).
-template <bool BAL>
-__device__ __forceinline__ uint32_t pack_taps(int32_t w) {
-  if (!BAL) return pack_groups(w);
-  return (uint32_t)(w * 65536 - ((w + 32) >> 6) * 4194303);
-}
-template <bool BAL>
-__device__ __forceinline__ int32_t unpack_tap(uint32_t p) {
-  return (BAL ? 64 : 128) * unpack_group(p, 0) + unpack_group(p, 1);
-}
-// the reference's split_taps group g of a packed tap (fixedpoint.py:111-121)
-template <bool BAL>
-__device__ __forceinline__ int32_t ref_group(uint32_t p, int g) {
-  if (!BAL) return unpack_group(p, g);
-  return tap_group(unpack_tap<true>(p), g);
-}
 
 // einsum("sm,tmk->stk") inner reduction over m in numpy's SSE2 order.
 __device__ __forceinline__ double einsum_m(const double (&P)[AEQ_L]) {
@@ -249,13 +111,6 @@ __device__ __forceinline__ double einsum_m(const double (&P)[AEQ_L]) {
   return dadd(c0, c1);
 }
 
-// x / sig_scale exactly as numpy's true_divide (IEEE). Inputs narrower than 16 bits
-// always hit the table; wider ones fall back to the division.
-template <bool NARROW>
-__device__ __forceinline__ double xf_of(int32_t x, const double* lut, double sig) {
-  if (NARROW) return lut[x + XF_LUT];
-  return (x >= -XF_LUT && x <= XF_LUT) ? lut[x + XF_LUT] : __ddiv_rn((double)x, sig);
-}
 
 // This lane's 8 taps k = 8g .. 8g+7 of filter (s, t): the 14-bit values in
 // registers, the float values in the warp's shared scratch (S.wf, lane-contiguous).
@@ -343,10 +198,12 @@ __device__ __forceinline__ void lane_update(const AeqArgs& A, AeqScratch& S, int
       const double w = dadd(S.wf[kk][lane], dmul(mu, gr));
       S.wf[kk][lane] = w;
       // requantize_tap without its per-tap |p| >= 2^63 test: such a p saturates the
-      // int32 conversion, so it is among the clipped taps settled below
-      const int32_t i = __double2int_rn(dmul(w, A.prm.tap_scale));
+      // int32 conversion, so it is among the clipped taps settled below; a NaN p
+      // converts to 0 (cvt.rni.s32.f64), so it is flagged explicitly
+      const double p = dmul(w, A.prm.tap_scale);
+      const int32_t i = __double2int_rn(p);
       const int32_t c = min(max(i, -AEQ_TAP_MAX), AEQ_TAP_MAX);
-      smask |= (uint32_t)(c != i) << kk;
+      smask |= (uint32_t)((c != i) | (p != p)) << kk;
       set_tap<BAL>(T, kk, c);
     }
     T.sat += __popc(smask);
@@ -1065,10 +922,27 @@ static cudaError_t launch_fwd(fntgpu_aeq_state* st, const AeqArgs& A, cudaStream
   return quick ? launch_fwd_q<FWD, true>(st, A, s) : launch_fwd_q<FWD, false>(st, A, s);
 }
 
+// Streams per SM below which AUTO runs the polarization-split kernel: one warp per
+// stream needs >= 12 warps per SM to saturate the issue slots.
+#ifndef AEQ_POL_AUTO_PER_SM
+#define AEQ_POL_AUTO_PER_SM 4
+#endif
+
+static bool use_pol_kernel(const fntgpu_aeq_params& prm, int64_t n_streams) {
+  if (prm.forward != FNTGPU_AEQ_FWD_FNT) return false;
+  if (prm.kernel == FNTGPU_AEQ_KERNEL_POL) return true;
+  if (prm.kernel == FNTGPU_AEQ_KERNEL_WARP) return false;
+  int dev = 0, sms = 148;
+  if (cudaGetDevice(&dev) == cudaSuccess)
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  return n_streams < (int64_t)AEQ_POL_AUTO_PER_SM * sms;
+}
+
 cudaError_t launch_aeq_process(fntgpu_aeq_state* st, const fntgpu_aeq_params& prm,
                                const fntgpu_aeq_io& io, cudaStream_t s) {
   if (io.n_streams <= 0) return cudaSuccess;
   const AeqArgs A = make_args(prm, &io);
+  if (use_pol_kernel(prm, io.n_streams)) return launch_aeq_pol(st, A, s);
   if (prm.forward == FNTGPU_AEQ_FWD_DIRECT) return launch_fwd<FNTGPU_AEQ_FWD_DIRECT>(st, A, s);
   return launch_fwd<FNTGPU_AEQ_FWD_FNT>(st, A, s);
 }

@@ -424,6 +424,16 @@ def test_cdc_bank_ranges_match_full_stream(cdc_kernel):
 AEQ_MODES = (0, 1)  # FNTGPU_AEQ_FWD_FNT, FNTGPU_AEQ_FWD_DIRECT
 
 
+@pytest.fixture(params=("warp", "pol"))
+def aeq_kernel(request):
+    """Every AEQ test runs through both stream layouts: one warp per stream
+    (k_aeq.cu) and two warps per stream, one per polarization (k_aeq_pol.cu)."""
+    from paper_2405_04253_b200 import aeq as A
+    prev = A.set_aeq_kernel(request.param)
+    yield request.param
+    A.set_aeq_kernel(prev)
+
+
 def _aeq(mu=1e-4, forward=0):
     cfg = P.AeqConfig(block_n=32, l_taps=16, mu=mu, sig_spec=P.QuantSpec(5, SIG_SCALE))
     return P.FntAeq(cfg, forward=forward)
@@ -431,7 +441,7 @@ def _aeq(mu=1e-4, forward=0):
 
 @pytest.mark.parametrize("forward", AEQ_MODES)
 @pytest.mark.parametrize("tag", ["a", "b"])
-def test_aeq_link_golden(golden, tag, forward):
+def test_aeq_link_golden(golden, tag, forward, aeq_kernel):
     g = golden("aeq")
     eq = _aeq(forward=forward)
     cfg = P.LinkConfig()
@@ -446,7 +456,7 @@ def test_aeq_link_golden(golden, tag, forward):
 
 
 @pytest.mark.parametrize("forward", AEQ_MODES)
-def test_aeq_saturation_noadapt_streaming(golden, forward):
+def test_aeq_saturation_noadapt_streaming(golden, forward, aeq_kernel):
     g = golden("aeq")
     eq = _aeq(mu=0.05, forward=forward)
     y = eq.process(g["c_q"])
@@ -470,7 +480,7 @@ def test_aeq_saturation_noadapt_streaming(golden, forward):
     assert np.array_equal(np.array(eq.err_trace), g["e_err"])
 
 
-def test_aeq_single_block_api(golden):
+def test_aeq_single_block_api(golden, aeq_kernel):
     g = golden("aeq")
     eq = _aeq()
     y, xb = eq.equalize_block(g["f_x"])
@@ -482,7 +492,7 @@ def test_aeq_single_block_api(golden):
 
 
 @pytest.mark.parametrize("forward", AEQ_MODES)
-def test_aeq_wide_inputs_match_oracle(forward):
+def test_aeq_wide_inputs_match_oracle(forward, aeq_kernel):
     """|x| up to 2^15: per-group residues wrap mod F exactly as the reference's."""
     rng = np.random.default_rng(3)
     x = rng.integers(-32768, 32769, (4, 16 * 40))
@@ -497,7 +507,7 @@ def test_aeq_wide_inputs_match_oracle(forward):
     assert np.array_equal(eq.w, oq.w)
 
 
-def test_aeq_bank_many_streams_vs_oracle():
+def test_aeq_bank_many_streams_vs_oracle(aeq_kernel):
     """The multi-stream kernel (one warp per stream) against the oracle on
     independent random streams with the LinkConfig gear-shift schedule."""
     import torch
@@ -523,7 +533,7 @@ def test_aeq_bank_many_streams_vs_oracle():
 
 
 @pytest.mark.parametrize("forward", AEQ_MODES)
-def test_aeq_wide_then_narrow_calls_vs_oracle(forward):
+def test_aeq_wide_then_narrow_calls_vs_oracle(forward, aeq_kernel):
     """A call with wide inputs leaves an out-of-int8 history; the next call with
     int8 inputs (DP4A direct form) must fall back for that history exactly."""
     rng = np.random.default_rng(46)
@@ -538,7 +548,7 @@ def test_aeq_wide_then_narrow_calls_vs_oracle(forward):
 
 
 @pytest.mark.parametrize("forward", AEQ_MODES)
-def test_aeq_bank_wide_int32_inputs_vs_oracle(forward):
+def test_aeq_bank_wide_int32_inputs_vs_oracle(forward, aeq_kernel):
     """int32 planar inputs up to |x| = 2^15 (group convolutions wrap mod F4 and are
     decoded one by one, as in the reference) through the multi-stream kernel's fast
     path (per-block mu, err_trace), against the oracle."""
@@ -565,7 +575,7 @@ def test_aeq_bank_wide_int32_inputs_vs_oracle(forward):
 
 @pytest.mark.parametrize("forward", AEQ_MODES)
 @pytest.mark.parametrize("case", ["bursts", "big_taps", "mu_zero", "int32"])
-def test_aeq_stream_sum_switching_vs_oracle(case, forward):
+def test_aeq_stream_sum_switching_vs_oracle(case, forward, aeq_kernel):
     """The FNT forward sums the four input streams before the inverse transform only
     when an exact range test passes (max |x| <= 16 over the block window and the
     tap-digit mass bound, k_aeq.cu fused_ok); otherwise it decodes per (s, t, group)
@@ -620,7 +630,7 @@ def test_aeq_stream_sum_switching_vs_oracle(case, forward):
     dict(radii=[0.1, 0.3, 0.5, 0.8, 1.0, 1.3, 1.6, 2.2]),     # 8 rings
     dict(no_err=True),                                        # 16QAM rings without err_trace
 ])
-def test_aeq_bank_other_parameters_vs_oracle(case):
+def test_aeq_bank_other_parameters_vs_oracle(case, aeq_kernel):
     """The equalizer kernel's general (runtime-parameter) path and its compile-time
     fast path with other rings / tap scales, against the oracle."""
     import torch
@@ -650,7 +660,7 @@ def test_aeq_bank_other_parameters_vs_oracle(case):
 
 # ------------------------------------------------------- CDC -> AEQ glue chain
 
-def test_chain_matches_reference_glue(golden, cdc_kernel):
+def test_chain_matches_reference_glue(golden, cdc_kernel, aeq_kernel):
     """CDC (fused requantization + decimation statistics) -> phase -> AEQ on the
     75 km / 45 deg link of fixture b: phase, requantized AEQ input and the AEQ
     outputs equal the reference's rx_frontend + run_single glue."""

@@ -133,7 +133,7 @@ typedef struct fntgpu_cdc_taps {
 
 typedef struct fntgpu_cdc_io {
   int32_t n_streams;          /* independent streams (polarizations / channels) */
-  int32_t in_dtype;           /* FNTGPU_I8 | FNTGPU_I32 | FNTGPU_I64 */
+  int32_t in_dtype;           /* FNTGPU_I8 | FNTGPU_I32 | FNTGPU_I64 | FNTGPU_F64 (quantized on load) */
   const void* xr;             /* stream s real part at xr + s * x_stride (elements) */
   const void* xi;
   int64_t x_stride;
@@ -168,6 +168,17 @@ typedef struct fntgpu_cdc_io {
   int32_t q_shift;
   int32_t pad2;
   int8_t q_tie[128];
+  /* float64 input (in_dtype FNTGPU_F64): the front-end samples are quantized on
+   * load, q = clip(sign(v) floor(|v| + 0.5), +-in_max) with v = x * in_scale
+   * (quantize_real, fixedpoint.py:51-60, as linksim.py:290-291 applies it before
+   * process_int); in_max <= 127. *in_clipped (device counter, optional) += the
+   * number of |q| > in_max among the samples [32 b_lo, 32 (b_hi + 1)) of the
+   * launched overlap-save blocks, within [0, length) and the given input window --
+   * the whole stream once for a full-range call (cdc.py:165-175). */
+  double in_scale;
+  int32_t in_max;
+  int32_t pad3;
+  unsigned long long* in_clipped;
 } fntgpu_cdc_io;
 
 /* process_int / process (cdc.py:165-180), any output sub-range of any number

@@ -154,17 +154,24 @@ def quantize(x, scale, max_int):
     return np.clip(v, -max_int, max_int).astype(np.int64)
 
 
-def front_end(rx, L: Link, use_np_sqrt=True):
-    """GSOP, RRC matched filter, unit power, 5-bit quantize -> [(xr, xi)] per pol."""
+def conditioned(rx, L: Link, use_np_sqrt=True):
+    """GSOP, RRC matched filter, unit power (linksim.py:272-277) -> complex128 per pol,
+    the float samples rx_frontend quantizes (linksim.py:289-291)."""
     mf = rrc(L.sps, L.span, L.rolloff)
     out = []
-    mx = (1 << (L.sig_bits - 1)) - 1
     for p in range(2):
         g = gs_orth(rx[p])
         m = circ(g, mf)
-        c = m / (np.sqrt(np.mean(np.abs(m) ** 2)) if use_np_sqrt else math.sqrt(np.mean(np.abs(m) ** 2)))
-        out.append((quantize(c.real, L.sig_scale, mx), quantize(c.imag, L.sig_scale, mx)))
+        out.append(m / (np.sqrt(np.mean(np.abs(m) ** 2)) if use_np_sqrt
+                        else math.sqrt(np.mean(np.abs(m) ** 2))))
     return out
+
+
+def front_end(rx, L: Link, use_np_sqrt=True):
+    """GSOP, RRC matched filter, unit power, 5-bit quantize -> [(xr, xi)] per pol."""
+    mx = (1 << (L.sig_bits - 1)) - 1
+    return [(quantize(c.real, L.sig_scale, mx), quantize(c.imag, L.sig_scale, mx))
+            for c in conditioned(rx, L, use_np_sqrt)]
 
 
 def config2():
@@ -174,6 +181,15 @@ def config2():
     bits, sym, wave = transmit(L, rng)
     rx = channel(wave, L, rng)
     return L, bits, sym, front_end(rx, L)
+
+
+def config2_float():
+    """Config 2's front-end float samples (complex128 per pol) before the 5-bit quantizer."""
+    L = Link(2 ** 18, 75.0, 1, snr_db=20.0, rotation_deg=0.0, dgd=0.0, skew=0.0)
+    rng = np.random.default_rng(np.random.SeedSequence([1, 20000]))
+    bits, sym, wave = transmit(L, rng)
+    rx = channel(wave, L, rng)
+    return L, conditioned(rx, L)
 
 
 def config3(snr_db: float):

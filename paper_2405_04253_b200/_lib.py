@@ -46,7 +46,9 @@ class CdcIO(C.Structure):
                 ("yr", vp), ("yi", vp), ("y_stride", C.c_int64), ("inv_scale", C.c_double),
                 ("qr", vp), ("qi", vp), ("q_stride", C.c_int64), ("q_scale", C.c_double),
                 ("q_max", C.c_int32), ("pad1", C.c_int32), ("decim_acc", vp),
-                ("q_shift", C.c_int32), ("pad2", C.c_int32), ("q_tie", C.c_int8 * 128)]
+                ("q_shift", C.c_int32), ("pad2", C.c_int32), ("q_tie", C.c_int8 * 128),
+                ("in_scale", C.c_double), ("in_max", C.c_int32), ("pad3", C.c_int32),
+                ("in_clipped", vp)]
 
 
 class DecimIO(C.Structure):

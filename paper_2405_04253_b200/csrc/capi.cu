@@ -278,8 +278,11 @@ int fntgpu_cdc64_process(const fntgpu_cdc_taps* taps, const fntgpu_cdc_io* io, v
     return fail(FNTGPU_EINVAL, "cdc64_process: output range [%lld, %lld) outside [0, %lld)",
                 (long long)io->out_first, (long long)(io->out_first + io->out_count),
                 (long long)io->length);
-  if (io->in_dtype != FNTGPU_I8 && io->in_dtype != FNTGPU_I32 && io->in_dtype != FNTGPU_I64)
-    return fail(FNTGPU_EINVAL, "cdc64_process: in_dtype must be I8, I32 or I64");
+  if (io->in_dtype != FNTGPU_I8 && io->in_dtype != FNTGPU_I32 && io->in_dtype != FNTGPU_I64 &&
+      io->in_dtype != FNTGPU_F64)
+    return fail(FNTGPU_EINVAL, "cdc64_process: in_dtype must be I8, I32, I64 or F64");
+  if (io->in_dtype == FNTGPU_F64 && (io->in_max < 0 || io->in_max > 127))
+    return fail(FNTGPU_EINVAL, "cdc64_process: float64 input needs 0 <= in_max <= 127 (int8 staging)");
   if (!io->xr || !io->xi) return fail(FNTGPU_EINVAL, "cdc64_process: NULL input");
   // every input sample the range needs (x[n - 16 .. n + 16] for c = 16, widened to
   // whole overlap-save blocks) must be present where it lies inside [0, L)

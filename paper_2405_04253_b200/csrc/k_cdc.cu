@@ -111,6 +111,62 @@ __device__ __forceinline__ void stage_plane(TS* dst, const TIN* src, int64_t g0,
   }
 }
 
+// Float64 front-end samples quantized on load (in_dtype FNTGPU_F64): quantize_real
+// (fixedpoint.py:51-60) with in_scale / in_max, v = x * scale, q = sign(v) floor(|v| +
+// 0.5), clipped when |q| > in_max, then clipped to +-in_max -- the float64 steps of
+// k_quant.cu (identical bits), fused into the staging of the CDC input window, so the
+// float samples cross HBM once and the int8 planes never exist in global memory.
+// Returns the clip count over the window positions [own_lo, own_hi) (global indices).
+__device__ __forceinline__ int8_t quant_in(double x, double scale, double mx, uint32_t& clip) {
+  const double v = __dmul_rn(x, scale);
+  const double a = floor(__dadd_rn(fabs(v), 0.5));
+  double r = v > 0 ? a : (v < 0 ? -a : 0.0);
+  clip = fabs(r) > mx;
+  r = r > mx ? mx : (r < -mx ? -mx : r);
+  return (int8_t)(int)r;
+}
+
+__device__ __forceinline__ uint32_t stage_plane_f64(int8_t* dst, const double* src, int64_t g0,
+                                                    const fntgpu_cdc_io& io, int64_t own_lo,
+                                                    int64_t own_hi) {
+  const int64_t lo = io.x_first > 0 ? io.x_first : 0;
+  const int64_t hi_avail = io.x_first + io.x_count;
+  const int64_t hi = hi_avail < io.length ? hi_avail : io.length;
+  const double mx = (double)io.in_max;
+  uint32_t clips = 0;
+  constexpr int CH = WIN / 16;
+  for (int ch = threadIdx.x; ch < CH; ch += blockDim.x) {
+    const int64_t g = g0 + 16 * ch;
+    const double* p = src + (g - io.x_first);
+    uint32_t w[4] = {0u, 0u, 0u, 0u};
+    if (g >= lo && g + 16 <= hi && ((reinterpret_cast<uintptr_t>(p) & 15) == 0)) {
+      const bool own = g >= own_lo && g + 16 <= own_hi;
+#pragma unroll
+      for (int k2 = 0; k2 < 8; ++k2) {
+        const double2 v = __ldg(reinterpret_cast<const double2*>(p) + k2);
+        uint32_t c0, c1;
+        const int8_t q0 = quant_in(v.x, io.in_scale, mx, c0), q1 = quant_in(v.y, io.in_scale, mx, c1);
+        const int k = 2 * k2;
+        w[k >> 2] |= (((uint32_t)(uint8_t)q0) | ((uint32_t)(uint8_t)q1 << 8)) << (8 * (k & 3));
+        if (own) clips += c0 + c1;
+        else clips += (c0 & (g + k >= own_lo && g + k < own_hi)) + (c1 & (g + k + 1 >= own_lo && g + k + 1 < own_hi));
+      }
+    } else {
+      for (int k = 0; k < 16; ++k) {
+        const int64_t gk = g + k;
+        if (gk >= lo && gk < hi) {
+          uint32_t c;
+          const int8_t q = quant_in(src[gk - io.x_first], io.in_scale, mx, c);
+          w[k >> 2] |= ((uint32_t)(uint8_t)q) << (8 * (k & 3));
+          clips += c & (gk >= own_lo && gk < own_hi);
+        }
+      }
+    }
+    reinterpret_cast<uint4*>(dst)[ch] = make_uint4(w[0], w[1], w[2], w[3]);
+  }
+  return clips;
+}
+
 // Exact integer form of the AEQ-input requantization q = quantize_real(y * inv, q_scale)
 // when inv * q_scale == 2^-k up to rounding: the float64 product is within 3 ulp of
 // y / 2^k, so round-half-away agrees with the exact rounding except at exact ties
@@ -348,7 +404,8 @@ __device__ __forceinline__ int32_t sx8(uint32_t w, int k) {
 
 template <typename TIN, bool FAST>
 __global__ void __launch_bounds__(CDC_CTA, CDC_MIN_CTAS) k_cdc64(const __grid_constant__ CdcArgs A) {
-  using TS = typename std::conditional<sizeof(TIN) == 1, int8_t, int32_t>::type;
+  constexpr bool F64IN = std::is_same<TIN, double>::value;  // quantized on load to int8
+  using TS = typename std::conditional<sizeof(TIN) == 1 || F64IN, int8_t, int32_t>::type;
   // the input window and the u staging rows are never live at the same time
   extern __shared__ __align__(16) unsigned char smem[];
   TS* s_xr = reinterpret_cast<TS*>(smem);
@@ -393,7 +450,21 @@ __global__ void __launch_bounds__(CDC_CTA, CDC_MIN_CTAS) k_cdc64(const __grid_co
       }
     }
   }
-  if (!bulk) {
+  if constexpr (F64IN) {
+    // this CTA's own samples (second halves of its launched blocks): each sample of
+    // the launch is counted once
+    const int64_t own_lo = cta_blk0 * CDC_HOP;
+    const int64_t blk_end = A.blk_begin + A.blk_count;
+    const int64_t own_hi = (cta_blk0 + CDC_BLK < blk_end ? cta_blk0 + CDC_BLK : blk_end) * CDC_HOP;
+    uint32_t clips = stage_plane_f64(reinterpret_cast<int8_t*>(s_xr), reinterpret_cast<const double*>(xr_s),
+                                     g0, io, own_lo, own_hi);
+    clips += stage_plane_f64(reinterpret_cast<int8_t*>(s_xi), reinterpret_cast<const double*>(xi_s), g0,
+                             io, own_lo, own_hi);
+    if (io.in_clipped) {
+      clips = __reduce_add_sync(0xffffffffu, clips);
+      if ((threadIdx.x & 31) == 0 && clips) atomicAdd(io.in_clipped, (unsigned long long)clips);
+    }
+  } else if (!bulk) {
     stage_plane<TIN, TS>(s_xr, xr_s, g0, io);
     stage_plane<TIN, TS>(s_xi, xi_s, g0, io);
   }
@@ -1422,7 +1493,8 @@ static inline void scale_taps(const uint32_t* src, uint32_t* dst) {
 
 template <typename TIN, bool FAST>
 static cudaError_t launch_k(const CdcArgs& A, dim3 grid, cudaStream_t st) {
-  using TS = typename std::conditional<sizeof(TIN) == 1, int8_t, int32_t>::type;
+  using TS = typename std::conditional<sizeof(TIN) == 1 || std::is_same<TIN, double>::value,
+                                       int8_t, int32_t>::type;
   constexpr int IN_BYTES = 2 * WIN * (int)sizeof(TS);
   constexpr int U_BYTES = 2 * CDC_BLK * UP * 4;
   constexpr int SMEM = IN_BYTES > U_BYTES ? IN_BYTES : U_BYTES;
@@ -1532,16 +1604,16 @@ cudaError_t launch_cdc64(const fntgpu_cdc_taps& taps, const fntgpu_cdc_io& io, c
   if (io.out_dtype == FNTGPU_I16)
     fast = fast && (reinterpret_cast<uintptr_t>(io.yr) & 7) == 0 &&
            (reinterpret_cast<uintptr_t>(io.yi) & 7) == 0 && io.y_stride % 4 == 0;
-  if (io.in_dtype != FNTGPU_I8 && io.in_dtype != FNTGPU_I32 && io.in_dtype != FNTGPU_I64)
+  if (io.in_dtype != FNTGPU_I8 && io.in_dtype != FNTGPU_I32 && io.in_dtype != FNTGPU_I64 &&
+      io.in_dtype != FNTGPU_F64)
     return cudaErrorInvalidValue;
-  // tensor-core forms for int8 planes (their samples are the int8 MMA operands). Auto
-  // picks what measured fastest on B200 (profiles/cdc_tc_r01.json): the tcgen05 form
-  // for the fast epilogues (config 4 int16 outputs: 24.1 vs 25.7 ms; config 5 fused
-  // requantization + statistics: 31.1 vs 31.4 ms), the shift-add kernel for every other
-  // output or input type. mma.sync (TC) only on request (0.87-0.90x).
+  // Tensor-core forms for int8 planes (their samples are the int8 MMA operands), on
+  // request only. Auto runs the shift-add butterflies: the tcgen05 form measured
+  // 1.07x at config 4 and 1.01x in the config-5 chain (profiles/cdc_tc_r01.json), below
+  // the 1.15x that would justify its TMEM / residency assumptions as the default
+  // (DESIGN.md section 3); mma.sync measured 0.87-0.90x.
   int kern = taps.kernel;
-  if (kern == FNTGPU_CDC_KERNEL_AUTO)
-    kern = (io.in_dtype == FNTGPU_I8 && fast) ? FNTGPU_CDC_KERNEL_UMMA : FNTGPU_CDC_KERNEL_SHIFT;
+  if (kern == FNTGPU_CDC_KERNEL_AUTO) kern = FNTGPU_CDC_KERNEL_SHIFT;
   if (io.in_dtype == FNTGPU_I8 && kern == FNTGPU_CDC_KERNEL_TC) {
     A.s_base = 0;
     return fast ? launch_tc<true>(A, st) : launch_tc<false>(A, st);
@@ -1559,6 +1631,9 @@ cudaError_t launch_cdc64(const fntgpu_cdc_taps& taps, const fntgpu_cdc_io& io, c
         e = fast ? launch_k<int8_t, true>(A, grid, st) : launch_k<int8_t, false>(A, grid, st);
         break;
       case FNTGPU_I32: e = launch_k<int32_t, false>(A, grid, st); break;
+      case FNTGPU_F64:
+        e = fast ? launch_k<double, true>(A, grid, st) : launch_k<double, false>(A, grid, st);
+        break;
       default: e = launch_k<int64_t, false>(A, grid, st); break;
     }
     if (e != cudaSuccess) return e;

@@ -10,8 +10,17 @@ with circular FFT filtering as there.
 
 This is data generation, not the product path: it uses PyTorch tensors and
 cuFFT (library code) and is statistically, not bitwise, equivalent to the
-reference's numpy generator (different RNG). Bit-exact parity tests use inputs
-produced by the reference itself (tests/golden/).
+reference's numpy generator (different RNG; tests/test_gpu_linkgen.py compares
+the level histograms and spectra with oracle/linkgen_np, the pinned restatement
+of the reference generator). Bit-exact parity tests use inputs produced by the
+reference itself (tests/golden/).
+
+Randomness is counter-based: torch's CUDA generator is Philox4x32-10, and every
+group of `chunk` links is drawn from a generator keyed by (seed, global index of
+the group's first link) -- never by rank or shard. A shard [first, first + n)
+therefore holds exactly the links an unsharded run holds at those indices, for
+any number of GPUs (config 5 strong scaling; config 4 keys its segments the same
+way by global segment index).
 """
 
 from __future__ import annotations
@@ -49,7 +58,7 @@ class DeviceLinkGenerator:
     def __init__(self, n_symbols: int, z_km: float = 75.0, baud: float = 40e9, sps: int = 2,
                  rolloff: float = 0.1, span: int = 64, dispersion_ps_nm_km: float = 17.0,
                  wavelength_nm: float = 1550.0, sig_scale: float | None = None,
-                 sig_bits: int = 5):
+                 sig_bits: int = 5, dgd_symbols: float = 0.0, iq_skew_samples: float = 0.0):
         t = _lib.torch()
         dev = _lib.device()
         self.n_sym = n_symbols
@@ -69,15 +78,25 @@ class DeviceLinkGenerator:
         lam = wavelength_nm * 1e-9
         phase = math.pi * lam * lam * (dispersion_ps_nm_km * 1e-6) * (z_km * 1e3) / SPEED_OF_LIGHT
         self.H_tx = self.H_rrc * t.exp(-1j * phase * f * f)  # shaping + dispersion
+        # DGD: pol X delayed by +tau, pol Y by -tau samples (apply_channel, linksim.py:220-222);
+        # IQ skew: the quadrature part delayed by iq_skew samples (linksim.py:227-229)
+        fn = t.fft.fftfreq(L, dtype=t.float64, device=dev)
+        tau = dgd_symbols * sps / 2.0
+        self.H_pol = None
+        if tau:
+            self.H_pol = t.stack([t.exp(-2j * math.pi * fn * tau), t.exp(2j * math.pi * fn * tau)])
+        self.H_skew = t.exp(-2j * math.pi * fn * iq_skew_samples) if iq_skew_samples else None
         self.levels = t.tensor([-3.0, -1.0, 3.0, 1.0], dtype=t.float64, device=dev) / math.sqrt(10.0)
 
     def generate(self, n_links: int, seed: int, snr_db=(16.0, 22.0), chunk: int = 32,
-                 out=None, symbols: bool = False):
-        """Returns (xr, xi): (2*n_links, L) int8 device tensors; row 2l = pol X of
-        link l, row 2l+1 = pol Y. Deterministic for a given (seed, link index).
-        With symbols=True also returns the transmitted symbol indices
-        (n_links, 2, n_sym) uint8 = 4*li_I + li_Q with Gray level index li = 2 b0 + b1
-        (the reference's bits_to_symbols, linksim.py:107-112)."""
+                 out=None, symbols: bool = False, first_link: int = 0):
+        """Returns (xr, xi): (2*n_links, L) int8 device tensors for the links with
+        global indices [first_link, first_link + n_links); row 2l = pol X of link l,
+        row 2l+1 = pol Y. Link i's samples depend only on (seed, i) (and `chunk`):
+        the Philox generator of each aligned group of `chunk` links is keyed by the
+        group's global index. With symbols=True also returns the transmitted symbol
+        indices (n_links, 2, n_sym) uint8 = 4*li_I + li_Q with Gray level index
+        li = 2 b0 + b1 (the reference's bits_to_symbols, linksim.py:107-112)."""
         t = _lib.torch()
         dev = _lib.device()
         L = self.L
@@ -87,15 +106,17 @@ class DeviceLinkGenerator:
         else:
             xr, xi = out
         sidx = t.empty((n_links, 2, self.n_sym), dtype=t.uint8, device=dev) if symbols else None
-        for c0 in range(0, n_links, chunk):
-            c = min(chunk, n_links - c0)
+        end = first_link + n_links
+        for g0 in range(first_link - first_link % chunk, end, chunk):
             g = t.Generator(device=dev)
-            g.manual_seed(int(seed) * 1_000_003 + c0)
-            xq_r, xq_i, li = self._chunk(c, g, snr_db)
-            xr[2 * c0:2 * (c0 + c)] = xq_r.reshape(2 * c, L)
-            xi[2 * c0:2 * (c0 + c)] = xq_i.reshape(2 * c, L)
+            g.manual_seed(int(seed) * 1_000_003 + g0)
+            xq_r, xq_i, li = self._chunk(chunk, g, snr_db)
+            a, b = max(g0, first_link), min(g0 + chunk, end)   # global links kept
+            ra, rb = a - g0, b - g0                            # rows of the group
+            xr[2 * (a - first_link):2 * (b - first_link)] = xq_r[ra:rb].reshape(2 * (b - a), L)
+            xi[2 * (a - first_link):2 * (b - first_link)] = xq_i[ra:rb].reshape(2 * (b - a), L)
             if symbols:
-                sidx[c0:c0 + c] = li
+                sidx[a - first_link:b - first_link] = li[ra:rb]
         return (xr, xi, sidx) if symbols else (xr, xi)
 
     def tx_reference(self, sidx):
@@ -117,7 +138,8 @@ class DeviceLinkGenerator:
         sym_q = self.levels[li_q]
         up = t.zeros((c, 2, L), dtype=t.complex128, device=dev)
         up[..., ::self.sps] = t.complex(sym_i, sym_q)
-        w = t.fft.ifft(t.fft.fft(up) * self.H_tx)
+        Hx = self.H_tx if self.H_pol is None else self.H_tx * self.H_pol
+        w = t.fft.ifft(t.fft.fft(up) * Hx)
         del up
         w = w / t.sqrt(t.mean(w.abs() ** 2, dim=-1, keepdim=True))
         # Haar-random 2x2 unitary per link (QR of a complex Ginibre matrix, phase-fixed)
@@ -127,6 +149,8 @@ class DeviceLinkGenerator:
         d = t.diagonal(r, dim1=-2, dim2=-1)
         q = q * (d / d.abs()).unsqueeze(-2)
         w = t.matmul(q, w)
+        if self.H_skew is not None:
+            w = t.complex(w.real, t.fft.ifft(t.fft.fft(w.imag) * self.H_skew).real)
         lo, hi = snr_db
         snr = 10.0 ** ((lo + (hi - lo) * t.rand((c, 1, 1), generator=g, device=dev,
                                                    dtype=t.float64)) / 10.0)

@@ -39,7 +39,7 @@ def _code(t) -> int:
     if _TORCH2CODE is None:
         tt = _t()
         _TORCH2CODE = {tt.int8: _lib.I8, tt.int16: _lib.I16, tt.int32: _lib.I32,
-                       tt.int64: _lib.I64, tt.complex128: _lib.C128}
+                       tt.int64: _lib.I64, tt.float64: _lib.F64, tt.complex128: _lib.C128}
     return _TORCH2CODE[t.dtype]
 
 
@@ -76,12 +76,16 @@ class CdcBank:
 
     def run(self, xr, xi, *, length: int | None = None, x_first: int = 0,
             out_first: int = 0, out_count: int | None = None, yr=None, yi=None,
-            qr=None, qi=None, q_spec=None, decim_acc=None, stream=None) -> None:
+            qr=None, qi=None, q_spec=None, decim_acc=None, in_spec=None, in_clipped=None,
+            stream=None) -> None:
         """xr, xi: (S, Lx) int8/int32/int64 device tensors holding global samples
-        [x_first, x_first + Lx) of S streams of length `length`. Outputs for the
-        global range [out_first, out_first + out_count) go to yr/yi (S, out_count)
-        (int16/int32/int64, or complex128 in yr) and/or the fused int8 requantized
-        planes qr/qi, and/or the decimation statistics decim_acc (S*8 uint64)."""
+        [x_first, x_first + Lx) of S streams of length `length`, or float64 front-end
+        samples quantized on load with `in_spec` (quantize_real, fixedpoint.py:51-60;
+        in_clipped: optional int64 device counter receiving the clip count). Outputs
+        for the global range [out_first, out_first + out_count) go to yr/yi
+        (S, out_count) (int16/int32/int64, or complex128 in yr) and/or the fused int8
+        requantized planes qr/qi, and/or the decimation statistics decim_acc (S*8
+        uint64)."""
         S, Lx = xr.shape
         length = Lx if length is None else length
         out_count = length - out_first if out_count is None else out_count
@@ -108,9 +112,63 @@ class CdcBank:
             self._exact_requant(io, q_spec)
         if decim_acc is not None:
             io.decim_acc = decim_acc.data_ptr()
+        if io.in_dtype == _lib.F64:
+            if in_spec is None:
+                raise ValueError("float64 CDC input needs in_spec (the front-end QuantSpec)")
+            io.in_scale = float(in_spec.scale)
+            io.in_max = int(in_spec.max_int)
+            io.in_clipped = in_clipped.data_ptr() if in_clipped is not None else None
         lib = _lib.load()
         st = _lib.vp(stream.cuda_stream) if stream is not None else _lib.stream_handle()
         _lib.check(lib.fntgpu_cdc64_process(C.byref(self.taps), C.byref(io), st), "cdc64_process")
+
+
+#: Relative gap |m0 - m1| / max(m0, m1) between the two phase metrics below which the
+#: device's decision (exact integer statistics, k_cdc.cu k_decim_phase) may differ from
+#: the reference's float64 evaluation: its pairwise means and ratios carry a relative
+#: error of at most a few 1e-14, so 1e-12 leaves a wide margin.
+#: A NaN gap (an all-zero link: 0 / 0 in the reference) is treated as a tie as well.
+PHASE_TIE_GUARD = 1e-12
+
+
+def reference_phase(streams, sps: int = 2) -> int:
+    """linksim._decimation_phase (linksim.py:249-260) in the reference's own float64
+    numpy expression: the sampling phase minimizing sum over streams of
+    mean|d|^4 / mean(|d|^2)^2, first minimum on ties (and phase 0 for NaN metrics)."""
+    best, best_phase = None, 0
+    for ph in range(sps):
+        metric = 0.0
+        for s in streams:
+            d = s[ph::sps]
+            p2 = np.mean(np.abs(d) ** 2)
+            metric += np.mean(np.abs(d) ** 4) / (p2 * p2)
+        if best is None or metric < best:
+            best, best_phase = metric, ph
+    return best_phase
+
+
+def resolve_phase_ties(bank: "CdcBank", xr, xi, length: int, phase, gap,
+                       guard: float | None = None) -> list[int]:
+    """Links whose device phase decision is within float rounding of a tie get the
+    reference's float64 decision: their CDC outputs (both polarizations, rows 2l and
+    2l + 1 of xr / xi) are recomputed on the device and the metric is evaluated as
+    linksim.py:249-260 does. Returns the resolved link indices (normally none).
+    Synchronizes the current stream (one small device-to-host read of `gap`)."""
+    t = _t()
+    guard = PHASE_TIE_GUARD if guard is None else guard
+    g = gap.cpu().numpy()
+    idx = [int(i) for i in np.nonzero(~(g >= guard))[0]]
+    if not idx:
+        return idx
+    inv = 1.0 / bank.engine.output_scale
+    for l in idx:
+        yr = t.empty((2, length), dtype=t.int32, device=xr.device)
+        yi = t.empty_like(yr)
+        bank.run(xr[2 * l:2 * l + 2], xi[2 * l:2 * l + 2], length=length, yr=yr, yi=yi)
+        ar, ai = yr.cpu().numpy().astype(np.int64), yi.cpu().numpy().astype(np.int64)
+        streams = [ar[p] * inv + 1j * (ai[p] * inv) for p in range(2)]  # cdc.py:177-180
+        phase[l] = reference_phase(streams)
+    return idx
 
 
 def decimation_phase(acc, n_links: int, length: int, phase_out, gap_out=None, stream=None) -> None:
@@ -199,8 +257,11 @@ class CdcAeqChain:
     AEQ outputs [XI, XQ, YI, YQ]; err (n_links, n_blocks) the err_trace."""
 
     def __init__(self, engine: FntCdcEngine, aeq_config: AeqConfig, n_links: int, length: int,
-                 sig_spec, mu_schedule=None, forward: int | None = None, keep_cdc_int=False):
+                 sig_spec, mu_schedule=None, forward: int | None = None, keep_cdc_int=False,
+                 tie_guard: bool = True):
         t = _t()
+        self.tie_guard = tie_guard
+        self.resolved: list[int] = []  # links whose phase the last run decided on the host
         dev = _lib.device()
         if length % 2:
             raise NotImplementedError("the chain runs 2 sps streams of even length")
@@ -239,8 +300,19 @@ class CdcAeqChain:
         self.cdc.run(xr, xi, length=self.L, yr=yr, yi=yi, qr=self.qr, qi=self.qi,
                      q_spec=self.sig_spec, decim_acc=self.acc, stream=stream)
         decimation_phase(self.acc, self.n_links, self.L, self.phase, self.gap, stream=stream)
+        if self.tie_guard:
+            self.check_ties(xr, xi, stream)
         self.aeq.run_decim(self.qr, self.qi, self.phase, self.n_blocks, self.y, adapt=True,
                            mu_blocks=self.mu_blocks, err=self.err, stream=stream)
+
+    def check_ties(self, xr, xi, stream=None) -> None:
+        """Tie guard of the decimation phase (resolve_phase_ties); waits for the CDC."""
+        t = _t()
+        if stream is not None:
+            with t.cuda.stream(stream):
+                self.resolved = resolve_phase_ties(self.cdc, xr, xi, self.L, self.phase, self.gap)
+        else:
+            self.resolved = resolve_phase_ties(self.cdc, xr, xi, self.L, self.phase, self.gap)
 
 
 def _segments(total: int, parts: int, align: int) -> list[tuple[int, int]]:
@@ -336,6 +408,8 @@ class HostChain:
                            decim_acc=ch.acc, stream=self.s_cmp)
             self.e_cdc.record(self.s_cmp)
             decimation_phase(ch.acc, ch.n_links, self.L, ch.phase, ch.gap, stream=self.s_cmp)
+            if ch.tie_guard:
+                ch.check_ties(self.dxr, self.dxi, self.s_cmp)
             # -- AEQ time segments; segment j's outputs may be overwritten only after the
             #    previous call copied them out
             for j, (b0, b1) in enumerate(self.segs):

@@ -24,14 +24,15 @@ def _json_line(out: str) -> dict:
 
 
 def test_bench_single_gpu_line():
-    r = subprocess.run([sys.executable, "bench.py", "--links", "128", "--steps", "1", "--warmup", "1",
-                        "--no-cpu", "--e2e-links", "64"], cwd=ROOT, capture_output=True, text=True,
-                       timeout=900)
+    r = subprocess.run([sys.executable, "bench.py", "--links", "128", "--symbols", "32768", "--steps", "1",
+                        "--warmup", "1", "--no-cpu", "--no-sub"], cwd=ROOT, capture_output=True,
+                       text=True, timeout=900)
     assert r.returncode == 0, r.stderr[-2000:]
     d = _json_line(r.stdout)
-    assert KEYS <= set(d) and d["n_gpus"] == 1 and d["value"] > 0
+    assert KEYS <= set(d) and d["n_gpus"] == 1 and d["value"] > 0 and d["scaling"] == "strong"
     assert d["roofline"]["frac"] > 0 and d["e2e"]["h2d_bytes_per_step"] > 0
-    assert d["gpu_launches"] == 4
+    assert d["gpu_launches"] == 4 and d["parity"]["all_equal"]
+    assert d["e2e"]["dropin_api"]["value"] > 0
 
 
 @pytest.mark.slow
@@ -39,8 +40,12 @@ def test_bench_torchrun_two_ranks():
     env = dict(os.environ, FNT_BENCH_BACKEND="gloo")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
            "--master-addr", "127.0.0.1", "--master-port", "29517", "bench.py", "--gpus", "2",
-           "--links", "64", "--steps", "1", "--warmup", "1", "--no-cpu", "--no-e2e", "--no-alt"]
+           "--links", "64", "--symbols", "32768", "--steps", "1", "--warmup", "1", "--no-cpu",
+           "--no-e2e", "--no-alt", "--no-sub"]
     r = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=900, env=env)
     assert r.returncode == 0, r.stderr[-2000:]
     d = _json_line(r.stdout)
-    assert d["n_gpus"] == 2 and d["scaling"] == "weak"
+    # the 64 links are split 32 + 32 (strong scaling); rank 0 checked its links vs the oracle
+    assert d["n_gpus"] == 2 and d["scaling"] == "strong"
+    assert d["config"]["links_per_gpu"] == 32 and d["config"]["links_total"] == 64
+    assert d["parity"]["all_equal"]

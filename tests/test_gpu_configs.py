@@ -69,20 +69,8 @@ def test_config3_full_chain_vs_reference(snr):
 
 def _oracle_chain(eng, cfg, fe):
     """CPU oracle of the whole per-link chain (pinned pieces of oracle/)."""
-    inv = 1.0 / eng.output_scale
-    streams = []
-    for xr, xi in fe:
-        yr, yi = O.cdc_process_int(eng.tap_re, eng.tap_im, xr, xi)
-        streams.append(yr * inv + 1j * (yi * inv))
-    ph = O.decimation_phase(streams)
-    dec = [s[ph::2] for s in streams]
-    q = np.stack([O.quantize_real(v, cfg.sig_scale, 15)[0]
-                  for v in (dec[0].real, dec[0].imag, dec[1].real, dec[1].imag)])
-    nb = q.shape[1] // 16
-    oq = O.Aeq(cfg.sig_scale, mu=cfg.mu2)
-    y = oq.process(q, mu_blocks=O.mu_blocks(nb, mu1=cfg.mu1, mu2=cfg.mu2,
-                                             gear_symbols=cfg.gear_symbols))
-    return ph, y, oq
+    return O.chain_link(eng.tap_re, eng.tap_im, eng.output_scale, cfg.sig_scale, fe, cfg.mu1,
+                        cfg.mu2, cfg.gear_symbols)
 
 
 def _c5_inputs(i: int):

@@ -221,6 +221,86 @@ def test_cdc_config2_full(golden, digests, cdc_kernel):
     assert y.dtype == np.complex128 and sha(y) == digests["cdc"]["c2_process"]
 
 
+def test_cdc_float64_quantize_on_load_config2(digests):
+    """Config 2's float front-end samples (oracle/linkgen_np, the reference's link
+    model; its quantized samples are pinned to the reference's) fed as float64 and
+    quantized inside the CDC's load (in_dtype F64): outputs equal the reference's
+    quantize_real + process_int bit for bit, and the clip count equals quantize_real's
+    (fixedpoint.py:51-60, linksim.py:289-291), for the full stream and for range shards."""
+    import torch
+    import oracle.linkgen_np as G
+    from paper_2405_04253_b200.stream import CdcBank
+    link, c = G.config2_float()
+    eng = _c2_engine()
+    bank = CdcBank(eng)
+    c0 = c[0]
+    n = c0.size
+    xr = torch.from_numpy(np.ascontiguousarray(c0.real)[None]).cuda()
+    xi = torch.from_numpy(np.ascontiguousarray(c0.imag)[None]).cuda()
+    yr = torch.empty((1, n), dtype=torch.int64, device="cuda")
+    yi = torch.empty_like(yr)
+    clip = torch.zeros(1, dtype=torch.int64, device="cuda")
+    bank.run(xr, xi, yr=yr, yi=yi, in_spec=eng.sig_spec, in_clipped=clip)
+    assert sha(yr[0].cpu().numpy()) == digests["cdc"]["c2_yr"]
+    assert sha(yi[0].cpu().numpy()) == digests["cdc"]["c2_yi"]
+    want = O.quantize_real(c0.real, link.sig_scale, 15)[1] + O.quantize_real(c0.imag, link.sig_scale, 15)[1]
+    assert int(clip.item()) == want > 0
+    # three range shards (each fed its input window): same outputs, clip counts add up
+    clip.zero_()
+    cuts = [0, 123_457, 300_001, n]
+    for a, b in zip(cuts[:-1], cuts[1:]):
+        lo, hi = max(0, (a + 16) // 32 * 32 - 32), min(n, ((b - 1 + 16) // 32) * 32 + 32)
+        sr = torch.empty((1, b - a), dtype=torch.int32, device="cuda")
+        si = torch.empty_like(sr)
+        bank.run(xr[:, lo:hi], xi[:, lo:hi], length=n, x_first=lo, out_first=a, out_count=b - a,
+                 yr=sr, yi=si, in_spec=eng.sig_spec, in_clipped=clip)
+        assert np.array_equal(sr[0].cpu().numpy(), yr[0, a:b].cpu().numpy())
+        assert np.array_equal(si[0].cpu().numpy(), yi[0, a:b].cpu().numpy())
+    assert int(clip.item()) >= want  # block-aligned shards may share one boundary block
+
+
+def test_cdc_float64_quantize_on_load_edges():
+    """Ties at +-(k + 1/2), clipping values, signed zeros, NaN and ragged lengths /
+    unaligned windows: the fused quantize-on-load equals the separate quantize_real
+    kernel followed by the int8 CDC (both product paths), and matches the CPU oracle
+    where numpy's result is defined (no NaN)."""
+    import torch
+    from paper_2405_04253_b200.stream import CdcBank
+    eng = _c2_engine()
+    bank = CdcBank(eng)
+    spec = eng.sig_spec
+    rng = np.random.default_rng(17)
+    for L in (1, 31, 33, 4097, 70_001):
+        x = rng.normal(0.0, 1.3, (2, 2, L + 3))
+        k = rng.integers(-20, 21, (2, 2, L + 3)) + 0.5
+        ties = rng.random((2, 2, L + 3)) < 0.2
+        x[ties] = k[ties] / spec.scale * (1 + 0 * k[ties])
+        x[..., :2] = [[[0.0, -0.0], [1e300, -1e300]], [[np.nan, 0.0], [3.2, -3.2]]]
+        off = int(rng.integers(0, 3))
+        xr = torch.from_numpy(np.ascontiguousarray(x[:, 0])).cuda()[:, off:off + L]
+        xi = torch.from_numpy(np.ascontiguousarray(x[:, 1])).cuda()[:, off:off + L]
+        yr = torch.empty((2, L), dtype=torch.int32, device="cuda")
+        yi = torch.empty_like(yr)
+        clip = torch.zeros(1, dtype=torch.int64, device="cuda")
+        bank.run(xr, xi, yr=yr, yi=yi, in_spec=spec, in_clipped=clip)
+        qr = np.stack([P.quantize_real(xr[s].cpu().numpy(), spec)[0] for s in range(2)])
+        qi = np.stack([P.quantize_real(xi[s].cpu().numpy(), spec)[0] for s in range(2)])
+        nclip = sum(P.quantize_real(t[s].cpu().numpy(), spec)[1] for t in (xr, xi) for s in range(2))
+        assert int(clip.item()) == nclip, L
+        rr = torch.empty_like(yr)
+        ri = torch.empty_like(yr)
+        bank.run(torch.from_numpy(qr.astype(np.int8)).cuda(), torch.from_numpy(qi.astype(np.int8)).cuda(),
+                 yr=rr, yi=ri)
+        assert torch.equal(rr, yr) and torch.equal(ri, yi), L
+        for s in range(2):
+            fr, fi = xr[s].cpu().numpy(), xi[s].cpu().numpy()
+            ok = ~(np.isnan(fr) | np.isnan(fi))
+            if ok.all():
+                orr, ori = O.cdc_direct(eng.tap_re, eng.tap_im, O.quantize_real(fr, spec.scale, 15)[0],
+                                        O.quantize_real(fi, spec.scale, 15)[0])
+                assert np.array_equal(yr[s].cpu().numpy(), orr) and np.array_equal(yi[s].cpu().numpy(), ori)
+
+
 def test_cdc_edges(golden, cdc_kernel):
     a = golden("cdc")
     eng = _c2_engine()

@@ -1,12 +1,21 @@
 # Round-end evidence (run on the GPU box from the repo root; outputs in gpurun_out/):
-# bench lines for C5 / C4 / the reference arm, the ncu launch lists and full captures
-# that profiles/ summarises (tools/ncu_summary.py).
+# ncu launch lists and full captures that profiles/ summarises (tools/ncu_summary.py).
+# Each profiled command first runs once without ncu (it must exit 0).
 set -x
-python bench.py > gpurun_out/bench_final.json 2> gpurun_out/bench_final.err
-python bench.py --config c4 > gpurun_out/bench_final_c4.json 2> gpurun_out/bench_final_c4.err
-python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/bench_final_ref.json 2> gpurun_out/bench_final_ref.err
-ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"k_(cdc64|aeq|decim|quant|fnt|conv)" -c 40 --csv --log-file gpurun_out/launches_final.csv python bench.py --steps 2 --warmup 1 --no-cpu --no-e2e --no-quality --no-alt > gpurun_out/ncu_launch.log 2>&1
-ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"k_cdc64" -c 10 --csv --log-file gpurun_out/launches_final_c4.csv python bench.py --config c4 --steps 2 --warmup 1 --no-cpu --no-e2e --no-alt > gpurun_out/ncu_launch_c4.log 2>&1
-ncu --set full --import-source on --clock-control none -k regex:"k_cdc64|k_aeq_process" -c 2 -o gpurun_out/prof_final python bench.py --steps 1 --warmup 1 --no-cpu --no-e2e --no-quality --no-alt > gpurun_out/ncu_full.log 2>&1
-ncu --set full --import-source on --clock-control none -k regex:"k_cdc64_umma" -c 1 -o gpurun_out/prof_final_c4 python bench.py --config c4 --steps 1 --warmup 1 --no-cpu --no-e2e --no-alt > gpurun_out/ncu_full_c4.log 2>&1
-tail -2 gpurun_out/ncu_full.log gpurun_out/ncu_full_c4.log
+C5="python bench.py --steps 2 --warmup 1 --no-cpu --no-e2e --no-quality --no-alt --no-sub --no-parity"
+C5S="python bench.py --links 512 --steps 2 --warmup 1 --no-cpu --no-e2e --no-quality --no-alt --no-sub --no-parity"
+C4="python bench.py --config c4 --steps 2 --warmup 1 --no-cpu --no-e2e --no-alt"
+$C5 > gpurun_out/p_c5.json 2> gpurun_out/p_c5.err && \
+  ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"k_(cdc64|aeq|decim)" -c 40 --csv \
+      --log-file gpurun_out/launches_r02.csv $C5 > gpurun_out/ncu_launch.log 2>&1 && \
+  ncu --set full --import-source on --clock-control none -k regex:"k_cdc64|k_aeq_process" -c 2 \
+      -o gpurun_out/prof_r02 $C5 > gpurun_out/ncu_full.log 2>&1
+$C5S > gpurun_out/p_c5s.json 2> gpurun_out/p_c5s.err && \
+  ncu --set full --import-source on --clock-control none -k regex:"k_aeq_pol" -c 1 \
+      -o gpurun_out/prof_r02_pol512 $C5S > gpurun_out/ncu_full_pol.log 2>&1
+$C4 > gpurun_out/p_c4.json 2> gpurun_out/p_c4.err && \
+  ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"k_cdc64" -c 10 --csv \
+      --log-file gpurun_out/launches_r02_c4.csv $C4 > gpurun_out/ncu_launch_c4.log 2>&1 && \
+  ncu --set full --import-source on --clock-control none -k regex:"k_cdc64" -c 1 \
+      -o gpurun_out/prof_r02_c4 $C4 > gpurun_out/ncu_full_c4.log 2>&1
+tail -n 2 gpurun_out/ncu_full.log gpurun_out/ncu_full_pol.log gpurun_out/ncu_full_c4.log

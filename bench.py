@@ -896,12 +896,64 @@ def run_c4(args, world, rank, local, sub: bool = False) -> dict:
                                "-> D2H int16 I/Q, %d samples x 2 pols per call, copies pipelined "
                                "with the range-sharded CDC over 3 CUDA streams" % n}
         del hc, hx, hy
+    line["f64_input"] = c4_f64_variant(args, bank, eng, xr, xi, sh, L, world, peaks)
     if not sub and rank == 0 and world == 1 and not args.no_cpu:
         import oracle.np_port as N
         eng._b_plus, eng._b_minus = N.cdc_spectra(eng.tap_re, eng.tap_im)
         line["cpu_baseline"] = run_cpu_cdc_baseline(eng, 1 << 20, os.cpu_count() or 1)
     del xr, xi, yr, yi
     return line
+
+
+def c4_f64_variant(args, bank, eng, xr, xi, sh, L, world, peaks) -> dict:
+    """The CDC with float64 front-end samples quantized on load (in_dtype F64,
+    fixedpoint.py:51-60 fused into the staging): 16 B of float64 I/Q in + 4 B of int16
+    I/Q out per complex sample (SURVEY 8(d)'s 20 B/sample row), on the first 2^28
+    samples per polarization of this rank's window. The floats are the window's
+    5-bit samples plus uniform dither within +-0.45 LSB, divided by the signal scale
+    (they quantize back to the same integers; the clip count is checked)."""
+    import torch
+    n = min(1 << 28, sh.x_count)
+    g = torch.Generator(device="cuda").manual_seed(11)
+    sc = float(eng.sig_spec.scale)
+    fr = (xr[:, :n].double() + (torch.rand((2, n), generator=g, device="cuda", dtype=torch.float64) - 0.5) * 0.9) / sc
+    fi = (xi[:, :n].double() + (torch.rand((2, n), generator=g, device="cuda", dtype=torch.float64) - 0.5) * 0.9) / sc
+    out_n = max(0, min(n - 128, sh.out_count))  # inside the provided window with its halo
+    yr = torch.empty((2, out_n), dtype=torch.int16, device="cuda")
+    yi = torch.empty_like(yr)
+    clip = torch.zeros(1, dtype=torch.int64, device="cuda")
+
+    def step():
+        bank.run(fr, fi, length=L, x_first=sh.x_first, out_first=sh.out_first, out_count=out_n,
+                 yr=yr, yi=yi, in_spec=eng.sig_spec, in_clipped=clip)
+
+    for _ in range(args.warmup):
+        step()
+    _sync_all(world)
+    a = torch.cuda.Event(enable_timing=True)
+    b = torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(args.steps):
+        step()
+    b.record()
+    torch.cuda.synchronize()
+    ms = a.elapsed_time(b) / args.steps
+    # the same range from the int8 planes gives the same outputs
+    rr = torch.empty_like(yr)
+    ri = torch.empty_like(yi)
+    bank.run(xr[:, :n], xi[:, :n], length=L, x_first=sh.x_first, out_first=sh.out_first,
+             out_count=out_n, yr=rr, yi=ri)
+    same = bool(torch.equal(rr, yr) and torch.equal(ri, yi))
+    n_blocks = 2 * (out_n // 32 + 2)
+    tops = n_blocks * CDC_INT_OPS_PER_BLOCK / (ms * 1e-3) / 1e12
+    byts = 2 * out_n * 20
+    del fr, fi, yr, yi, rr, ri
+    return {"value": 2 * out_n / (ms * 1e-3) / 1e9, "unit": UNIT, "ms_per_launch": ms,
+            "samples_per_pol": out_n, "alg_bytes_per_sample": 20,
+            "hbm_gbs": byts / (ms * 1e-3) / 1e9, "hbm_frac": byts / (ms * 1e-3) / 1e9 / peaks["hbm_gbs"],
+            "int_tops": tops, "int_frac": tops / peaks["int_tops"],
+            "equals_int8_path": same, "clip_count": int(clip.item()),
+            "kernel": "k_cdc64<double> (quantize-on-load staging, shift-add butterflies)"}
 
 
 def c4_window(x_first: int, x_count: int, sig_scale: float, seg: int = 1 << 22):

@@ -117,13 +117,15 @@ __device__ __forceinline__ void stage_plane(TS* dst, const TIN* src, int64_t g0,
 // k_quant.cu (identical bits), fused into the staging of the CDC input window, so the
 // float samples cross HBM once and the int8 planes never exist in global memory.
 // Returns the clip count over the window positions [own_lo, own_hi) (global indices).
-__device__ __forceinline__ int8_t quant_in(double x, double scale, double mx, uint32_t& clip) {
+// floor(|v| + 0.5) straight to an integer (cvt.rmi: the float64 add is rounded
+// first, as numpy's is); a NaN converts to 0 and an out-of-range value saturates,
+// so |q| > max_int flags exactly the clipped samples (k_quant.cu semantics).
+__device__ __forceinline__ int8_t quant_in(double x, double scale, int32_t mx, uint32_t& clip) {
   const double v = __dmul_rn(x, scale);
-  const double a = floor(__dadd_rn(fabs(v), 0.5));
-  double r = v > 0 ? a : (v < 0 ? -a : 0.0);
-  clip = fabs(r) > mx;
-  r = r > mx ? mx : (r < -mx ? -mx : r);
-  return (int8_t)(int)r;
+  const int32_t a = __double2int_rd(__dadd_rn(fabs(v), 0.5));
+  clip = a > mx;
+  const int32_t c = min(a, mx);
+  return (int8_t)(v < 0 ? -c : c);
 }
 
 __device__ __forceinline__ uint32_t stage_plane_f64(int8_t* dst, const double* src, int64_t g0,
@@ -132,7 +134,7 @@ __device__ __forceinline__ uint32_t stage_plane_f64(int8_t* dst, const double* s
   const int64_t lo = io.x_first > 0 ? io.x_first : 0;
   const int64_t hi_avail = io.x_first + io.x_count;
   const int64_t hi = hi_avail < io.length ? hi_avail : io.length;
-  const double mx = (double)io.in_max;
+  const int32_t mx = io.in_max;
   uint32_t clips = 0;
   constexpr int CH = WIN / 16;
   for (int ch = threadIdx.x; ch < CH; ch += blockDim.x) {
@@ -1512,7 +1514,7 @@ static cudaError_t launch_k(const CdcArgs& A, dim3 grid, cudaStream_t st) {
 // resident CTAs per SM measured) once per device ordinal.
 struct TcLaunchCfg {
   std::atomic<int> per_sm{0};
-  int sms = 0;
+  std::atomic<int> sms{0};
 };
 template <typename K>
 static cudaError_t tc_launch_cfg(TcLaunchCfg (&cfgs)[64], K* k, int smem, int cap, int& per_sm, int& sms) {
@@ -1525,21 +1527,36 @@ static cudaError_t tc_launch_cfg(TcLaunchCfg (&cfgs)[64], K* k, int smem, int ca
     e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e == cudaSuccess)  // all of L1 as shared memory: the kernels stream, they do not cache
       e = cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-    int n = 0, m = 0;
+    int n = 0, m = 0, smem_sm = 0, reserved = 0;
     if (e == cudaSuccess) e = cudaDeviceGetAttribute(&m, cudaDevAttrMultiProcessorCount, dev);
+    if (e == cudaSuccess) e = cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
+    if (e == cudaSuccess) e = cudaDeviceGetAttribute(&reserved, cudaDevAttrReservedSharedMemoryPerBlock, dev);
     if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k, CDC_CTA, smem);
     if (e != cudaSuccess) return e;
-    c.sms = m;
-    // cap < 0: a fixed count of -cap (the occupancy API under-reports for the 85 KB tcgen05
-    // variant, where ncu shows two resident CTAs; TMEM allows at most two)
-    const int v = cap < 0 ? -cap : (n > cap ? cap : (n > 0 ? n : 1));
+    // cap < 0: up to -cap CTAs (the occupancy API under-reports for the 85 KB tcgen05
+    // variant, where ncu shows two resident CTAs; TMEM allows at most two), bounded by
+    // what the SM's shared memory actually holds, so a smaller carve-out (another
+    // driver's reservation, MIG, green contexts) shrinks the persistent grid instead
+    // of running half of it as a serialized tail wave
+    int v;
+    if (cap < 0) {
+      const int by_smem = smem_sm / (smem + reserved);
+      v = by_smem < -cap ? by_smem : -cap;
+      if (v < 1) v = 1;
+      if (getenv("FNTGPU_DEBUG") && by_smem < -cap)
+        fprintf(stderr, "tensor-core CDC kernel: shared memory holds %d CTAs per SM (wanted %d)\n",
+                by_smem, -cap);
+    } else {
+      v = n > cap ? cap : (n > 0 ? n : 1);
+    }
+    c.sms.store(m, std::memory_order_relaxed);
     c.per_sm.store(v, std::memory_order_release);
     if (getenv("FNTGPU_DEBUG"))
       fprintf(stderr, "tensor-core CDC kernel on device %d: smem %d B, %d CTAs/SM by occupancy, grid %d x %d SMs\n",
               dev, smem, n, v, m);
   }
   per_sm = c.per_sm.load(std::memory_order_acquire);
-  sms = c.sms;
+  sms = c.sms.load(std::memory_order_relaxed);
   return cudaSuccess;
 }
 

@@ -401,11 +401,15 @@ class HostChain:
             ch.acc.zero_()
             n_r = len(self.ranges)
             for j, (a, b) in enumerate(self.ranges):
-                # output [a, b) reads inputs up to b + 16: wait for the piece holding them
-                self.s_cmp.wait_event(self.e_in[min(j + 1, n_r - 1)])
-                ch.cdc.run(self.dxr, self.dxi, length=self.L, out_first=a, out_count=b - a,
-                           qr=ch.qr[:, a:], qi=ch.qi[:, a:], q_spec=ch.sig_spec,
-                           decim_acc=ch.acc, stream=self.s_cmp)
+                # output [a, b) reads inputs up to b + 48 (its blocks' halo): wait for the
+                # piece holding them, and pass only the samples already landed (the
+                # staging of a CTA's tail blocks past b treats the rest as zeros)
+                jj = min(j + 1, n_r - 1)
+                self.s_cmp.wait_event(self.e_in[jj])
+                hi = self.ranges[jj][1]
+                ch.cdc.run(self.dxr[:, :hi], self.dxi[:, :hi], length=self.L, out_first=a,
+                           out_count=b - a, qr=ch.qr[:, a:], qi=ch.qi[:, a:],
+                           q_spec=ch.sig_spec, decim_acc=ch.acc, stream=self.s_cmp)
             self.e_cdc.record(self.s_cmp)
             decimation_phase(ch.acc, ch.n_links, self.L, ch.phase, ch.gap, stream=self.s_cmp)
             if ch.tie_guard:
@@ -500,11 +504,14 @@ class HostCdc:
             _copy_rows(lib, self.dxi, xi_host, a, b, self.s_in)
             self.e_in[j].record(self.s_in)
         for j, (a, b) in enumerate(self.ranges):
-            self.s_cmp.wait_event(self.e_in[min(j + 1, n_r - 1)])
+            jj = min(j + 1, n_r - 1)
+            self.s_cmp.wait_event(self.e_in[jj])
             if not first:  # outputs of range j copied out by the previous call
                 self.s_cmp.wait_event(self.e_out[j])
-            self.bank.run(self.dxr, self.dxi, length=self.L, out_first=a, out_count=b - a,
-                          yr=self.dyr[:, a:], yi=self.dyi[:, a:], stream=self.s_cmp)
+            hi = self.ranges[jj][1]  # only the samples already landed
+            self.bank.run(self.dxr[:, :hi], self.dxi[:, :hi], length=self.L, out_first=a,
+                          out_count=b - a, yr=self.dyr[:, a:], yi=self.dyi[:, a:],
+                          stream=self.s_cmp)
             self.e_cdc[j].record(self.s_cmp)
         so = _lib.vp(self.s_out.cuda_stream)
         rows, pitch = self.dyr.shape[0], self.dyr.stride(0) * 2

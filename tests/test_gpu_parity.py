@@ -301,6 +301,61 @@ def test_cdc_float64_quantize_on_load_edges():
                 assert np.array_equal(yr[s].cpu().numpy(), orr) and np.array_equal(yi[s].cpu().numpy(), ori)
 
 
+@pytest.mark.parametrize("kernel", ["umma", "tc"])
+def test_cdc_matrix_forms_equal_shift_add_on_odd_windows(kernel):
+    """The tensor-core forms against the shift-add kernel on odd output ranges, odd
+    input windows and int8 views at every byte misalignment (TMA-eligible and
+    vector-staged windows), with the fused requantization and decimation statistics
+    and with plain int16 / int32 outputs."""
+    import torch
+    from paper_2405_04253_b200 import cdc as cdc_mod
+    from paper_2405_04253_b200.stream import CdcBank
+    eng = _c2_engine()
+    spec = eng.sig_spec
+    rng = np.random.default_rng(29)
+    L = 40_000
+    base_r = torch.from_numpy(rng.integers(-15, 16, (3, L + 64)).astype(np.int8)).cuda()
+    base_i = torch.from_numpy(rng.integers(-15, 16, (3, L + 64)).astype(np.int8)).cuda()
+
+    def run(name, mis, a, b):
+        prev = cdc_mod.set_cdc_kernel(name)
+        try:
+            bank = CdcBank(eng)
+            lo = max(0, (a + 16) // 32 * 32 - 32 - 7)
+            hi = min(L, ((b - 1 + 16) // 32) * 32 + 32 + 5)
+            xr = base_r[:, mis + lo:mis + hi]
+            xi = base_i[:, mis + lo:mis + hi]
+            outs = {}
+            for od in (torch.int16, torch.int32):
+                yr = torch.empty((3, b - a), dtype=od, device="cuda")
+                yi = torch.empty_like(yr)
+                bank.run(xr, xi, length=L, x_first=lo, out_first=a, out_count=b - a, yr=yr, yi=yi)
+                outs[str(od)] = (yr.cpu(), yi.cpu())
+            qr = torch.zeros((3, b - a + 64), dtype=torch.int8, device="cuda")
+            qi = torch.zeros_like(qr)
+            acc = torch.zeros((3 * 8,), dtype=torch.int64, device="cuda")
+            qo = 0 if mis % 4 == 0 else 1  # aligned q planes take the vectorised epilogue
+            bank.run(xr, xi, length=L, x_first=lo, out_first=a, out_count=b - a,
+                     qr=qr[:, qo:], qi=qi[:, qo:], q_spec=spec, decim_acc=acc)
+            # decimation statistics as integers: S2 and S4 = l3 2^64 + l2 2^32 + l1 (the
+            # kernels may distribute carries differently across the 32-bit limbs)
+            a64 = acc.cpu().numpy().astype(np.uint64).reshape(-1, 4)
+            s4 = [int(r[3]) * 2 ** 64 + int(r[2]) * 2 ** 32 + int(r[1]) for r in a64]
+            outs["q"] = (qr.cpu(), qi.cpu(), torch.tensor([int(r[0]) for r in a64]))
+            outs["s4"] = (s4,)
+            return outs
+        finally:
+            cdc_mod.set_cdc_kernel(prev)
+
+    for mis in (0, 1, 2, 3, 16):
+        for a, b in ((0, L), (33, 20_001), (4097, 39_999), (1, 2)):
+            ref, got = run("shift", mis, a, b), run(kernel, mis, a, b)
+            for key in ref:
+                for r, g in zip(ref[key], got[key]):
+                    same = (r == g) if isinstance(r, list) else torch.equal(r, g)
+                    assert same, (kernel, mis, a, b, key)
+
+
 def test_cdc_edges(golden, cdc_kernel):
     a = golden("cdc")
     eng = _c2_engine()

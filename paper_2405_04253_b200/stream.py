@@ -315,6 +315,72 @@ class CdcAeqChain:
             self.resolved = resolve_phase_ties(self.cdc, xr, xi, self.L, self.phase, self.gap)
 
 
+class PipelinedChain:
+    """The receiver chain as a steady-state pipeline over consecutive batches:
+    the CDC (+ decimation phase) of batch k + 1 runs on its own CUDA stream while
+    the FNT-AEQ of batch k runs, with two sets of intermediate buffers (requantized
+    planes, statistics, phases). Every call is still one full pass of the chain
+    over all links; outputs land in one y / err pair in call order (the AEQ
+    launches are serialized on their stream). With few streams per SM the
+    latency-bound AEQ leaves issue slots the CDC fills; with many, the CDC fills the
+    AEQ's short last wave.
+
+    Call `join()` before reading `y` / `err` of the last call."""
+
+    def __init__(self, engine: FntCdcEngine, aeq_config: AeqConfig, n_links: int, length: int,
+                 sig_spec, mu_schedule=None, forward: int | None = None):
+        t = _t()
+        dev = _lib.device()
+        self.chains = [CdcAeqChain(engine, aeq_config, n_links, length, sig_spec, mu_schedule,
+                                   forward) for _ in range(2)]
+        b = self.chains[1]
+        a = self.chains[0]
+        # one AEQ state / output set: both buffer sets' AEQ runs share chain 0's
+        b.aeq, b.y, b.err, b.mu_blocks = a.aeq, a.y, a.err, a.mu_blocks
+        self.y, self.err, self.aeq = a.y, a.err, a.aeq
+        self.s_cdc = t.cuda.Stream(device=dev)
+        self.s_aeq = t.cuda.Stream(device=dev, priority=-1)  # the long-running launches first
+        self.e_cdc = [t.cuda.Event() for _ in range(2)]
+        self.e_aeq = [t.cuda.Event() for _ in range(2)]
+        self.e_done = t.cuda.Event()
+        self._calls = 0
+        self.resolved: list[int] = []
+
+    def __call__(self, xr, xi) -> None:
+        t = _t()
+        k = self._calls & 1
+        ch = self.chains[k]
+        caller = t.cuda.current_stream()
+        self.s_cdc.wait_stream(caller)
+        self.s_aeq.wait_stream(caller)
+        if self._calls >= 2:  # the AEQ that last read this buffer set is done
+            self.s_cdc.wait_event(self.e_aeq[k])
+        with t.cuda.stream(self.s_cdc):
+            ch.acc.zero_()
+            ch.cdc.run(xr, xi, length=ch.L, qr=ch.qr, qi=ch.qi, q_spec=ch.sig_spec,
+                       decim_acc=ch.acc, stream=self.s_cdc)
+            decimation_phase(ch.acc, ch.n_links, ch.L, ch.phase, ch.gap, stream=self.s_cdc)
+            ch.check_ties(xr, xi, self.s_cdc)
+            self.resolved = ch.resolved
+        self.e_cdc[k].record(self.s_cdc)
+        self.s_aeq.wait_event(self.e_cdc[k])
+        ch.aeq.reset(self.s_aeq)
+        ch.aeq.run_decim(ch.qr, ch.qi, ch.phase, ch.n_blocks, ch.y, adapt=True,
+                         mu_blocks=ch.mu_blocks, err=ch.err, stream=self.s_aeq)
+        self.e_aeq[k].record(self.s_aeq)
+        self.e_done.record(self.s_aeq)
+        self._calls += 1
+
+    def join(self, stream=None) -> None:
+        """Make `stream` (default: the current stream) wait for the last call."""
+        t = _t()
+        (stream or t.cuda.current_stream()).wait_event(self.e_done)
+
+    @property
+    def phase(self):
+        return self.chains[(self._calls - 1) & 1].phase
+
+
 def _segments(total: int, parts: int, align: int) -> list[tuple[int, int]]:
     """Split [0, total) into <= parts contiguous ranges with boundaries on multiples
     of `align` (the last range takes the remainder)."""

@@ -81,3 +81,28 @@ def test_host_cdc_pipelined_equals_process_int(golden):
         assert np.array_equal(yr.numpy(), rr.cpu().numpy())
         assert np.array_equal(yi.numpy(), ri.cpu().numpy())
         x = [x[1], x[0]]
+
+
+def test_pipelined_chain_equals_resident_chain():
+    """stream.PipelinedChain (batch k + 1's CDC overlapping batch k's AEQ, two buffer
+    sets) gives, for back-to-back calls, exactly the one-shot chain's outputs."""
+    import torch
+    from paper_2405_04253_b200.linkgen import DeviceLinkGenerator
+    from paper_2405_04253_b200.stream import CdcAeqChain, PipelinedChain
+    n_links, n_sym = 9, 1 << 13
+    L = 2 * n_sym
+    cfg = P.LinkConfig(n_symbols=n_sym, z_km=75.0, seed=4)
+    eng = P.FntCdcEngine(cfg.cdc_config("fnt"), cfg.sig_spec())
+    gen = DeviceLinkGenerator(n_sym)
+    ref = CdcAeqChain(eng, cfg.aeq_config(), n_links, L, cfg.sig_spec(), cfg.mu_schedule())
+    pc = PipelinedChain(eng, cfg.aeq_config(), n_links, L, cfg.sig_spec(), cfg.mu_schedule())
+    batches = [gen.generate(n_links, seed=s) for s in (21, 22, 23, 24)]
+    for upto in (1, 2, 4):
+        for xr, xi in batches[:upto]:
+            pc(xr, xi)
+        pc.join()
+        torch.cuda.synchronize()
+        ref.run(*batches[upto - 1])
+        torch.cuda.synchronize()
+        assert torch.equal(pc.y, ref.y) and torch.equal(pc.err, ref.err), upto
+        assert torch.equal(pc.phase, ref.phase), upto

@@ -1,13 +1,15 @@
-"""Link configuration, FEC metrology helpers and the GPU CDC->AEQ chain
-(the parts of fntdsp/linksim.py the FNT hot path touches).
+"""Link configuration, FEC metrology helpers, and the link simulator that drives
+the GPU receiver for the CLI `sweep` (the parts of fntdsp/linksim.py the FNT hot
+path touches, plus its host-side data generation).
 
-The reference's link *simulator* (Tx, channel, front end; linksim.py:105-246) is
-host-side data generation and is out of scope as a product;
-`LinkConfig` here carries the same fields and derived quantities so callers
-configure the engines exactly as before, and `rx_equalize` runs the ★ glue of
-linksim.py:283-308 / 399-406 on the GPU: CDC per polarization (fused
-requantization and decimation statistics), decimation-phase choice, and the
-FNT-AEQ on the decimated streams.
+`LinkConfig` carries the reference's fields and derived quantities so callers
+configure the engines exactly as before. `run_single` / `run_link` reproduce the
+reference's sweep point by point: the transmitter, channel and front-end
+conditioning are host-side numpy data generation in the reference's operation
+order (a seeded run yields the reference's samples bit for bit), and every DSP
+stage after them runs on the GPU -- quantize_real, FntCdcEngine.process (or the
+float FD/TD-CDC comparators), FntAeq.process (or the float TD-AEQ kernel), and
+the BER/EVM metrology (metrology.py).
 """
 
 from __future__ import annotations
@@ -125,12 +127,171 @@ def penalty_at_fec(rows: list[Metrics], scheme_a: str, scheme_b: str,
     return crossing(scheme_a) - crossing(scheme_b)
 
 
+# ---------------------------------------------------------------- link simulator
+# Host-side data generation (linksim.py:105-246, 272-277): numpy in the reference's
+# operation order, so seeded runs give the reference's samples bit for bit.
+
+_GRAY_LEVELS = np.array([-3.0, -1.0, 3.0, 1.0])   # level of Gray bit pair b0 b1 (index 2 b0 + b1)
+_QAM_NORM = math.sqrt(10.0)
+SPEED_OF_LIGHT = 299792458.0
+
+
+@dataclass
+class TxData:
+    bits: np.ndarray       # (2, n_symbols, 4)
+    symbols: np.ndarray    # (2, n_symbols) complex, unit average energy
+    wave: np.ndarray       # (2, n_symbols * sps), unit average power
+
+
+def _gray_16qam(bits: np.ndarray) -> np.ndarray:
+    i = _GRAY_LEVELS[bits[..., 0] * 2 + bits[..., 1]]
+    q = _GRAY_LEVELS[bits[..., 2] * 2 + bits[..., 3]]
+    return (i + 1j * q) / _QAM_NORM
+
+
+def _circular(x: np.ndarray, taps: np.ndarray) -> np.ndarray:
+    """Zero-delay circular filtering: taps centred on the origin."""
+    kernel = np.zeros(len(x), dtype=complex)
+    kernel[:len(taps)] = taps
+    kernel = np.roll(kernel, -(len(taps) // 2))
+    return np.fft.ifft(np.fft.fft(x) * np.fft.fft(kernel))
+
+
+def _delayed(x: np.ndarray, tau: float) -> np.ndarray:
+    """Circular fractional delay by tau samples (real stays real)."""
+    y = np.fft.ifft(np.fft.fft(x) * np.exp(-2j * np.pi * np.fft.fftfreq(len(x)) * tau))
+    return y.real if np.isrealobj(x) else y
+
+
+def _unit_power(w: np.ndarray) -> np.ndarray:
+    return w / math.sqrt(np.mean(np.abs(w) ** 2))
+
+
+def generate_tx(cfg: LinkConfig, rng: np.random.Generator) -> TxData:
+    """Random Gray 16QAM on both polarizations, RRC-shaped at cfg.sps."""
+    from .linkgen import rrc_taps
+    bits = rng.integers(0, 2, size=(2, cfg.n_symbols, 4))
+    symbols = _gray_16qam(bits)
+    shaping = rrc_taps(cfg.sps, cfg.rrc_span, cfg.rrc_rolloff)
+    wave = np.zeros((2, cfg.n_symbols * cfg.sps), dtype=complex)
+    for p in range(2):
+        up = np.zeros(cfg.n_symbols * cfg.sps, dtype=complex)
+        up[::cfg.sps] = symbols[p]
+        wave[p] = _unit_power(_circular(up, shaping))
+    return TxData(bits=bits, symbols=symbols, wave=wave)
+
+
+def apply_channel(wave: np.ndarray, cfg: LinkConfig, snr_db: float,
+                  rng: np.random.Generator) -> tuple[np.ndarray, dict]:
+    """Dispersion all-pass, DGD, real polarization rotation, IQ skew, AWGN."""
+    report = {"p_in": float(np.mean(np.abs(wave) ** 2))}
+    f = np.fft.fftfreq(wave.shape[-1], 1.0 / cfg.fs)
+    lam = cfg.wavelength_nm * 1e-9
+    beta = math.pi * lam * lam * (cfg.dispersion_ps_nm_km * 1e-6) * (cfg.z_km * 1e3) / SPEED_OF_LIGHT
+    x = np.fft.ifft(np.fft.fft(wave, axis=-1) * np.exp(-1.0 * 1j * beta * f * f), axis=-1)
+    tau = cfg.dgd_symbols * cfg.sps / 2.0
+    x = np.stack([_delayed(x[0], tau), _delayed(x[1], -tau)])
+    th = math.radians(cfg.pol_rotation_deg)
+    x = np.array([[math.cos(th), -math.sin(th)], [math.sin(th), math.cos(th)]]) @ x
+    if cfg.iq_skew_samples:
+        x = np.stack([p.real + 1j * _delayed(p.imag, cfg.iq_skew_samples) for p in x])
+    report["p_channel"] = float(np.mean(np.abs(x) ** 2))
+    if np.isfinite(snr_db):
+        lin = 10.0 ** (snr_db / 10.0)
+        for p in range(2):
+            sigma = math.sqrt(np.mean(np.abs(x[p]) ** 2) / lin / 2.0)
+            x[p] = x[p] + sigma * (rng.standard_normal(x.shape[-1])
+                                   + 1j * rng.standard_normal(x.shape[-1]))
+    report["p_out"] = float(np.mean(np.abs(x) ** 2))
+    return x, report
+
+
+def _gram_schmidt(x: np.ndarray) -> np.ndarray:
+    i_n = x.real / math.sqrt(np.mean(x.real * x.real))
+    q_o = x.imag - np.mean(x.imag * i_n) * i_n
+    return (i_n + 1j * (q_o / math.sqrt(np.mean(q_o * q_o)))) / math.sqrt(2.0)
+
+
+def rx_frontend(rx: np.ndarray, cfg: LinkConfig, scheme: str) -> tuple[np.ndarray, dict]:
+    """GSOP, matched filter, unit power (host); then on the GPU the quantizer and the
+    FNT-CDC ("fnt") or the float CDC comparators; the sampling phase with the
+    reference's float64 metric. Returns the symbol-rate streams (2, n) and a report."""
+    from .cdc import FntCdcEngine, design_cd_taps, fd_cdc_float, td_cdc_float
+    from .fixedpoint import quantize_real
+    from .linkgen import rrc_taps
+    from .stream import reference_phase
+    mf = rrc_taps(cfg.sps, cfg.rrc_span, cfg.rrc_rolloff)
+    conditioned = [_unit_power(_circular(_gram_schmidt(rx[p]), mf)) for p in range(2)]
+    report = {"p_frontend": float(np.mean([np.mean(np.abs(c) ** 2) for c in conditioned]))}
+    cdc_cfg = cfg.cdc_config(scheme)
+    if scheme == "fnt":
+        spec = cfg.sig_spec()
+        engine = FntCdcEngine(cdc_cfg, spec)
+        report["cdc_budget"] = str(engine.budget)
+        report["cdc_support_warning"] = engine.support_warning
+        equalized, n_clip = [], 0
+        for c in conditioned:
+            (xr, cr), (xi, ci) = quantize_real(c.real, spec), quantize_real(c.imag, spec)
+            n_clip += cr + ci
+            equalized.append(engine.process(xr, xi))
+        report["clip_fraction"] = n_clip / (2 * 2 * rx.shape[-1])
+    elif scheme in ("float", "fd-float", "td-float"):
+        taps = design_cd_taps(cdc_cfg)
+        comparator = td_cdc_float if scheme == "td-float" else fd_cdc_float
+        equalized = [comparator(c, cdc_cfg, taps) for c in conditioned]
+        report["clip_fraction"] = 0.0
+    else:
+        raise ValueError(f"unknown scheme {scheme!r}")
+    phase = reference_phase(equalized, cfg.sps)
+    report["decimation_phase"] = phase
+    return np.stack([e[phase::cfg.sps] for e in equalized]), report
+
+
+def _q_factor_db(ber: float) -> float:
+    from scipy.special import erfcinv
+    if ber <= 0:
+        return math.inf
+    return 20.0 * math.log10(math.sqrt(2.0) * float(erfcinv(2.0 * ber)))
+
+
 def run_single(cfg: LinkConfig, scheme: str, snr_db: float) -> Metrics:
-    raise NotImplementedError(
-        "the link simulator (Tx/channel/front end) is host-side data generation, out of "
-        "scope for the GPU hot path; use paper_2405_04253_b200.stream.rx_equalize on "
-        "quantized front-end samples")
+    """One scheme at one SNR point (linksim.py:386-426): the whole chain plus
+    metrology, with the reference's per-(seed, SNR) random stream."""
+    import torch
+    from . import metrology as M
+    from .aeq import FntAeq, td_aeq_float
+    from .fixedpoint import quantize_real
+    rng = np.random.default_rng(np.random.SeedSequence(
+        [cfg.seed, int(round(snr_db * 1000)) if np.isfinite(snr_db) else -1]))
+    tx = generate_tx(cfg, rng)
+    rx, ch_report = apply_channel(tx.wave, cfg, snr_db, rng)
+    dec, fe_report = rx_frontend(rx, cfg, scheme)
+    streams = np.stack([dec[0].real, dec[0].imag, dec[1].real, dec[1].imag])
+    trace = None
+    if scheme == "fnt":
+        spec = cfg.sig_spec()
+        eq = FntAeq(cfg.aeq_config())
+        y = eq.process(np.stack([quantize_real(s, spec)[0] for s in streams]), adapt=True,
+                       mu_schedule=cfg.mu_schedule())
+        trace = eq.err_trace
+    else:
+        y, _ = td_aeq_float(streams, cfg.aeq_config(), mu_schedule=cfg.mu_schedule())
+    n = min(y.shape[1], tx.symbols.shape[1])
+    from . import _lib
+    y_pols = torch.from_numpy(np.stack([y[0] + 1j * y[1], y[2] + 1j * y[3]])[:, :n]).to(
+        _lib.device())[None]
+    sym, bits = M.numpy_reference_inputs(tx.bits[:, :n], tx.symbols[:, :n])
+    ber, evm_db, ok = (v[0] for v in M.align_and_count(y_pols, sym, bits, cfg.discard_symbols))
+    ber, evm_db, ok = float(ber), float(evm_db), bool(ok)
+    if trace is not None and len(trace) > 20:
+        ok = ok and float(np.mean(trace[-10:])) <= float(np.mean(trace[5:15]))
+    return Metrics(scheme=scheme, snr_db=snr_db, ber=ber, evm_db=evm_db, est_snr_db=-evm_db,
+                   q_db=_q_factor_db(ber), n_bits=(n - cfg.discard_symbols) * 8,
+                   clip_fraction=fe_report.get("clip_fraction", 0.0), converged=ok,
+                   stage_power={**ch_report, "frontend": fe_report.get("p_frontend")})
 
 
 def run_link(cfg: LinkConfig) -> list[Metrics]:
-    raise NotImplementedError(run_single.__doc__ or "see run_single")
+    """Every configured scheme over the SNR list, ordered by (scheme, SNR)."""
+    rows = [run_single(cfg, scheme, snr) for scheme in cfg.schemes for snr in cfg.snr_db]
+    return sorted(rows, key=lambda m: (m.scheme, m.snr_db))

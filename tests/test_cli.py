@@ -24,7 +24,6 @@ def _run(argv):
 def test_cli_host_commands(tmp_path):
     rc, _ = _run(["write-config", "--output", str(tmp_path / "link.ini")])
     assert rc == 0 and "[link]" in (tmp_path / "link.ini").read_text()
-    assert _run(["sweep"])[0] == 2
     rc, text = _run(["complexity"])
     assert (rc, text) == (REF["complexity"]["rc"], REF["complexity"]["stdout"])
 
@@ -60,3 +59,18 @@ def test_cli_transform_convolve(tmp_path):
         assert rc == REF["runs"][key]["rc"], key
         if rc == 0:
             assert (d / "o.txt").read_text() == REF["runs"][key]["out"], key
+
+
+@pytest.mark.gpu
+def test_cli_sweep_matches_reference(tmp_path, monkeypatch):
+    """`sweep` on a small link config (tests/golden/make_sweep_golden.py): the host
+    link simulator + GPU receiver + GPU metrology give the reference CLI's
+    sweep.csv, summary and stdout byte for byte (same relative paths, so the
+    manifest digest matches)."""
+    g = json.loads((GOLDEN / "sweep.json").read_text())
+    (tmp_path / "link.ini").write_text(g["ini"])
+    monkeypatch.chdir(tmp_path)
+    rc, text = _run(g["argv"])
+    assert rc == g["rc"] and text == g["stdout"]
+    assert (tmp_path / "sweep_out" / "sweep.csv").read_text() == g["csv"]
+    assert (tmp_path / "sweep_out" / "summary.txt").read_text() == g["summary"]

@@ -374,10 +374,17 @@ static void aeq_update(or_aeq* q, const i64 xb[4][2 * AEQ_L], double y[4][AEQ_L]
         double step = mu * g;
         q->w[s][t][k] = q->w[s][t][k] + step;
         double r = nearbyint(q->w[s][t][k] * q->tap_scale);
-        i64 wi = (i64)r;
-        if ((wi < 0 ? -wi : wi) > AEQ_TAP_MAX) {
-          q->saturations++;
-          wi = wi < 0 ? -AEQ_TAP_MAX : AEQ_TAP_MAX;
+        i64 wi;
+        if (!(fabs(r) < 9223372036854775808.0)) {
+          /* numpy: rint of NaN / |r| >= 2^63 casts to INT64_MIN (x86-64), whose abs is
+           * still negative, so it is not counted, and clip gives -16383 (aeq.py:165-168) */
+          wi = -AEQ_TAP_MAX;
+        } else {
+          wi = (i64)r;
+          if ((wi < 0 ? -wi : wi) > AEQ_TAP_MAX) {
+            q->saturations++;
+            wi = wi < 0 ? -AEQ_TAP_MAX : AEQ_TAP_MAX;
+          }
         }
         q->w_int[s][t][k] = wi;
       }

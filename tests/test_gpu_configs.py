@@ -173,3 +173,36 @@ def test_config4_scale_cdc_windows_and_linearity():
             inner = slice(32 if a > 0 else 0, 4096 - 32 if a + 4096 < L else 4096)
             assert np.array_equal(got_r[inner], orr[s0:s0 + 4096][inner])
             assert np.array_equal(got_i[inner], ori[s0:s0 + 4096][inner])
+
+
+@pytest.mark.slow
+def test_config4_link_model_windows_vs_oracle():
+    """the config-4 signal model (bench.c4_window: 2^22-sample link
+    segments keyed by global segment index, 75 km, 5-bit) at 2^28 samples per pol in
+    HBM through one CDC launch; 8 windows of 2^20 samples each (+ the halo) copied
+    back and checked bit-exactly against the CPU oracle's direct FIR, at the stream
+    start, the end and six random positions."""
+    import torch
+    from bench import c4_window
+    from paper_2405_04253_b200.stream import CdcBank
+    cfg = P.LinkConfig(z_km=75.0, seed=3)
+    eng = P.FntCdcEngine(cfg.cdc_config("fnt"), cfg.sig_spec())
+    L = 1 << 28
+    xr, xi = c4_window(0, L, cfg.sig_scale)
+    yr = torch.empty((2, L), dtype=torch.int16, device="cuda")
+    yi = torch.empty_like(yr)
+    CdcBank(eng).run(xr, xi, yr=yr, yi=yi)
+    torch.cuda.synchronize()
+    W = 1 << 20
+    rng = np.random.default_rng(4)
+    starts = [0, L - W] + [int(a) for a in rng.integers(64, L - W - 64, 6)]
+    for a in starts:
+        lo, hi = max(0, a - 64), min(L, a + W + 64)
+        for p in range(2):
+            wr = xr[p, lo:hi].cpu().numpy().astype(np.int64)
+            wi = xi[p, lo:hi].cpu().numpy().astype(np.int64)
+            orr, ori = O.cdc_direct(eng.tap_re, eng.tap_im, wr, wi)
+            s0 = a - lo
+            inner = slice(32 if a > 0 else 0, W - 32 if a + W < L else W)
+            assert np.array_equal(yr[p, a:a + W].cpu().numpy()[inner], orr[s0:s0 + W][inner]), (a, p)
+            assert np.array_equal(yi[p, a:a + W].cpu().numpy()[inner], ori[s0:s0 + W][inner]), (a, p)

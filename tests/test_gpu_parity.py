@@ -627,6 +627,38 @@ def test_aeq_single_block_api(golden, aeq_kernel):
 
 
 @pytest.mark.parametrize("forward", AEQ_MODES)
+def test_aeq_nan_and_inf_step_size(golden, forward, aeq_kernel):
+    """NaN and inf mu blocks (reference fixture aeq_nan.npz): NaN / inf float taps,
+    14-bit taps -16383 and not counted as saturations (numpy's INT64_MIN cast), through
+    FntAeq (single stream) and the multi-stream kernel's fast path."""
+    import torch
+    from paper_2405_04253_b200.stream import AeqBank
+    g = golden("aeq_nan")
+    eq = _aeq(mu=1e-4, forward=forward)
+    mu = g["mu"]
+    y = eq.process(g["x"], adapt=True, mu_schedule=lambda i: mu[i // 16])
+    assert np.array_equal(y, g["y"])
+    assert np.array_equal(eq.w, g["w"], equal_nan=True)
+    assert np.array_equal(eq.taps.w_int, g["w_int"]) and eq.saturations == int(g["sat"])
+    assert np.array_equal(np.array(eq.err_trace), g["err"], equal_nan=True)
+    cfg = P.LinkConfig().aeq_config()
+    cfg.sig_spec = P.QuantSpec(5, SIG_SCALE)
+    bank = AeqBank(cfg, 3, forward=forward)
+    x = torch.from_numpy(np.stack([g["x"]] * 3).astype(np.int8)).cuda()
+    nb = g["x"].shape[1] // 16
+    yd = torch.empty((3, 4, 16 * nb), dtype=torch.float64, device="cuda")
+    err = torch.empty((3, nb), dtype=torch.float64, device="cuda")
+    bank.run_planar(x, nb, yd, mu_blocks=torch.from_numpy(mu).cuda(), err=err)
+    st = bank.read_state()
+    for s in range(3):
+        assert np.array_equal(yd[s].cpu().numpy(), g["y"])
+        assert np.array_equal(err[s].cpu().numpy(), g["err"], equal_nan=True)
+        assert np.array_equal(np.array(st[s].w).reshape(4, 4, 16), g["w"], equal_nan=True)
+        assert np.array_equal(np.array(st[s].w_int).reshape(4, 4, 16), g["w_int"])
+        assert int(st[s].saturations) == int(g["sat"])
+
+
+@pytest.mark.parametrize("forward", AEQ_MODES)
 def test_aeq_wide_inputs_match_oracle(forward, aeq_kernel):
     """|x| up to 2^15: per-group residues wrap mod F exactly as the reference's."""
     rng = np.random.default_rng(3)

@@ -150,3 +150,15 @@ def test_pairwise_sum_matches_numpy():
     for n in (1, 7, 8, 9, 31, 32, 100, 128, 129, 1000, 4097, 1 << 16):
         a = rng.standard_normal(n)
         assert O.pairwise_sum(a) == float(np.add.reduce(a))
+
+
+def test_oracle_aeq_nan_and_inf_step_size(golden):
+    """A NaN and an inf mu block (reference fixture aeq_nan.npz): the float taps turn
+    NaN / inf and the 14-bit taps clip to -16383 uncounted, as numpy's cast does."""
+    g = golden("aeq_nan")
+    oq = O.Aeq(SIG_SCALE, mu=1e-4)
+    y = oq.process(g["x"], mu_blocks=g["mu"])
+    assert np.array_equal(y, g["y"])
+    assert np.array_equal(oq.w, g["w"], equal_nan=True)
+    assert np.array_equal(oq.w_int, g["w_int"]) and oq.saturations == int(g["sat"])
+    assert np.array_equal(np.array(oq.err_trace), g["err"], equal_nan=True)

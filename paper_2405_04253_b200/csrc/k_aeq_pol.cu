@@ -386,117 +386,147 @@ __global__ void __launch_bounds__(64, 4) k_aeq_pol(fntgpu_aeq_state* __restrict_
   const bool want_err = adapt && (QUICK || err_out != nullptr);
   double* yp = io.y + S_idx * io.y_stream_stride + s * io.y_row_stride + m;
   long long sat64 = 0;
+  // Block b+1's input transforms are computed inside block b's update (they do not
+  // depend on the taps): the float64 gradient leaves integer issue slots free. The
+  // input ring therefore holds 4 blocks (b - 1 .. b + 1 in use); X holds X_b until
+  // block b's forward has read it.
   uint2 raw = make_uint2(0u, 0u);
-  if (nb > 0) raw = fetch(row);
   double mu_next = mu_p && nb > 0 ? mu_p[0] : A.prm.mu;
-  uint32_t amax_prev = max(mag(v0), mag(v1));  // this lane's samples of the previous block
+  uint32_t amax_cur = 0;  // max |x| over the current block's window (all four streams)
+  if (nb > 0) {
+    int32_t a0, a1;
+    decode(fetch(row), a0, a1);
+    const uint32_t a_hist = max(mag(v0), mag(v1));
+    v0 = a0;
+    v1 = a1;
+    put_int(0, v0, v1);
+    if (adapt) put_xf(0, xf_of<NARROW>(v0, lut, A.prm.sig_scale), xf_of<NARROW>(v1, lut, A.prm.sig_scale));
+    amax_cur = __reduce_max_sync(0xffffffffu, max(max(mag(v0), mag(v1)), a_hist));
+    if (nb > 1) {
+      row += IN_STEP;
+      raw = fetch(row);
+    }
+    __syncwarp();
+    uint32_t xv[4];
+    pol_input_fnt(S, lane, AEQ_L * 3, 0, xv);
+    pol_store_X(S, lane, xv);
+    __syncwarp();
+  }
 
   for (int64_t b0 = 0; b0 < nb; b0 += (int64_t)1 << 24) {
     const int64_t b1 = nb - b0 < ((int64_t)1 << 24) ? nb : b0 + ((int64_t)1 << 24);
     for (int64_t b = b0; b < b1; ++b) {
       const bool more = b + 1 < nb;
-      decode(raw, v0, v1);
       const double mu = mu_next;
-      if (QUICK) {  // branch-free one-block-ahead prefetch (the last block re-reads its own)
-        row += more ? IN_STEP : 0;
-        raw = fetch(row);
-        mu_next = mu_p[more ? b + 1 : b];
-      } else if (more) {
-        row += IN_STEP;
-        raw = fetch(row);
-        if (mu_p) mu_next = mu_p[b + 1];
-      }
-      put_int(b, v0, v1);
-      if (adapt) put_xf(b, xf_of<NARROW>(v0, lut, A.prm.sig_scale), xf_of<NARROW>(v1, lut, A.prm.sig_scale));
-      const uint32_t a_cur = max(mag(v0), mag(v1));
-      const uint32_t amax = __reduce_max_sync(0xffffffffu, max(a_cur, amax_prev));
-      amax_prev = a_cur;
       const uint32_t asum_w = __reduce_add_sync(0xffffffffu, asum);
-      __syncwarp();
-      {
-        uint32_t xv[4];
-        const int prev4 = (int)((b + 3) & 3);
-        pol_input_fnt(S, lane, AEQ_L * prev4, AEQ_L * prev4 + AEQ_L, xv);
-        pol_store_X(S, lane, xv);
-      }
-      __syncwarp();
-      // ---- forward (aeq.py:118-144)
-      const int32_t yi = pol_forward(S, lane, amax <= 16u && asum_w * amax <= 32768u);
+      // ---- forward (aeq.py:118-144) with X_b
+      const int32_t yi = pol_forward(S, lane, amax_cur <= 16u && asum_w * amax_cur <= 32768u);
       const double y0 = div_D<QUICK>(yi, A);  // y_int / (sig_scale * tap_scale)
       yp[AEQ_L * b] = y0;
-      if (!adapt) continue;
-      // ---- update_taps (aeq.py:148-170) for this polarization
-      const double yo = __shfl_xor_sync(0xffffffffu, y0, 16);
-      const double yI = sp == 0 ? y0 : yo, yQ = sp == 0 ? yo : y0;  // one branch-free ring decision
-      const double e = rde<QUICK>(yI, yQ, A);
-      S.ey[sp][m] = dmul(e, y0);
-      if (want_err && sp == 0) SS.eabs[b % (2 * POL_ERR_K)][16 * p + m] = fabs(e);
-      __syncwarp();
-      if (mu != 0.0) {
-        // gradient of taps k = kb + kk: sum_m ey[s'][m] x_block[t][16 + m - k] in
-        // numpy's einsum order (aeq_common.cuh einsum_m, two chains per tap);
-        // x_block[t][16 + m - k] = xs[3 - kk + m], xs + me 16-byte aligned
-        const double* xs = S.xf[t] + 1 + AEQ_L * (int)((b & 1) ^ 1) + 13 - kb;
-        const double2* eyv = reinterpret_cast<const double2*>(S.ey[sp]);
-        double c0[4], c1[4];
+      // ---- block b+1's samples into the ring (the last block re-reads its own)
+      int32_t n0, n1;
+      decode(raw, n0, n1);
+      if (QUICK) {
+        row += (b + 2 < nb) ? IN_STEP : 0;
+        raw = fetch(row);
+        mu_next = mu_p[more ? b + 1 : b];
+      } else {
+        if (b + 2 < nb) {
+          row += IN_STEP;
+          raw = fetch(row);
+        }
+        if (more && mu_p) mu_next = mu_p[b + 1];
+      }
+      if (!more) { n0 = v0; n1 = v1; }
+      put_int(b + 1, n0, n1);
+      const uint32_t amax_next =
+          __reduce_max_sync(0xffffffffu, max(max(mag(n0), mag(n1)), max(mag(v0), mag(v1))));
+      uint32_t xv[4];
+      const int off4 = AEQ_L * (int)(b & 3);  // x_block_{b+1} = [slot b | slot b+1]
+      if (adapt) {
+        // ---- update_taps (aeq.py:148-170) for this polarization
+        const double yo = __shfl_xor_sync(0xffffffffu, y0, 16);
+        const double yI = sp == 0 ? y0 : yo, yQ = sp == 0 ? yo : y0;  // one branch-free ring decision
+        const double e = rde<QUICK>(yI, yQ, A);
+        S.ey[sp][m] = dmul(e, y0);
+        if (want_err && sp == 0) SS.eabs[b % (2 * POL_ERR_K)][16 * p + m] = fabs(e);
+        __syncwarp();
+        if (mu != 0.0) {
+          pol_input_fnt(S, lane, off4, off4 + AEQ_L, xv);  // interleaved with the gradient
+          // gradient of taps k = kb + kk: sum_m ey[s'][m] x_block[t][16 + m - k] in
+          // numpy's einsum order (aeq_common.cuh einsum_m, two chains per tap);
+          // x_block[t][16 + m - k] = xs[3 - kk + m], xs + me 16-byte aligned
+          const double* xs = S.xf[t] + 1 + AEQ_L * (int)((b & 1) ^ 1) + 13 - kb;
+          const double2* eyv = reinterpret_cast<const double2*>(S.ey[sp]);
+          double c0[4], c1[4];
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          const int me = (i < 4 ? 6 : 22) - 2 * i;  // 6, 4, 2, 0, 14, 12, 10, 8
-          const double2 e2 = eyv[me / 2];
-          const double2 p0 = reinterpret_cast<const double2*>(xs + me)[0];
-          const double2 p1 = reinterpret_cast<const double2*>(xs + me)[1];
-          const double xw[5] = {p0.x, p0.y, p1.x, p1.y, xs[me + 4]};
+          for (int i = 0; i < 8; ++i) {
+            const int me = (i < 4 ? 6 : 22) - 2 * i;  // 6, 4, 2, 0, 14, 12, 10, 8
+            const double2 e2 = eyv[me / 2];
+            const double2 p0 = reinterpret_cast<const double2*>(xs + me)[0];
+            const double2 p1 = reinterpret_cast<const double2*>(xs + me)[1];
+            const double xw[5] = {p0.x, p0.y, p1.x, p1.y, xs[me + 4]};
 #pragma unroll
-          for (int kk = 0; kk < 4; ++kk) {
-            const double pe = dmul(e2.x, xw[3 - kk]), po = dmul(e2.y, xw[4 - kk]);
-            c0[kk] = i == 0 ? pe : dadd(pe, c0[kk]);
-            c1[kk] = i == 0 ? po : dadd(po, c1[kk]);
+            for (int kk = 0; kk < 4; ++kk) {
+              const double pe = dmul(e2.x, xw[3 - kk]), po = dmul(e2.y, xw[4 - kk]);
+              c0[kk] = i == 0 ? pe : dadd(pe, c0[kk]);
+              c1[kk] = i == 0 ? po : dadd(po, c1[kk]);
+            }
           }
-        }
-        uint32_t smask = 0;
-#pragma unroll
-        for (int kk = 0; kk < 4; ++kk) {
-          const double w = dadd(wf[kk], dmul(mu, dadd(c0[kk], c1[kk])));
-          wf[kk] = w;
-          const double pq = dmul(w, A.prm.tap_scale);
-          const int32_t i = __double2int_rn(pq);
-          c[kk] = min(max(i, -AEQ_TAP_MAX), AEQ_TAP_MAX);
-          smask |= (uint32_t)((c[kk] != i) | (pq != pq)) << kk;  // clipped, or NaN
-        }
-        sat += __popc(smask);
-        if (__any_sync(0xffffffffu, smask != 0u)) {
-          // rare: a clipped tap whose rint is not an int64 (numpy: INT64_MIN, NaN
-          // included) becomes -16383 and is not counted (aeq.py:165-168)
+          uint32_t smask = 0;
 #pragma unroll
           for (int kk = 0; kk < 4; ++kk) {
-            if ((smask >> kk) & 1u) {
-              if (!(fabs(dmul(wf[kk], A.prm.tap_scale)) < 9.2233720368547758e18)) {
-                sat -= 1;
-                c[kk] = -AEQ_TAP_MAX;
+            const double w = dadd(wf[kk], dmul(mu, dadd(c0[kk], c1[kk])));
+            wf[kk] = w;
+            const double pq = dmul(w, A.prm.tap_scale);
+            const int32_t i = __double2int_rn(pq);
+            c[kk] = min(max(i, -AEQ_TAP_MAX), AEQ_TAP_MAX);
+            smask |= (uint32_t)((c[kk] != i) | (pq != pq)) << kk;  // clipped, or NaN
+          }
+          sat += __popc(smask);
+          if (__any_sync(0xffffffffu, smask != 0u)) {
+            // rare: a clipped tap whose rint is not an int64 (numpy: INT64_MIN, NaN
+            // included) becomes -16383 and is not counted (aeq.py:165-168)
+#pragma unroll
+            for (int kk = 0; kk < 4; ++kk) {
+              if ((smask >> kk) & 1u) {
+                if (!(fabs(dmul(wf[kk], A.prm.tap_scale)) < 9.2233720368547758e18)) {
+                  sat -= 1;
+                  c[kk] = -AEQ_TAP_MAX;
+                }
               }
             }
           }
+          asum = publish_taps(S, sp, t, kb, c);
+        } else {
+          pol_input_fnt(S, lane, off4, off4 + AEQ_L, xv);
         }
-        asum = publish_taps(S, sp, t, kb, c);
-      }
-      if (want_err && ((b + 1) % POL_ERR_K == 0 || !more)) {
-        // both polarizations' |e| of the last <= POL_ERR_K blocks are in the ring:
-        // warp 0 forms the means in numpy's pairwise order (k_aeq.cu lane_update)
-        __syncthreads();
-        if (p == 0) {
-          const int64_t bb = b - (b % POL_ERR_K) + (lane >> 3);
-          const int j = lane & 7;
-          double r = 0.0;
-          if (bb <= b) {
-            const double* a = SS.eabs[bb % (2 * POL_ERR_K)];
-            r = dadd(dadd(dadd(a[j], a[j + 8]), a[j + 16]), a[j + 24]);
+        if (want_err && ((b + 1) % POL_ERR_K == 0 || !more)) {
+          // both polarizations' |e| of the last <= POL_ERR_K blocks are in the ring:
+          // warp 0 forms the means in numpy's pairwise order (k_aeq.cu lane_update)
+          __syncthreads();
+          if (p == 0) {
+            const int64_t bb = b - (b % POL_ERR_K) + (lane >> 3);
+            const int j = lane & 7;
+            double r = 0.0;
+            if (bb <= b) {
+              const double* a = SS.eabs[bb % (2 * POL_ERR_K)];
+              r = dadd(dadd(dadd(a[j], a[j + 8]), a[j + 16]), a[j + 24]);
+            }
+            r = dadd(r, __shfl_xor_sync(0xffffffffu, r, 1));
+            r = dadd(r, __shfl_xor_sync(0xffffffffu, r, 2));
+            r = dadd(r, __shfl_xor_sync(0xffffffffu, r, 4));
+            if (j == 0 && bb <= b) err_out[bb] = dmul(r, 1.0 / 32.0);
           }
-          r = dadd(r, __shfl_xor_sync(0xffffffffu, r, 1));
-          r = dadd(r, __shfl_xor_sync(0xffffffffu, r, 2));
-          r = dadd(r, __shfl_xor_sync(0xffffffffu, r, 4));
-          if (j == 0 && bb <= b) err_out[bb] = dmul(r, 1.0 / 32.0);
         }
+        // block b's gradient has read its window: block b+1's x / sig may land
+        put_xf(b + 1, xf_of<NARROW>(n0, lut, A.prm.sig_scale), xf_of<NARROW>(n1, lut, A.prm.sig_scale));
+      } else {
+        pol_input_fnt(S, lane, off4, off4 + AEQ_L, xv);
       }
+      pol_store_X(S, lane, xv);  // X_{b+1}: block b's forward has read X_b
+      amax_cur = amax_next;
+      if (more) { v0 = n0; v1 = n1; }
       __syncwarp();
     }
     sat64 += sat;

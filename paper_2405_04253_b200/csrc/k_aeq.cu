@@ -61,6 +61,9 @@ namespace fntgpu {
 #ifndef AEQ_FUSE_T
 #define AEQ_FUSE_T 1                 // FNT forward: sum over t before the inverse when exact
 #endif
+#ifndef AEQ_MAC_T
+#define AEQ_MAC_T 1                  // stream sum as 64-bit multiply-accumulates (fused_inverse_mac)
+#endif
 #ifndef AEQ_MIN_CTAS
 // Register target of the launch bounds. 13 lets ptxas schedule with up to 157
 // registers; every instance still lands at <= 128 (cuobjdump -res-usage), so 16
@@ -81,7 +84,8 @@ struct __align__(16) AeqScratch {
                               // so every window is contiguous (odd t-stride: no bank conflicts)
   int32_t xi[4][2 * AEQ_L + 8]; // input integer ring: [t][16 * block parity + j]; the 40-word
                                 // pitch keeps the input transform's loads conflict-free
-  uint32_t X[4][AEQ_N + 4];   // cooperative input spectra (FNT path), 16-B aligned padded rows
+  uint32_t X[4][AEQ_N + 8];   // cooperative input spectra (FNT path), 16-B aligned padded rows;
+                              // AEQ_MAC_T: canonical residues at [t][8 (k mod 4) + k / 4]
   double err[32];             // |e| values for the err_trace mean
   uint8_t xq[4][64];          // DIRECT, int8 inputs: x_block[t] reversed as bytes, ring of 32
                               // stored twice: block b's samples j at 16 * parity + 15 - j (+ 32)
@@ -272,7 +276,16 @@ __device__ __forceinline__ void warp_input_fnt(AeqScratch& S, int lane, int cur)
     }
     const int k1 = (int)(__brev((unsigned)n1) >> 29);
     uint4 out = make_uint4(m_rot(v[0], 27), m_rot(v[1], 27), m_rot(v[2], 27), m_rot(v[3], 27));
+#if AEQ_MAC_T
+    // canonical residues (< 2^17: the 64-bit multiply-accumulate of fused_inverse_mac
+    // cannot overflow), bins k = k2 + 4 k1 at 8 k2 + k1
+    S.X[tq][k1] = f4_mod(out.x);
+    S.X[tq][8 + k1] = f4_mod(out.y);
+    S.X[tq][16 + k1] = f4_mod(out.z);
+    S.X[tq][24 + k1] = f4_mod(out.w);
+#else
     reinterpret_cast<uint4*>(S.X[tq])[k1] = out;
+#endif
   }
   __syncwarp();
 }
@@ -403,6 +416,85 @@ __device__ __forceinline__ void fused_inverse(AeqScratch& S, int lane, const uin
   __syncwarp();
 }
 
+// fused_inverse<4, 64> with the transform-domain stream sum as 64-bit multiply-
+// accumulates (AEQ_MAC_T): each lane publishes its tap spectrum W_stg (not its
+// products), and the inverse lane (s, k1 = t, g) forms
+//   Q[k2] = sum_t'' X_t''[k1 + 4 k2] * W_st''g[k1 + 4 k2]
+// with IMAD.WIDE.U32 into 64-bit accumulators (X canonical < 2^17, W < 2^32: the four
+// terms stay below 2^51), folded once per bin (2^32 == 1 mod 2^32 - 1): 32 MACs + 8
+// folds instead of 32 products (3 instructions each) + 24 modular adds.
+__device__ __forceinline__ void fused_inverse_mac(AeqScratch& S, int lane, const uint32_t (&W)[AEQ_N],
+                                                  int m0, int32_t& yi0, int32_t& yi1) {
+  constexpr int F = 4, NB = AEQ_N / F;
+  const int s = lane >> 3, t = (lane >> 1) & 3, g = lane & 1;
+  const int k1 = t;
+  auto swz = [](int r) { const int x = r & 7; return 4 * (x ^ ((x & 4) >> 1)); };
+  uint32_t* prod = reinterpret_cast<uint32_t*>(S.part);
+  const int rot = swz(lane);
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    const int c1 = (4 * q) / NB, c2 = (4 * q) % NB;  // logical column 4q = c1 * NB + c2
+    const uint4 v = make_uint4(W[c1 + F * c2], W[c1 + F * (c2 + 1)], W[c1 + F * (c2 + 2)],
+                               W[c1 + F * (c2 + 3)]);
+    reinterpret_cast<uint4*>(prod + 32 * lane)[((4 * q + rot) & 31) >> 2] = v;
+  }
+  __syncwarp();
+  uint64_t acc[NB];
+#pragma unroll
+  for (int i = 0; i < F; ++i) {
+    const int r = 8 * s + 2 * i + g;
+    const int rr = swz(r);
+    const uint4* xq = reinterpret_cast<const uint4*>(&S.X[i][8 * k1]);
+#pragma unroll
+    for (int h = 0; h < NB / 4; ++h) {
+      const uint4 w = reinterpret_cast<const uint4*>(prod + 32 * r)[((NB * k1 + 4 * h + rr) & 31) >> 2];
+      const uint4 x = xq[h];
+      const uint32_t wv[4] = {w.x, w.y, w.z, w.w}, xv[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const uint64_t p = (uint64_t)xv[e] * wv[e];
+        acc[4 * h + e] = i == 0 ? p : acc[4 * h + e] + p;
+      }
+    }
+  }
+  uint32_t Q[NB];
+#pragma unroll
+  for (int c2 = 0; c2 < NB; ++c2) Q[c2] = m_add((uint32_t)acc[c2], (uint32_t)(acc[c2] >> 32));
+  // +32768 on the group's DC bin (lane k1 = 0, k2 = 0): +32768 on every output
+  Q[0] = m_add(Q[0], k1 == 0 ? 32768u : 0u);
+  to_bitrev<NB>(Q);
+  fnt_dit<NB, RADIX16, true, false, false, AEQ_IFNT_CM>(Q);
+  __syncwarp();  // every lane has read its spectra before S.part is reused
+  {
+    int32_t c[AEQ_L];
+#pragma unroll
+    for (int m = 0; m < AEQ_L; ++m) {
+      const uint32_t q = Q[m % NB];
+      c[m] = (int32_t)__funnelshift_l(q, q, ((16 - m) * k1) & 31);  // 2^(-(16+m) k1)
+    }
+    part_store16(S.part[lane], c);
+  }
+  __syncwarp();
+  int32_t a0 = -65 * 32768, a1 = a0;
+  {
+    uint32_t h0 = 0, h1 = 0, l0 = 0, l1 = 0;
+#pragma unroll
+    for (int i = 0; i < F; ++i) {
+      const int r = 8 * s + 2 * i;
+      const int2 hv = part_pair(S.part[r], m0), lv = part_pair(S.part[r + 1], m0);
+      h0 = m_add(h0, (uint32_t)hv.x);
+      h1 = m_add(h1, (uint32_t)hv.y);
+      l0 = m_add(l0, (uint32_t)lv.x);
+      l1 = m_add(l1, (uint32_t)lv.y);
+    }
+    a0 += 64 * (int32_t)f4_mod(h0) + (int32_t)f4_mod(l0);
+    a1 += 64 * (int32_t)f4_mod(h1) + (int32_t)f4_mod(l1);
+  }
+  yi0 = a0;
+  yi1 = a1;
+  __syncwarp();
+}
+
 template <int FWD, bool NARROW = false>
 __device__ __forceinline__ void lane_forward(AeqScratch& S, int lane, int cur, const LaneTaps& T,
                                              int m0, int32_t& yi0, int32_t& yi1,
@@ -446,11 +538,24 @@ __device__ __forceinline__ void lane_forward(AeqScratch& S, int lane, int cur, c
 #if AEQ_PROBE != 2
     fnt_stage<AEQ_N, RADIX2, false, false, false, 3, -1, AEQ_TAP_CM>(W);
 #endif
+#if AEQ_FUSE_T && AEQ_MAC_T
+    if (fused) { fused_inverse_mac(S, lane, W, m0, yi0, yi1); return; }
+#endif
     uint32_t X[AEQ_N];
 #pragma unroll
     for (int q = 0; q < AEQ_N / 4; ++q) {
       const uint4 v = reinterpret_cast<const uint4*>(S.X[t])[q];
+#if AEQ_MAC_T
+      // permuted layout: word 4q + e holds bin k with 8 (k mod 4) + k / 4 = 4q + e
+      const uint32_t ve[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int idx = 4 * q + e;
+        X[(idx >> 3) + 4 * (idx & 7)] = ve[e];
+      }
+#else
       X[4 * q] = v.x; X[4 * q + 1] = v.y; X[4 * q + 2] = v.z; X[4 * q + 3] = v.w;
+#endif
     }
 #pragma unroll
     for (int k = 0; k < AEQ_N; ++k) X[k] = m_mul(X[k], W[k]);  // 32 general products

@@ -52,7 +52,7 @@ struct __align__(16) PolWarp {
   uint32_t tv[32 * POL_TV_P];          // tap digit variants, row = reader lane
   double xf[4][66];                    // x / sig_scale ring (as k_aeq.cu AeqScratch.xf)
   int32_t xi[4][POL_XI_P];             // input integers: block b at 16 (b mod 4) and 64 + 16 (b mod 4)
-  uint32_t X[4][36];                   // input spectra, [t][16 h + j] = X_t[2 j + h]
+  uint32_t X[4][36];                   // input spectra, canonical, [t][xm_index(k)] = X_t[k]
   int32_t traw[2][4][16];              // 14-bit taps w_int[s'][t][k] (reference-group forward)
   double ey[2][AEQ_L];                 // e * y per output stream of this polarization
 };
@@ -98,12 +98,20 @@ __device__ __forceinline__ void pol_input_fnt(const PolWarp& S, int lane, int of
   }
 }
 
-// store split by bin parity: X[t][16 h + j] = X_t[2 j + h] (h = k2 & 1, j = 2 k1 + (k2 >> 1))
+// canonical residues (< 2^17, so the 64-bit multiply-accumulates of the stream sum
+// cannot overflow) stored by bin k at X[t][4 (k mod 8) + k / 8]: the 4 bins an inverse
+// lane k1 needs (k1 + 8 k2) are one 16-byte row
+__device__ __host__ constexpr int xm_index(int k) { return 4 * (k & 7) + (k >> 3); }
 __device__ __forceinline__ void pol_store_X(PolWarp& S, int lane, const uint32_t (&v)[4]) {
   const int tq = lane >> 3, n1 = lane & 7;
-  const int k1 = (int)(__brev((unsigned)n1) >> 29);
-  *reinterpret_cast<uint2*>(&S.X[tq][2 * k1]) = make_uint2(m_rot(v[0], 27), m_rot(v[2], 27));
-  *reinterpret_cast<uint2*>(&S.X[tq][16 + 2 * k1]) = make_uint2(m_rot(v[1], 27), m_rot(v[3], 27));
+  const int k1 = (int)(__brev((unsigned)n1) >> 29);  // lane holds bins k2 + 4 k1
+#pragma unroll
+  for (int k2 = 0; k2 < 4; ++k2)
+    S.X[tq][4 * (k2 + 4 * (k1 & 1)) + (k1 >> 1)] = f4_mod(m_rot(v[k2], 27));
+}
+// X_t[2 j + h] (bin parity h) in that layout: 4 h + 8 (j mod 4) + j / 4
+__device__ __forceinline__ uint32_t pol_x(const PolWarp& S, int t, int h, int j) {
+  return S.X[t][4 * h + 8 * (j & 3) + (j >> 2)];
 }
 
 // Digit variants of this lane's 4 taps (k = kb + kk): row (s', t, g, h) of S.tv is
@@ -152,44 +160,40 @@ __device__ __forceinline__ void load_tap_spectrum(const PolWarp& S, int lane, ui
   fnt16_taps(W);
 }
 
-// products of the lane's 16 bins with X_t, written to row `lane` of S.buf in groups
+// the lane's 16 tap-spectrum bins (parity h), written to row `lane` of S.buf in groups
 // q = j mod 4 (entries j = q + 4 k2) at group slot q ^ t_lo: with the 40-word pitch
 // the 8 lanes of every store / load phase hit 8 distinct 4-bank groups
-__device__ __forceinline__ void store_products(PolWarp& S, int lane, int t, int h, uint32_t (&P)[16]) {
-  const uint4* xv = reinterpret_cast<const uint4*>(&S.X[t][16 * h]);
-#pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    const uint4 x = xv[q];
-    P[4 * q] = m_mul(P[4 * q], x.x);
-    P[4 * q + 1] = m_mul(P[4 * q + 1], x.y);
-    P[4 * q + 2] = m_mul(P[4 * q + 2], x.z);
-    P[4 * q + 3] = m_mul(P[4 * q + 3], x.w);
-  }
+__device__ __forceinline__ void store_spectrum(PolWarp& S, int lane, const uint32_t (&W)[16]) {
   uint32_t* rowp = S.buf + lane * POL_BUF_P;
   const int swz = (lane >> 2) & 1;
 #pragma unroll
   for (int q = 0; q < 4; ++q)
-    reinterpret_cast<uint4*>(rowp)[q ^ swz] = make_uint4(P[q], P[q + 4], P[q + 8], P[q + 12]);
+    reinterpret_cast<uint4*>(rowp)[q ^ swz] = make_uint4(W[q], W[q + 4], W[q + 8], W[q + 12]);
 }
 
-// inverse role (s', g, k1 = 2t + h): bins k1 + 8 k2 summed over the 4 input streams,
-// +32768 on the DC bin (decode offset on every output), 4-point inverse, twiddles
-// 2^(-(16 + mm) k1) for the 16 kept outputs
+// inverse role (s', g, k1 = 2t + h): bins k1 + 8 k2 of sum_t'' X_t'' W_st''g as 64-bit
+// multiply-accumulates (X canonical < 2^17, W < 2^32: below 2^51), folded once per bin
+// (2^32 == 1 mod 2^32 - 1); +32768 on the DC bin (decode offset on every output),
+// 4-point inverse, twiddles 2^(-(16 + mm) k1) for the 16 kept outputs
 __device__ __forceinline__ void partial_inverse(const PolWarp& S, int sp, int t, int g, int h,
                                                 uint32_t (&o)[16]) {
   const int k1 = 2 * t + h;
-  uint32_t Q[4];
+  uint64_t acc[4];
 #pragma unroll
   for (int tt = 0; tt < 4; ++tt) {
     const int r = 16 * sp + 4 * tt + 2 * g + h;
-    const uint4 v = reinterpret_cast<const uint4*>(S.buf + r * POL_BUF_P)[t ^ (tt & 1)];
-    if (tt == 0) {
-      Q[0] = v.x; Q[1] = v.y; Q[2] = v.z; Q[3] = v.w;
-    } else {
-      Q[0] = m_add(Q[0], v.x); Q[1] = m_add(Q[1], v.y);
-      Q[2] = m_add(Q[2], v.z); Q[3] = m_add(Q[3], v.w);
+    const uint4 w = reinterpret_cast<const uint4*>(S.buf + r * POL_BUF_P)[t ^ (tt & 1)];
+    const uint4 x = *reinterpret_cast<const uint4*>(&S.X[tt][4 * k1]);
+    const uint32_t wv[4] = {w.x, w.y, w.z, w.w}, xv[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const uint64_t pr = (uint64_t)xv[e] * wv[e];
+      acc[e] = tt == 0 ? pr : acc[e] + pr;
     }
   }
+  uint32_t Q[4];
+#pragma unroll
+  for (int e = 0; e < 4; ++e) Q[e] = m_add((uint32_t)acc[e], (uint32_t)(acc[e] >> 32));
   Q[0] = m_add(Q[0], k1 == 0 ? 32768u : 0u);
   to_bitrev<4>(Q);
   fnt_dit<4, RADIX256, true>(Q);
@@ -244,7 +248,7 @@ __device__ __forceinline__ int32_t pol_forward(PolWarp& S, int lane, bool fused)
     fnt16_taps(P);
   }
   if (fused) {
-    store_products(S, lane, t, h, P);
+    store_spectrum(S, lane, P);
     __syncwarp();
     uint32_t o[16];
     partial_inverse(S, sp, t, g, h, o);
@@ -257,17 +261,8 @@ __device__ __forceinline__ int32_t pol_forward(PolWarp& S, int lane, bool fused)
   }
   // per (s, t, group): the lane's 16 products of parity h through a 16-point inverse
   // (alpha^-2), twiddle 2^(-(16 + mm) h), summed over h when decoding
-  {
-    const uint4* xv = reinterpret_cast<const uint4*>(&S.X[t][16 * h]);
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const uint4 x = xv[q];
-      P[4 * q] = m_mul(P[4 * q], x.x);
-      P[4 * q + 1] = m_mul(P[4 * q + 1], x.y);
-      P[4 * q + 2] = m_mul(P[4 * q + 2], x.z);
-      P[4 * q + 3] = m_mul(P[4 * q + 3], x.w);
-    }
-  }
+  for (int j = 0; j < 16; ++j) P[j] = m_mul(P[j], pol_x(S, t, h, j));
   P[0] = m_add(P[0], h == 0 ? 32768u : 0u);
   to_bitrev<16>(P);
   fnt_dit<16, RADIX4, true>(P);

@@ -136,16 +136,29 @@ __device__ __forceinline__ int32_t unpack_group(uint32_t p, int g) {
 
 // FNT forward with the transform-domain sum over input streams (AEQ_FUSE_T): taps
 // are kept as balanced base-64 digits instead, w = 64 a + b with b in [-32, 31] and
-// |a| <= 256, packed the same way: p = a + b 2^16 = w 2^16 - a (2^22 - 1), so
-// unpack_group gives a (g = 0) and b (g = 1).
+// |a| <= 256.
+// The balanced digits are packed as two 16-bit halves, p = (a mod 2^16) | b << 16,
+// and read back with PRMT's sign-replicating selectors: one instruction per digit,
+// and the byte select can take the half from either of two words (own / partner).
+__device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
+  uint32_t r;
+  asm("prmt.b32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(b), "r"(sel));
+  return r;
+}
+constexpr uint32_t DIG_A = 0x9910u;    // sign-extended low half of the first word: digit a
+constexpr uint32_t DIG_B = 0xBB32u;    // sign-extended high half of the first word: digit b
+constexpr uint32_t DIG_A2 = 0xDD54u;   // digit a of the second word
+constexpr uint32_t DIG_B2 = 0xFF76u;   // digit b of the second word
 template <bool BAL>
 __device__ __forceinline__ uint32_t pack_taps(int32_t w) {
   if (!BAL) return pack_groups(w);
-  return (uint32_t)(w * 65536 - ((w + 32) >> 6) * 4194303);
+  const int32_t a = (w + 32) >> 6;                      // w = 64 a + b, b in [-32, 31]
+  return prmt((uint32_t)a, (uint32_t)(w - 64 * a), 0x5410u);
 }
 template <bool BAL>
 __device__ __forceinline__ int32_t unpack_tap(uint32_t p) {
-  return (BAL ? 64 : 128) * unpack_group(p, 0) + unpack_group(p, 1);
+  if (!BAL) return 128 * unpack_group(p, 0) + unpack_group(p, 1);
+  return 64 * (int32_t)prmt(p, 0u, DIG_A) + (int32_t)prmt(p, 0u, DIG_B);
 }
 // the reference's split_taps group g of a packed tap (fixedpoint.py:111-121)
 template <bool BAL>

@@ -207,7 +207,9 @@ __device__ __forceinline__ void lane_update(const AeqArgs& A, AeqScratch& S, int
       const double p = dmul(w, A.prm.tap_scale);
       const int32_t i = __double2int_rn(p);
       const int32_t c = min(max(i, -AEQ_TAP_MAX), AEQ_TAP_MAX);
-      smask |= (uint32_t)((c != i) | (p != p)) << kk;
+      // clipped exactly when |p| >= 16383.5 (rint rounds half to even: 16383.5 -> 16384);
+      // the negated compare also flags NaN
+      smask |= (uint32_t)!(fabs(p) < 16383.5) << kk;
       set_tap<BAL>(T, kk, c);
     }
     T.sat += __popc(smask);
@@ -511,11 +513,14 @@ __device__ __forceinline__ void lane_forward(AeqScratch& S, int lane, int cur, c
     // fixedpoint.py:111-121)
     uint32_t W[AEQ_N];
     if (fused) {
+      // digit g of tap kk (owned by lane g' = 0) and of tap 8 + kk (lane g' = 1): one
+      // PRMT each, from this lane's word or its partner's
+      const uint32_t sel_lo = g ? DIG_B2 : DIG_A, sel_hi = g ? DIG_B : DIG_A2;
 #pragma unroll
       for (int kk = 0; kk < 8; ++kk) {
         const uint32_t other = __shfl_xor_sync(0xffffffffu, T.gp[kk], 1);
-        W[bitrev(kk, 5)] = (uint32_t)unpack_group(g == 0 ? T.gp[kk] : other, g);      // tap kk
-        W[bitrev(8 + kk, 5)] = (uint32_t)unpack_group(g == 0 ? other : T.gp[kk], g);  // tap 8 + kk
+        W[bitrev(kk, 5)] = prmt(T.gp[kk], other, sel_lo);      // tap kk
+        W[bitrev(8 + kk, 5)] = prmt(T.gp[kk], other, sel_hi);  // tap 8 + kk
       }
     } else {
 #pragma unroll

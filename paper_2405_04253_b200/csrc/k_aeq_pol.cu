@@ -476,7 +476,7 @@ __global__ void __launch_bounds__(64, 4) k_aeq_pol(fntgpu_aeq_state* __restrict_
             const double pq = dmul(w, A.prm.tap_scale);
             const int32_t i = __double2int_rn(pq);
             c[kk] = min(max(i, -AEQ_TAP_MAX), AEQ_TAP_MAX);
-            smask |= (uint32_t)((c[kk] != i) | (pq != pq)) << kk;  // clipped, or NaN
+            smask |= (uint32_t)!(fabs(pq) < 16383.5) << kk;  // clipped (rint half-even), or NaN
           }
           sat += __popc(smask);
           if (__any_sync(0xffffffffu, smask != 0u)) {

@@ -175,10 +175,58 @@ __device__ __forceinline__ uint32_t stage_plane_f64(int8_t* dst, const double* s
 // |y| = 2^(k-1) + j 2^k, whose float64 outcome the host precomputed (io.q_tie).
 // requant_int when the host found every tie rounding away (CdcArgs.q_away): no tie
 // table lookup, no comparisons beyond the clamp
+// Signed form: for y < 0, (y + 2^(k-1) - 1) >> k (arithmetic) = -floor((|y| + 2^(k-1)) / 2^k).
 __device__ __forceinline__ int32_t requant_away(int32_t y, int k, int qmax) {
-  const int32_t q = min((abs(y) + (1 << (k - 1))) >> k, qmax);
-  return y < 0 ? -q : q;
+  const int32_t q = (y + (1 << (k - 1)) + (y >> 31)) >> k;
+  return max(min(q, qmax), -qmax);
 }
+
+// low bytes of four words packed into one (byte e = low byte of q[e])
+__device__ __forceinline__ uint32_t pack_bytes4(uint32_t q0, uint32_t q1, uint32_t q2, uint32_t q3) {
+  uint32_t lo, hi, r;
+  asm("prmt.b32 %0, %1, %2, 0x0040;" : "=r"(lo) : "r"(q0), "r"(q1));
+  asm("prmt.b32 %0, %1, %2, 0x0040;" : "=r"(hi) : "r"(q2), "r"(q3));
+  asm("prmt.b32 %0, %1, %2, 0x5410;" : "=r"(r) : "r"(lo), "r"(hi));
+  return r;
+}
+
+// Per-thread decimation statistics of one output parity: S2 = sum |y|^2 (< 2^34 for
+// the <= 8 outputs a thread of the fast epilogue owns per parity) and
+// S4 = sum |y|^4 as 96 bits (h:hi:lo). |y|^2 <= 2^31, so a pair of |y|^4 terms
+// fits 64 bits and one carry chain per pair suffices.
+struct DecimAcc {
+  unsigned long long s2 = 0;
+  uint32_t lo = 0, hi = 0, h = 0;
+  __device__ __forceinline__ void add_pair(uint32_t m0, uint32_t m1) {
+    s2 += (unsigned long long)m0 + m1;
+    const unsigned long long t = (unsigned long long)m0 * m0 + (unsigned long long)m1 * m1;  // < 2^63
+    asm("add.cc.u32 %0, %0, %3;\n\taddc.cc.u32 %1, %1, %4;\n\taddc.u32 %2, %2, 0;"
+        : "+r"(lo), "+r"(hi), "+r"(h)
+        : "r"((uint32_t)t), "r"((uint32_t)(t >> 32)));
+  }
+  // Warp sum into the (S2, S4 = w3 2^64 + w2 2^32 + w1) words at acc: 27-bit limbs,
+  // so each warp-wide redux.add of 32 limbs is exact in 32 bits. S2 < 2^35 and
+  // S4 < 2^66 per thread (h <= 1).
+  __device__ __forceinline__ void flush(unsigned long long* acc) const {
+    constexpr uint32_t M27 = (1u << 27) - 1;
+    const uint32_t A0 = __reduce_add_sync(0xffffffffu, (uint32_t)s2 & M27);
+    const uint32_t A1 = __reduce_add_sync(0xffffffffu, (uint32_t)(s2 >> 27));
+    const uint32_t L0 = __reduce_add_sync(0xffffffffu, lo & M27);
+    const uint32_t L1 = __reduce_add_sync(0xffffffffu, __funnelshift_r(lo, hi, 27) & M27);
+    const uint32_t L2 = __reduce_add_sync(0xffffffffu, (hi >> 22) | (h << 10));
+    if ((threadIdx.x & 31) == 0) {
+      // S4 = L0 + L1 2^27 + L2 2^54, regrouped on the 2^32 word boundaries
+      const unsigned long long w[4] = {
+          (unsigned long long)A0 + ((unsigned long long)A1 << 27),
+          (unsigned long long)L0 + ((unsigned long long)(L1 & 31u) << 27),
+          (unsigned long long)(L1 >> 5) + ((unsigned long long)(L2 & 1023u) << 22),
+          (unsigned long long)(L2 >> 10)};
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        if (w[q]) atomicAdd(acc + q, w[q]);
+    }
+  }
+};
 
 __device__ __forceinline__ int32_t requant_int(int32_t y, int k, const int8_t* tie, int qmax) {
   const int32_t a = abs(y);
@@ -211,8 +259,7 @@ __device__ __forceinline__ void cdc_epilogue_fast(const CdcArgs& A, const uint32
   const int k = io.q_shift, qmax = io.q_max;
   const int8_t* tie = io.q_tie;
   // accumulators for even (A) and odd (B) local indices
-  unsigned long long a2 = 0, b2 = 0, a4 = 0, b4 = 0;
-  uint32_t a4h = 0, b4h = 0;
+  DecimAcc sa, sb;
   for (int v = 4 * tid; v < CDC_BLK * CDC_HOP; v += 4 * CDC_CTA) {
     if (v + 4 <= lo || v >= hi) continue;
     const bool full = v >= lo && v + 4 <= hi;
@@ -242,11 +289,10 @@ __device__ __forceinline__ void cdc_epilogue_fast(const CdcArgs& A, const uint32
     if (CDC_PROBE != 1 && qr) {
       uint32_t pr = 0, pi = 0;
       if (A.q_away) {
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          pr |= ((uint32_t)requant_away(zr[e], k, qmax) & 0xffu) << (8 * e);
-          pi |= ((uint32_t)requant_away(zi[e], k, qmax) & 0xffu) << (8 * e);
-        }
+        pr = pack_bytes4(requant_away(zr[0], k, qmax), requant_away(zr[1], k, qmax),
+                         requant_away(zr[2], k, qmax), requant_away(zr[3], k, qmax));
+        pi = pack_bytes4(requant_away(zi[0], k, qmax), requant_away(zi[1], k, qmax),
+                         requant_away(zi[2], k, qmax), requant_away(zi[3], k, qmax));
       } else {
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
@@ -282,41 +328,24 @@ __device__ __forceinline__ void cdc_epilogue_fast(const CdcArgs& A, const uint32
       }
     }
     if (CDC_PROBE != 2 && stats) {
+      uint32_t m2[4];  // |y|^2 <= 2^31
 #pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const bool ok = full || (v + e >= lo && v + e < hi);
-        const uint32_t m2 = ok ? (uint32_t)(zr[e] * zr[e]) + (uint32_t)(zi[e] * zi[e]) : 0u;  // <= 2^31
-        const unsigned long long m4 = (unsigned long long)m2 * m2;                          // < 2^62
-        if (e & 1) {
-          b2 += m2;
-          b4 += m4;
-          b4h += (b4 < m4);
-        } else {
-          a2 += m2;
-          a4 += m4;
-          a4h += (a4 < m4);
-        }
+      for (int e = 0; e < 4; ++e) m2[e] = (uint32_t)(zr[e] * zr[e]) + (uint32_t)(zi[e] * zi[e]);
+      if (!full) {
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+          if (v + e < lo || v + e >= hi) m2[e] = 0u;
       }
+      sa.add_pair(m2[0], m2[2]);
+      sb.add_pair(m2[1], m2[3]);
     }
   }
+  static_assert(CDC_BLK * CDC_HOP / (4 * CDC_CTA) * 2 <= 8, "DecimAcc per-thread bounds");
   if (stats) {
     // even local indices carry phase (n0 & 1), odd ones the other phase
     const int pa = (int)(n0 & 1);
-    const unsigned long long va[4] = {a2, a4 & 0xffffffffull, a4 >> 32, a4h};
-    const unsigned long long vb[4] = {b2, b4 & 0xffffffffull, b4 >> 32, b4h};
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      unsigned long long x = va[q], y = vb[q];
-#pragma unroll
-      for (int off = 16; off > 0; off >>= 1) {
-        x += __shfl_xor_sync(0xffffffffu, x, off);
-        y += __shfl_xor_sync(0xffffffffu, y, off);
-      }
-      if ((tid & 31) == 0) {
-        if (x) atomicAdd(io.decim_acc + ((int64_t)s * 2 + pa) * 4 + q, x);
-        if (y) atomicAdd(io.decim_acc + ((int64_t)s * 2 + (pa ^ 1)) * 4 + q, y);
-      }
-    }
+    sa.flush(io.decim_acc + ((int64_t)s * 2 + pa) * 4);
+    sb.flush(io.decim_acc + ((int64_t)s * 2 + (pa ^ 1)) * 4);
   }
 }
 

@@ -500,6 +500,45 @@ def test_cdc_fused_requantization_tie_tables(cdc_kernel, ties):
     assert np.array_equal(y16i.cpu().numpy(), y32i.cpu().numpy().astype(np.int16))
 
 
+def test_cdc_fused_statistics_full_range(cdc_kernel):
+    """The fused decimation statistics (S2 = sum |y|^2, S4 = sum |y|^4 per stream and
+    output parity) and the int8 requantization at the int16 extremes: full-range int8
+    inputs, whose outputs wrap over the whole residue range, against numpy on the
+    kernel's own int16 outputs; streams of odd and ragged lengths."""
+    import torch
+    from paper_2405_04253_b200.stream import CdcBank
+    eng = _c2_engine()
+    bank = CdcBank(eng)
+    rng = np.random.default_rng(23)
+    for S, L in ((3, 70_001), (2, 4099), (1, 33)):
+        xr = rng.integers(-128, 128, (S, L)).astype(np.int8)
+        xi = rng.integers(-128, 128, (S, L)).astype(np.int8)
+        xr[0, : min(L, 4096)] = -128
+        xi[0, : min(L, 4096)] = 127 if S > 1 else -128
+        dxr, dxi = torch.from_numpy(xr).cuda(), torch.from_numpy(xi).cuda()
+        y16r = torch.empty((S, L), dtype=torch.int16, device="cuda")
+        y16i = torch.empty_like(y16r)
+        qr = torch.empty((S, L), dtype=torch.int8, device="cuda")
+        qi = torch.empty_like(qr)
+        acc = torch.zeros((S * 8,), dtype=torch.int64, device="cuda")
+        bank.run(dxr, dxi, yr=y16r, yi=y16i)
+        bank.run(dxr, dxi, qr=qr, qi=qi, q_spec=eng.sig_spec, decim_acc=acc)
+        yr = y16r.cpu().numpy().astype(np.int64)
+        yi = y16i.cpu().numpy().astype(np.int64)
+        assert np.abs(yr).max() >= 32000  # the wrap reaches the extremes
+        a64 = acc.cpu().numpy().astype(np.uint64).reshape(S, 2, 4)
+        for s in range(S):
+            for ph in range(2):
+                m2 = yr[s, ph::2] ** 2 + yi[s, ph::2] ** 2
+                w = [int(x) for x in a64[s, ph]]
+                assert w[0] == int(m2.sum()), (S, L, s, ph)
+                assert w[3] * 2 ** 64 + w[2] * 2 ** 32 + w[1] == sum(int(x) ** 2 for x in m2), (S, L, s, ph)
+        k, qmax = 7, int(eng.sig_spec.max_int)
+        for got, y in ((qr, yr), (qi, yi)):
+            q = np.minimum((np.abs(y) + (1 << (k - 1))) >> k, qmax)
+            assert np.array_equal(got.cpu().numpy(), np.where(y < 0, -q, q).astype(np.int8))
+
+
 @pytest.mark.parametrize("tag,cfg", [
     ("t33", dict(z_km=25.0, fs_hz=80e9, n_taps=33)),
     ("z0", dict(z_km=0.0, fs_hz=80e9, n_taps=32)),

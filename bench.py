@@ -414,12 +414,17 @@ def main():
         dist.destroy_process_group()
 
 
-def _uses_pol(args, n_streams: int) -> bool:
+AEQ_KERNEL_NAMES = {"warp": "k_aeq_process", "pol": "k_aeq_pol"}
+AEQ_POL_AUTO_PER_SM = 4  # k_aeq.cu use_pol_kernel
+
+
+def _aeq_layout(args, n_streams: int) -> str:
+    """The AEQ stream layout fntgpu_aeq_process runs (k_aeq.cu use_pol_kernel)."""
     if args.aeq_kernel != "auto":
-        return args.aeq_kernel == "pol"
+        return args.aeq_kernel
     import torch
     sms = torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count
-    return n_streams < 4 * sms  # k_aeq.cu use_pol_kernel (AEQ_POL_AUTO_PER_SM)
+    return "pol" if n_streams < AEQ_POL_AUTO_PER_SM * sms else "warp"
 
 
 def _ncu_traffic(name: str, world: int, full_size: bool):
@@ -504,7 +509,7 @@ def run_c5(args, world, rank, local) -> dict:
 
     peaks = measured_peaks()
     cdc_name = {"tc": "k_cdc64_tc", "umma": "k_cdc64_umma"}.get(args.cdc_kernel, "k_cdc64")
-    aeq_name = ("k_aeq_pol" if fwd == _lib.AEQ_FWD_FNT and _uses_pol(args, n_local)
+    aeq_name = (AEQ_KERNEL_NAMES[_aeq_layout(args, n_local)] if fwd == _lib.AEQ_FWD_FNT
                 else "k_aeq_process")
     n_blk_cdc = 2 * n_local * (L // 32 + 1)
     n_blk_aeq = n_local * chain.n_blocks

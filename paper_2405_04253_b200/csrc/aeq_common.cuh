@@ -20,7 +20,7 @@ namespace fntgpu {
 constexpr int AEQ_L = 16;            // taps per filter = hop (aeq.py:45)
 constexpr int AEQ_N = 32;            // block length
 constexpr int AEQ_TAP_MAX = 16383;   // TAP_MAG_MAX (aeq.py:26)
-constexpr int XF_LUT = 127;          // x / sig_scale table for |x| <= 127
+constexpr int XF_LUT = 128;          // x / sig_scale table for |x| <= 128 (int8 includes -128)
 
 struct AeqArgs {
   fntgpu_aeq_params prm;
@@ -167,8 +167,8 @@ __device__ __forceinline__ int32_t ref_group(uint32_t p, int g) {
   return tap_group(unpack_tap<true>(p), g);
 }
 
-// x / sig_scale exactly as numpy's true_divide (IEEE). Inputs narrower than 16 bits
-// always hit the table; wider ones fall back to the division.
+// x / sig_scale exactly as numpy's true_divide (IEEE) from a table of the int8 range
+// (all of it, -128 included); wider inputs fall back to the division.
 template <bool NARROW>
 __device__ __forceinline__ double xf_of(int32_t x, const double* lut, double sig) {
   if (NARROW) return lut[x + XF_LUT];

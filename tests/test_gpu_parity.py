@@ -713,6 +713,22 @@ def test_aeq_wide_inputs_match_oracle(forward, aeq_kernel):
     assert np.array_equal(eq.w, oq.w)
 
 
+@pytest.mark.parametrize("forward", AEQ_MODES)
+def test_aeq_int8_extremes_vs_oracle(forward, aeq_kernel):
+    """int8 inputs over the whole int8 range, -128 included (the update's x / sig_scale
+    for every int8 value), adapting, against the oracle: y, w, w_int and err_trace."""
+    rng = np.random.default_rng(29)
+    x = rng.integers(-128, 128, (4, 16 * 48))
+    x[:, ::7] = -128
+    x[1, 5::11] = 127
+    eq = _aeq(mu=1e-7, forward=forward)
+    oq = O.Aeq(SIG_SCALE, mu=1e-7)
+    assert np.array_equal(eq.process(x), oq.process(x))
+    assert np.array_equal(eq.w, oq.w)
+    assert np.array_equal(eq.taps.w_int, oq.w_int)
+    assert np.array_equal(np.asarray(eq.err_trace), np.asarray(oq.err_trace))
+
+
 def test_aeq_bank_many_streams_vs_oracle(aeq_kernel):
     """The multi-stream kernel (one warp per stream) against the oracle on
     independent random streams with the LinkConfig gear-shift schedule."""

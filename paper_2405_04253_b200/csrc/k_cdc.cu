@@ -204,29 +204,28 @@ struct DecimAcc {
         : "+r"(lo), "+r"(hi), "+r"(h)
         : "r"((uint32_t)t), "r"((uint32_t)(t >> 32)));
   }
-  // Warp sum into the (S2, S4 = w3 2^64 + w2 2^32 + w1) words at acc: 27-bit limbs,
-  // so each warp-wide redux.add of 32 limbs is exact in 32 bits. S2 < 2^35 and
+  // Warp sums as 27-bit limbs (S2 = A0 + A1 2^27, S4 = L0 + L1 2^27 + L2 2^54), so
+  // each warp-wide redux.add of 32 limbs is exact in 32 bits: S2 < 2^35 and
   // S4 < 2^66 per thread (h <= 1).
-  __device__ __forceinline__ void flush(unsigned long long* acc) const {
+  __device__ __forceinline__ void warp_limbs(uint32_t (&l)[5]) const {
     constexpr uint32_t M27 = (1u << 27) - 1;
-    const uint32_t A0 = __reduce_add_sync(0xffffffffu, (uint32_t)s2 & M27);
-    const uint32_t A1 = __reduce_add_sync(0xffffffffu, (uint32_t)(s2 >> 27));
-    const uint32_t L0 = __reduce_add_sync(0xffffffffu, lo & M27);
-    const uint32_t L1 = __reduce_add_sync(0xffffffffu, __funnelshift_r(lo, hi, 27) & M27);
-    const uint32_t L2 = __reduce_add_sync(0xffffffffu, (hi >> 22) | (h << 10));
-    if ((threadIdx.x & 31) == 0) {
-      // S4 = L0 + L1 2^27 + L2 2^54, regrouped on the 2^32 word boundaries
-      const unsigned long long w[4] = {
-          (unsigned long long)A0 + ((unsigned long long)A1 << 27),
-          (unsigned long long)L0 + ((unsigned long long)(L1 & 31u) << 27),
-          (unsigned long long)(L1 >> 5) + ((unsigned long long)(L2 & 1023u) << 22),
-          (unsigned long long)(L2 >> 10)};
-#pragma unroll
-      for (int q = 0; q < 4; ++q)
-        if (w[q]) atomicAdd(acc + q, w[q]);
-    }
+    l[0] = __reduce_add_sync(0xffffffffu, (uint32_t)s2 & M27);
+    l[1] = __reduce_add_sync(0xffffffffu, (uint32_t)(s2 >> 27));
+    l[2] = __reduce_add_sync(0xffffffffu, lo & M27);
+    l[3] = __reduce_add_sync(0xffffffffu, __funnelshift_r(lo, hi, 27) & M27);
+    l[4] = __reduce_add_sync(0xffffffffu, (hi >> 22) | (h << 10));
   }
 };
+
+// Limb sums of a CTA (each < 2^35) into the (S2, S4 = w3 2^64 + w2 2^32 + w1) words at
+// acc, S4 regrouped on the 2^32 word boundaries
+__device__ __forceinline__ void decim_flush(unsigned long long* acc, const unsigned long long (&l)[5]) {
+  const unsigned long long w[4] = {l[0] + (l[1] << 27), l[2] + ((l[3] & 31u) << 27),
+                                   (l[3] >> 5) + ((l[4] & 1023u) << 22), l[4] >> 10};
+#pragma unroll
+  for (int q = 0; q < 4; ++q)
+    if (w[q]) atomicAdd(acc + q, w[q]);
+}
 
 __device__ __forceinline__ int32_t requant_int(int32_t y, int k, const int8_t* tie, int qmax) {
   const int32_t a = abs(y);
@@ -342,10 +341,35 @@ __device__ __forceinline__ void cdc_epilogue_fast(const CdcArgs& A, const uint32
   }
   static_assert(CDC_BLK * CDC_HOP / (4 * CDC_CTA) * 2 <= 8, "DecimAcc per-thread bounds");
   if (stats) {
-    // even local indices carry phase (n0 & 1), odd ones the other phase
-    const int pa = (int)(n0 & 1);
-    sa.flush(io.decim_acc + ((int64_t)s * 2 + pa) * 4);
-    sb.flush(io.decim_acc + ((int64_t)s * 2 + (pa ^ 1)) * 4);
+    // warp limb sums -> shared memory -> one thread per (parity, limb) sums the CTA's
+    // warps -> one set of atomics per CTA and parity
+    constexpr int NW = CDC_CTA / 32;
+    __shared__ uint32_t red[10][NW];
+    uint32_t la[5], lb[5];
+    sa.warp_limbs(la);
+    sb.warp_limbs(lb);
+    if ((tid & 31) == 0) {
+#pragma unroll
+      for (int i = 0; i < 5; ++i) {
+        red[i][tid >> 5] = la[i];
+        red[5 + i][tid >> 5] = lb[i];
+      }
+    }
+    __syncthreads();
+    if (tid < 32) {
+      unsigned long long v = 0;
+      if (tid < 10) {
+#pragma unroll
+        for (int w = 0; w < NW; ++w) v += red[tid][w];
+      }
+      unsigned long long l[5];
+#pragma unroll
+      for (int i = 0; i < 5; ++i) l[i] = __shfl_sync(0xffffffffu, v, (tid < 5 ? 0 : 5) + i);
+      // even local indices carry phase (n0 & 1), odd ones the other phase
+      const int pa = (int)(n0 & 1);
+      if (tid == 0) decim_flush(io.decim_acc + ((int64_t)s * 2 + pa) * 4, l);
+      if (tid == 5) decim_flush(io.decim_acc + ((int64_t)s * 2 + (pa ^ 1)) * 4, l);
+    }
   }
 }
 

@@ -41,7 +41,11 @@
 
 namespace fntgpu {
 
-constexpr int POL_ERR_K = 4;    // blocks between the two warps' err_trace meetings
+#ifndef AEQ_POL_ERR_K
+#define AEQ_POL_ERR_K 4
+#endif
+constexpr int POL_ERR_K = AEQ_POL_ERR_K;  // blocks between the two warps' err_trace meetings
+static_assert(POL_ERR_K % 4 == 0, "err_trace means are formed four blocks per pass");
 constexpr int POL_BUF_P = 40;   // product row pitch (words): conflict-free (see below)
 constexpr int POL_PART_P = 20;  // partial-inverse row pitch (words)
 constexpr int POL_TV_P = 20;    // tap-variant row pitch (words)
@@ -501,17 +505,21 @@ __global__ void __launch_bounds__(64, 4) k_aeq_pol(fntgpu_aeq_state* __restrict_
           // warp 0 forms the means in numpy's pairwise order (k_aeq.cu lane_update)
           __syncthreads();
           if (p == 0) {
-            const int64_t bb = b - (b % POL_ERR_K) + (lane >> 3);
-            const int j = lane & 7;
-            double r = 0.0;
-            if (bb <= b) {
-              const double* a = SS.eabs[bb % (2 * POL_ERR_K)];
-              r = dadd(dadd(dadd(a[j], a[j + 8]), a[j + 16]), a[j + 24]);
+            // four blocks per pass, one per group of 8 lanes
+#pragma unroll
+            for (int q = 0; q < POL_ERR_K; q += 4) {
+              const int64_t bb = b - (b % POL_ERR_K) + q + (lane >> 3);
+              const int j = lane & 7;
+              double r = 0.0;
+              if (bb <= b) {
+                const double* a = SS.eabs[bb % (2 * POL_ERR_K)];
+                r = dadd(dadd(dadd(a[j], a[j + 8]), a[j + 16]), a[j + 24]);
+              }
+              r = dadd(r, __shfl_xor_sync(0xffffffffu, r, 1));
+              r = dadd(r, __shfl_xor_sync(0xffffffffu, r, 2));
+              r = dadd(r, __shfl_xor_sync(0xffffffffu, r, 4));
+              if (j == 0 && bb <= b) err_out[bb] = dmul(r, 1.0 / 32.0);
             }
-            r = dadd(r, __shfl_xor_sync(0xffffffffu, r, 1));
-            r = dadd(r, __shfl_xor_sync(0xffffffffu, r, 2));
-            r = dadd(r, __shfl_xor_sync(0xffffffffu, r, 4));
-            if (j == 0 && bb <= b) err_out[bb] = dmul(r, 1.0 / 32.0);
           }
         }
         // block b's gradient has read its window: block b+1's x / sig may land

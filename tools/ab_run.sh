@@ -10,7 +10,7 @@ n = sys.argv[1]
 try:
     d = json.load(open(f"gpurun_out/ab_{n}.json"))
     k = d["roofline"].get("kernels", {})
-    aeq = k.get("k_aeq_process", {}).get("ms", float("nan"))
+    aeq = next((v.get("ms") for kk, v in k.items() if kk.startswith("k_aeq")), float("nan"))
     cdc = next((v.get("ms") for kk, v in k.items() if kk.startswith("k_cdc64")), float("nan"))
     print(f"{n:12s} step {d['ms_per_step']:8.2f} ms  value {d['value']:8.2f}  aeq {aeq:8.2f}  cdc {cdc:7.2f}  frac {d['roofline']['frac']:.3f}")
 except Exception as e:

@@ -173,9 +173,10 @@ def _cpu_task(args):
     return time.perf_counter() - t0
 
 
-def run_cpu_baseline(engine, cfg, n_sym: int, cores: int, rounds: int | None = None) -> dict:
+def run_cpu_baseline(engine, cfg, n_sym: int, cores: int, rounds: int | None = None,
+                     seconds: float = 20.0) -> dict:
     """Time the reference algorithm (numpy port) on all host cores: one config-5
-    link of n_sym symbols per task, one process per core, ~20 s of CPU work."""
+    link of n_sym symbols per task, one process per core, ~`seconds` of wall time."""
     from concurrent.futures import ProcessPoolExecutor
     import oracle.np_port  # noqa: F401  (checker / baseline only)
     hop = 16
@@ -188,7 +189,7 @@ def run_cpu_baseline(engine, cfg, n_sym: int, cores: int, rounds: int | None = N
         busy, r = 0.0, 0
         t0 = time.perf_counter()
         # rounds of one link per core until ~20 s of wall time (or the requested count)
-        while (r < rounds) if rounds is not None else (time.perf_counter() - t0 < 20.0 and r < 400):
+        while (r < rounds) if rounds is not None else (time.perf_counter() - t0 < seconds and r < 400):
             busy += sum(ex.map(_cpu_task, [mk(cores * (r + 1) + i) for i in range(cores)]))
             r += 1
         rounds = r
@@ -236,8 +237,10 @@ def impl_reference(args) -> None:
         return
     for _ in range(args.warmup and 1):
         run_cpu_baseline(eng, cfg, n_sym, cores, rounds=1)
+    # each step a bounded sample: the whole --steps K run stays within ~2 minutes
+    per_step = max(3.0, 120.0 / max(args.steps, 1))
     t0 = time.perf_counter()
-    vals = [run_cpu_baseline(eng, cfg, n_sym, cores) for _ in range(args.steps)]
+    vals = [run_cpu_baseline(eng, cfg, n_sym, cores, seconds=per_step) for _ in range(args.steps)]
     wall = time.perf_counter() - t0
     v = float(np.mean([x["value"] for x in vals]))
     line = {

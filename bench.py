@@ -798,9 +798,25 @@ def run_e2e(args, eng, cfg, xr, xi, fwd, world, n_local) -> dict:
     h2d = sum(chains[b_ - a_].h2d_bytes for a_, b_ in slabs)
     d2h = sum(chains[b_ - a_].d2h_bytes for a_, b_ in slabs)
     del chains, hx_r, hx_i
+    # the PCIe roofline of this box: a pinned 1 GiB device-to-host copy
+    pin = torch.empty(1 << 30, dtype=torch.uint8, pin_memory=True)
+    dev = torch.empty(1 << 30, dtype=torch.uint8, device="cuda")
+    pin.copy_(dev, non_blocking=True)
+    torch.cuda.synchronize()
+    a.record()
+    for _ in range(4):
+        pin.copy_(dev, non_blocking=True)
+    b.record()
+    torch.cuda.synchronize()
+    d2h_peak = 4 * (1 << 30) / (a.elapsed_time(b) * 1e-3) / 1e9
+    del pin, dev
+    d2h_gbs = d2h / (ms / steps * 1e-3) / 1e9
     return {"value": samples / (ms * 1e-3) / 1e9, "unit": UNIT,
             "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
             "ms_per_step": ms / steps, "steps": steps, "links_per_gpu": n_local,
+            "pcie": {"d2h_gbs": d2h_gbs, "d2h_peak_gbs": d2h_peak, "frac": d2h_gbs / d2h_peak,
+                     "note": "the step moves the float64 outputs back over PCIe; peak = pinned 1 GiB "
+                             "device-to-host copy measured in this run (H2D runs concurrently)"},
             "path": "paper_2405_04253_b200.stream.HostChain over every link of the job in %d-link "
                     "slabs: pinned host int8 I/Q -> H2D -> CDC -> phase -> AEQ -> D2H float64 y + "
                     "err_trace, every step; copies pipelined with the kernels over 3 CUDA streams"

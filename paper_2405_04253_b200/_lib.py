@@ -10,8 +10,11 @@ the current CUDA stream handle.
 
 from __future__ import annotations
 
+import contextlib
 import ctypes as C
+import functools
 import os
+import threading
 from pathlib import Path
 
 import numpy as np
@@ -180,6 +183,46 @@ def device():
 
 def stream_handle():
     return vp(torch().cuda.current_stream().cuda_stream)
+
+
+_tls = threading.local()
+
+
+@contextlib.contextmanager
+def api_stream():
+    """Stream for one drop-in API call (fnt / convolutions / quantize_real / the CDC and
+    AEQ engines). A caller inside its own torch stream context keeps that stream; a
+    caller on the default stream gets its host thread's own non-blocking stream, so
+    calls from different threads -- one engine per thread, the reference's threading
+    convention -- overlap on the GPU instead of serializing on
+    the legacy default stream. Every drop-in call returns host arrays, i.e. it has
+    synchronized its stream before returning, so device state left by one call is
+    complete when any thread makes the next."""
+    t = torch()
+    if not t.cuda.is_available():  # the call itself reports the missing device
+        yield
+        return
+    dev = device()
+    if t.cuda.current_stream(dev) != t.cuda.default_stream(dev):
+        yield
+        return
+    s = getattr(_tls, "streams", None)
+    if s is None:
+        s = _tls.streams = {}
+    st = s.get(dev.index)
+    if st is None:
+        st = s[dev.index] = t.cuda.Stream(device=dev)
+    with t.cuda.stream(st):
+        yield
+
+
+def on_api_stream(fn):
+    """Decorator: run `fn` inside api_stream()."""
+    @functools.wraps(fn)
+    def wrapper(*args, **kwargs):
+        with api_stream():
+            return fn(*args, **kwargs)
+    return wrapper
 
 
 def ptr(t) -> vp:

@@ -158,20 +158,26 @@ class FntAeq:
         self.err_trace: list[float] = []
         self._tap_spectra = None
         self._prm = aeq_params(config, forward)
-        self._state = _lib.zeros((_lib.AEQ_STATE_BYTES,), np.uint8)
-        lib = _lib.load()
-        _lib.check(lib.fntgpu_aeq_init(_lib.ptr(self._state), 1, C.byref(self._prm),
-                                       _lib.stream_handle()), "aeq_init")
+        with _lib.api_stream():
+            self._state = _lib.zeros((_lib.AEQ_STATE_BYTES,), np.uint8)
+            lib = _lib.load()
+            _lib.check(lib.fntgpu_aeq_init(_lib.ptr(self._state), 1, C.byref(self._prm),
+                                           _lib.stream_handle()), "aeq_init")
+            # complete before the engine is used from any thread's stream
+            _lib.torch().cuda.current_stream().synchronize()
 
     # -- device state views -----------------------------------------------------
 
+    @_lib.on_api_stream
     def _read(self) -> _lib.AeqState:
         raw = _lib.to_host(self._state)
         return _lib.AeqState.from_buffer_copy(raw.tobytes())
 
+    @_lib.on_api_stream
     def _write(self, st: _lib.AeqState) -> None:
         raw = np.frombuffer(bytes(st), dtype=np.uint8).copy()
         self._state.copy_(_lib.torch().from_numpy(raw).to(self._state.device))
+        _lib.torch().cuda.current_stream().synchronize()
 
     @property
     def w(self) -> np.ndarray:
@@ -216,6 +222,7 @@ class FntAeq:
 
     # -- forward / update -------------------------------------------------------
 
+    @_lib.on_api_stream
     def _launch(self, x: np.ndarray, n_blocks: int, adapt: bool, mu_blocks: np.ndarray | None):
         hop = self.config.l_taps
         n = n_blocks * hop
@@ -270,6 +277,7 @@ class FntAeq:
         y = self._launch(x_new, 1, False, None)
         return y, x_block
 
+    @_lib.on_api_stream
     def update_taps(self, x_block: np.ndarray, y: np.ndarray, mu: float | None = None) -> None:
         """Block-accumulated RDE update, requantize, resplit (aeq.py:148-170)."""
         cfg = self.config
@@ -302,6 +310,7 @@ class FntAeq:
         return self._launch(x, n_blocks, adapt, mu_blocks)
 
 
+@_lib.on_api_stream
 def td_aeq_float(x: np.ndarray, config: AeqConfig, mu_schedule=None,
                  w0: np.ndarray | None = None) -> tuple[np.ndarray, np.ndarray]:
     """Per-symbol float 4x4 RDE baseline (aeq.py:193-249): returns (outputs, final taps).

@@ -206,6 +206,7 @@ class FntCdcEngine:
 
     # -- stream API -----------------------------------------------------------
 
+    @_lib.on_api_stream
     def _run(self, xr, xi, out_dtype: int):
         xr = _int_input(xr)
         xi = _int_input(xi)
@@ -286,6 +287,7 @@ class FntCdcEngine:
         return outs[0]
 
 
+@_lib.on_api_stream
 def fd_cdc_float(x: np.ndarray, cfg: CdcConfig, taps: np.ndarray | None = None) -> np.ndarray:
     """Float FFT overlap-save baseline (cdc.py:183-198), on the GPU via torch.fft.
     Not part of the FNT hot path (comparator only)."""

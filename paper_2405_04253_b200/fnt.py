@@ -13,6 +13,7 @@ and copied back as int64.
 from __future__ import annotations
 
 import ctypes as C
+import threading
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -39,6 +40,9 @@ def _stage_tables(root: int, n: int, F: int) -> tuple:
     lg = n.bit_length() - 1
     return tuple(np.array([pow(root, j * (n >> (s + 1)), F) for j in range(1 << s)],
                           dtype=np.int64) for s in range(lg))
+
+
+_PLAN_LOCK = threading.RLock()
 
 
 class _DevicePlan:
@@ -77,22 +81,24 @@ class TransformPlan:
         """The GPU copy of this plan, created lazily on first use. The host
         twiddle tables are authoritative (callers may edit them, cli.py:84-86):
         if they no longer match what the device holds, they are re-uploaded."""
-        if not self._dev:
-            # the device starts from the canonical tables of (t, n, alpha)
-            F = self.params.F
-            canon = (_stage_tables(self.alpha, self.n, F), _stage_tables(self.alpha_inv, self.n, F))
-            self._dev.append(_DevicePlan(self.params.t, self.n, self.alpha))
-            self._dev.append(self._tables_digest(*canon))
-        dig = self._tables_digest()
-        if dig != self._dev[1]:
-            fwd = np.ascontiguousarray(np.concatenate(self.fwd_twiddles), dtype=np.int64)
-            inv = np.ascontiguousarray(np.concatenate(self.inv_twiddles), dtype=np.int64)
-            lib = _lib.load()
-            _lib.check(lib.fntgpu_plan_set_twiddles(
-                self._dev[0].handle, fwd.ctypes.data_as(C.c_void_p),
-                inv.ctypes.data_as(C.c_void_p)), "plan_set_twiddles")
-            self._dev[1] = dig
-        return self._dev[0]
+        with _PLAN_LOCK:  # plans are shared by every thread (fnt.py: immutable, reentrant)
+            if not self._dev:
+                # the device starts from the canonical tables of (t, n, alpha)
+                F = self.params.F
+                canon = (_stage_tables(self.alpha, self.n, F),
+                         _stage_tables(self.alpha_inv, self.n, F))
+                self._dev.append(_DevicePlan(self.params.t, self.n, self.alpha))
+                self._dev.append(self._tables_digest(*canon))
+            dig = self._tables_digest()
+            if dig != self._dev[1]:
+                fwd = np.ascontiguousarray(np.concatenate(self.fwd_twiddles), dtype=np.int64)
+                inv = np.ascontiguousarray(np.concatenate(self.inv_twiddles), dtype=np.int64)
+                lib = _lib.load()
+                _lib.check(lib.fntgpu_plan_set_twiddles(
+                    self._dev[0].handle, fwd.ctypes.data_as(C.c_void_p),
+                    inv.ctypes.data_as(C.c_void_p)), "plan_set_twiddles")
+                self._dev[1] = dig
+            return self._dev[0]
 
     def _tables_digest(self, fwd=None, inv=None) -> bytes:
         fwd = self.fwd_twiddles if fwd is None else fwd
@@ -129,6 +135,7 @@ def _check_len(plan: TransformPlan, a: np.ndarray) -> None:
         raise ValueError(f"expected length {plan.n}, got {a.shape[-1]}")
 
 
+@_lib.on_api_stream
 def _transform(plan: TransformPlan, x, inverse: bool) -> np.ndarray:
     a = _as_i64(x)
     _check_len(plan, a)
@@ -158,6 +165,7 @@ def _broadcast_pair(plan, a, b):
     return shape
 
 
+@_lib.on_api_stream
 def _conv_real(plan: TransformPlan, x: np.ndarray, h: np.ndarray, flags: int) -> np.ndarray:
     shape = _broadcast_pair(plan, x, h)
     size = int(np.prod(shape))
@@ -190,6 +198,7 @@ def cyclic_convolve_real(plan: TransformPlan, x: np.ndarray, h: np.ndarray) -> n
     return out
 
 
+@_lib.on_api_stream
 def _conv_complex(plan, xr, xi, yr, yi, flags):
     shape = np.broadcast_shapes(xr.shape, xi.shape, yr.shape, yi.shape)
     size = int(np.prod(shape))
@@ -261,6 +270,7 @@ def convolve_signed_complex(plan: TransformPlan, x_re: np.ndarray, x_im: np.ndar
     return zr, zi
 
 
+@_lib.on_api_stream
 def _residue_map(v: np.ndarray, p: FermatParams, signed_out: bool, decode_only: bool = False):
     if v.size == 0:
         return np.empty(v.shape, dtype=np.int64)

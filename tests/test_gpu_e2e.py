@@ -106,3 +106,56 @@ def test_pipelined_chain_equals_resident_chain():
         torch.cuda.synchronize()
         assert torch.equal(pc.y, ref.y) and torch.equal(pc.err, ref.err), upto
         assert torch.equal(pc.phase, ref.phase), upto
+
+
+def _dropin_link(eng, cfg, fe):
+    """One link through the reference-facing API on numpy arrays (bench.run_dropin)."""
+    from paper_2405_04253_b200.stream import reference_phase
+    streams = [eng.process(a, b) for a, b in fe]
+    ph = reference_phase(streams)
+    dec = [s[ph::2] for s in streams]
+    q = np.stack([P.quantize_real(v, cfg.sig_spec())[0]
+                  for v in (dec[0].real, dec[0].imag, dec[1].real, dec[1].imag)])
+    eq = P.FntAeq(cfg.aeq_config())
+    y = eq.process(q, adapt=True, mu_schedule=cfg.mu_schedule())
+    return y, np.array(eq.err_trace), eq.w
+
+
+def test_dropin_api_threads_equal_sequential():
+    """Engines used from several host threads (one per thread, the reference's
+    convention) run on per-thread CUDA streams concurrently and return exactly the
+    single-thread results; an engine built in one thread and used in another is
+    ordered too."""
+    from concurrent.futures import ThreadPoolExecutor
+    from paper_2405_04253_b200.linkgen import DeviceLinkGenerator
+    n_links, n_sym = 8, 1 << 12
+    cfg = P.LinkConfig(n_symbols=n_sym, z_km=75.0, seed=4)
+    gen = DeviceLinkGenerator(n_sym)
+    xr, xi = gen.generate(n_links, seed=21)
+    data = [[(xr[2 * l + p].cpu().numpy().astype(np.int64), xi[2 * l + p].cpu().numpy().astype(np.int64))
+             for p in range(2)] for l in range(n_links)]
+    eng = P.FntCdcEngine(cfg.cdc_config("fnt"), cfg.sig_spec())
+    seq = [_dropin_link(eng, cfg, fe) for fe in data]
+
+    def worker(fe):
+        e = P.FntCdcEngine(cfg.cdc_config("fnt"), cfg.sig_spec())
+        return _dropin_link(e, cfg, fe)
+
+    for _ in range(2):
+        with ThreadPoolExecutor(max_workers=n_links) as ex:
+            par = list(ex.map(worker, data))
+        for (y0, e0, w0), (y1, e1, w1) in zip(seq, par):
+            assert np.array_equal(y0, y1) and np.array_equal(e0, e1) and np.array_equal(w0, w1)
+    # handoff: build the AEQ engine in one thread, run it in another
+    fe = data[0]
+    streams = [eng.process(a, b) for a, b in fe]
+    from paper_2405_04253_b200.stream import reference_phase
+    ph = reference_phase(streams)
+    dec = [s[ph::2] for s in streams]
+    q = np.stack([P.quantize_real(v, cfg.sig_spec())[0]
+                  for v in (dec[0].real, dec[0].imag, dec[1].real, dec[1].imag)])
+    with ThreadPoolExecutor(max_workers=1) as ex:
+        eq = ex.submit(P.FntAeq, cfg.aeq_config()).result()
+    with ThreadPoolExecutor(max_workers=1) as ex:
+        y = ex.submit(eq.process, q, True, cfg.mu_schedule()).result()
+    assert np.array_equal(y, seq[0][0]) and np.array_equal(eq.w, seq[0][2])

@@ -1115,7 +1115,32 @@ def run_c1(args) -> dict:
         run()
     b.record()
     torch.cuda.synchronize()
-    k_us = a.elapsed_time(b)  # ms for 1000 launches = us per launch
+    loop_us = a.elapsed_time(b)  # ms for 1000 launches = us per launch (host launch rate bound)
+    # the kernel alone: 100 launches captured in a CUDA graph, replayed 10 times (the
+    # Python/ctypes launch loop above cannot issue a ~5 us kernel back to back)
+    k_us, timing = loop_us, "1000 launches from a Python loop (CUDA events)"
+    try:
+        g = torch.cuda.CUDAGraph()
+        cs = torch.cuda.Stream()
+        cs.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(cs):
+            with torch.cuda.graph(g, stream=cs):
+                gst = _lib.stream_handle()
+                for _ in range(100):
+                    lib.fntgpu_cyclic_convolve_real(dp.handle, dx.data_ptr(), dh.data_ptr(), 64,
+                                                    dz.data_ptr(), 16384, 0, gst)
+        torch.cuda.synchronize()
+        g.replay()
+        torch.cuda.synchronize()
+        a.record()
+        for _ in range(10):
+            g.replay()
+        b.record()
+        torch.cuda.synchronize()
+        k_us = a.elapsed_time(b)  # ms for 1000 graph-launched kernels = us per launch
+        timing = "100 launches captured in a CUDA graph, replayed 10 times (CUDA events)"
+    except Exception as e:  # noqa: BLE001 -- keep the loop number
+        timing += f" (graph capture failed: {e})"
     n = 16384 * 64
     peaks = measured_peaks()
     tops = n * C1_OPS_PER_ELEMENT / (k_us * 1e-6) / 1e12
@@ -1127,6 +1152,7 @@ def run_c1(args) -> dict:
                        "alg_ops_per_element": C1_OPS_PER_ELEMENT, "achieved_tops": tops,
                        "int_frac": tops / peaks["int_tops"],
                        "hbm_gbs_int64": n * 24 / (k_us * 1e-6) / 1e9,
+                       "timing": timing, "python_loop_us_per_launch": loop_us,
                        "note": "the API takes the reference's int64 arrays (24 B per element moved); "
                                "SURVEY 8(d)'s 6 B/element assumes int8 / int32 I/O"},
             "parity_vs_oracle": ok}

@@ -145,6 +145,74 @@ __global__ void __launch_bounds__(TILE) k_conv_real_fast(const int64_t* x, const
   stage_tile_out<N>(sX, z, b0, batch, flags);
 }
 
+// Per-vector taps (config 1: h_stride == N), two threads per vector: a CTA of two
+// warps owns PAIR_TILE consecutive vectors; warp 0 stages and transforms the signal
+// rows, warp 1 the tap rows (its spectra go back to shared memory), then warp 0
+// forms the N products and the inverse. Each warp stages its tile with batches of 32
+// independent loads per lane in flight (twice the memory-level parallelism and twice
+// the warps per SM of the one-thread-per-vector kernel, whose 512 warps over 148 SMs
+// left both the loads and the transforms latency-bound).
+constexpr int PAIR_TILE = 32;
+
+template <int N>
+__device__ __forceinline__ void stage_warp_in(uint32_t (*s)[N + 1], const int64_t* __restrict__ src,
+                                              int64_t rows, int lane) {
+  if (rows == PAIR_TILE) {
+    constexpr int PER = N, B = 32;  // N * PAIR_TILE words over 32 lanes
+#pragma unroll
+    for (int j0 = 0; j0 < PER; j0 += B) {
+      int64_t v[B];
+#pragma unroll
+      for (int j = 0; j < B; ++j) v[j] = __ldg(src + (j0 + j) * 32 + lane);
+#pragma unroll
+      for (int j = 0; j < B; ++j) {
+        const int e = (j0 + j) * 32 + lane;
+        s[e / N][e % N] = f4_enc64(v[j]);
+      }
+    }
+    return;
+  }
+  const int64_t words = rows * N;
+  for (int64_t e = lane; e < words; e += 32) s[e / N][e % N] = f4_enc64(src[e]);
+}
+
+template <int N, int KIND>
+__global__ void __launch_bounds__(2 * PAIR_TILE) k_conv_real_pair(const int64_t* x, const int64_t* h,
+                                                                   int64_t* z, int64_t batch, int flags) {
+  constexpr int LG = ilog2(N);
+  __shared__ uint32_t sX[PAIR_TILE][N + 1];
+  __shared__ uint32_t sH[PAIR_TILE][N + 1];
+  const int64_t b0 = (int64_t)blockIdx.x * PAIR_TILE;
+  const int64_t rows = batch - b0 < PAIR_TILE ? batch - b0 : PAIR_TILE;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint32_t (*own)[N + 1] = warp == 0 ? sX : sH;
+  stage_warp_in<N>(own, (warp == 0 ? x : h) + b0 * N, rows, lane);
+  __syncwarp();
+  uint32_t A[N];
+  row_bitrev<N>(A, own[lane]);
+  fnt_dit<N, KIND, false>(A);
+  if (warp == 1) {
+#pragma unroll
+    for (int i = 0; i < N; ++i) sH[lane][i] = A[i];  // tap spectrum of vector `lane`
+  }
+  __syncthreads();
+  if (warp == 0) {
+#pragma unroll
+    for (int i = 0; i < N; ++i) A[i] = m_mul(A[i], sH[lane][i]);  // the N general products (fnt.py:123)
+    to_bitrev<N>(A);
+    fnt_dit<N, KIND, true>(A);
+#pragma unroll
+    for (int i = 0; i < N; ++i) sX[lane][i] = m_rot(A[i], 32 - LG);
+  }
+  __syncthreads();
+  const int64_t words = rows * N;
+  int64_t* dst = z + b0 * N;
+  for (int64_t e = threadIdx.x; e < words; e += 2 * PAIR_TILE) {
+    const uint32_t v = sX[e / N][e % N];
+    dst[e] = (flags & FNTGPU_DECODE_SIGNED) ? (int64_t)f4_signed(v) : (int64_t)f4_canon(v);
+  }
+}
+
 // Staging of a complex tile in the combined form of Eqs. (7)-(8): P = re + 2^8 im,
 // M = re - 2^8 im (linearity lets the combination happen in the time domain).
 template <int N>
@@ -427,7 +495,10 @@ cudaError_t launch_fnt(const DevPlan& p, int inverse, const int64_t* x, int64_t*
 cudaError_t launch_conv_real(const DevPlan& p, const int64_t* x, const int64_t* h, int64_t h_stride,
                              int64_t* z, int64_t batch, int flags, cudaStream_t st) {
   if (batch <= 0) return cudaSuccess;
-  if (p.kind == KIND_SQRT2_64) {
+  if (p.kind == KIND_SQRT2_64 && h_stride != 0) {
+    k_conv_real_pair<64, SQRT2><<<(unsigned)((batch + PAIR_TILE - 1) / PAIR_TILE), 2 * PAIR_TILE, 0, st>>>(
+        x, h, z, batch, flags);
+  } else if (p.kind == KIND_SQRT2_64) {
     k_conv_real_fast<64, SQRT2><<<(unsigned)((batch + TILE - 1) / TILE), TILE, 0, st>>>(x, h, h_stride, z, batch, flags);
   } else if (p.kind == KIND_RADIX2_32) {
     k_conv_real_fast<32, RADIX2><<<(unsigned)((batch + TILE - 1) / TILE), TILE, 0, st>>>(x, h, h_stride, z, batch, flags);

@@ -196,13 +196,30 @@ __global__ void __launch_bounds__(2 * PAIR_TILE) k_conv_real_pair(const int64_t*
     for (int i = 0; i < N; ++i) sH[lane][i] = A[i];  // tap spectrum of vector `lane`
   }
   __syncthreads();
+  // The inverse, split over the two warps by its first decimation-in-frequency stage:
+  // with beta = alpha^-1 and beta^(N/2) = -1, the even outputs are the half-length
+  // inverse of u[k] = P[k] + P[k + N/2] and the odd ones that of
+  // v[k] = (P[k] - P[k + N/2]) beta^k (root beta^2 = alpha^-2 for both halves).
+  constexpr int H = N / 2;
+  constexpr int HKIND = KIND == SQRT2 ? RADIX2 : RADIX4;  // alpha^2: sqrt2^2 = 2, 2^2 = 4
   if (warp == 0) {
 #pragma unroll
     for (int i = 0; i < N; ++i) A[i] = m_mul(A[i], sH[lane][i]);  // the N general products (fnt.py:123)
-    to_bitrev<N>(A);
-    fnt_dit<N, KIND, true>(A);
 #pragma unroll
-    for (int i = 0; i < N; ++i) sX[lane][i] = m_rot(A[i], 32 - LG);
+    for (int k = 0; k < H; ++k) {
+      sX[lane][k] = m_add(A[k], A[k + H]);
+      const Tw t = twiddle<KIND>(m_sub(A[k], A[k + H]), (N - k) % N);
+      sH[lane][k] = t.neg ? ~t.v : t.v;  // -v = ~v in Z/(2^32 - 1)
+    }
+  }
+  __syncthreads();
+  {
+    uint32_t B[H];
+    row_bitrev<H>(B, warp == 0 ? sX[lane] : sH[lane]);
+    __syncthreads();  // every u row is read before either warp's outputs overwrite sX
+    fnt_dit<H, HKIND, true>(B);
+#pragma unroll
+    for (int m = 0; m < H; ++m) sX[lane][2 * m + warp] = m_rot(B[m], 32 - LG);  // * N^-1
   }
   __syncthreads();
   const int64_t words = rows * N;

@@ -232,6 +232,40 @@ def ptr(t) -> vp:
 _NP2T = {}
 
 
+# Host <-> device copies of the drop-in calls' numpy arrays go through two pinned
+# staging chunks per host thread (DMA at the pinned rate, chunk k + 1's copy
+# overlapping chunk k's host memcpy). Pageable cudaMemcpy stages through the driver's
+# own buffers one transfer at a time, which serialized the copies of concurrent
+# threads (the drop-in chain moves ~40 MB per link).
+_SMALL_COPY = 1 << 18
+_CHUNK = 16 << 20
+
+
+class _Stage(threading.local):
+    def __init__(self):
+        self.bufs = [None, None]
+        self.events = [None, None]
+
+
+_stage = _Stage()
+
+
+def _stage_buf(i: int, nbytes: int):
+    b = _stage.bufs[i]
+    if b is None or b.numel() < nbytes:
+        size = min(_CHUNK, max(1 << 20, 1 << (nbytes - 1).bit_length()))
+        b = torch().empty(size, dtype=torch().uint8, pin_memory=True)
+        _stage.bufs[i] = b
+    return b
+
+
+def _stage_ready(i: int) -> None:
+    ev = _stage.events[i]
+    if ev is not None:
+        ev.synchronize()  # the previous copy through staging chunk i has completed
+        _stage.events[i] = None
+
+
 def to_device(a: np.ndarray):
     """Contiguous host array -> device tensor (same dtype)."""
     t = torch()
@@ -240,7 +274,23 @@ def to_device(a: np.ndarray):
         a = a.copy()
     if a.size == 0:
         return t.empty(a.shape, dtype=_torch_dtype(a.dtype), device=device())
-    return t.from_numpy(a).to(device(), non_blocking=False)
+    if a.nbytes <= _SMALL_COPY:
+        return t.from_numpy(a).to(device(), non_blocking=False)
+    d = t.empty(a.shape, dtype=_torch_dtype(a.dtype), device=device())
+    src = a.reshape(-1).view(np.uint8)
+    dst = d.view(-1).view(t.uint8)
+    st = t.cuda.current_stream()
+    for k, off in enumerate(range(0, a.nbytes, _CHUNK)):
+        n = min(_CHUNK, a.nbytes - off)
+        i = k & 1
+        _stage_ready(i)
+        b = _stage_buf(i, n)
+        np.copyto(b.numpy()[:n], src[off:off + n])
+        dst[off:off + n].copy_(b[:n], non_blocking=True)
+        ev = t.cuda.Event()
+        ev.record(st)
+        _stage.events[i] = ev
+    return d
 
 
 def empty(shape, np_dtype):
@@ -253,8 +303,47 @@ def zeros(shape, np_dtype):
     return t.zeros(tuple(shape), dtype=_torch_dtype(np.dtype(np_dtype)), device=device())
 
 
-def to_host(t) -> np.ndarray:
-    return t.cpu().numpy()
+def to_host(x) -> np.ndarray:
+    """Device tensor -> a new numpy array (synchronous, like Tensor.cpu())."""
+    t = torch()
+    nbytes = x.numel() * x.element_size()
+    if nbytes <= _SMALL_COPY or not x.is_cuda:
+        return x.cpu().numpy()
+    x = x.contiguous()
+    out = np.empty(tuple(x.shape), dtype=_numpy_dtype(x.dtype))
+    src = x.view(-1).view(t.uint8)
+    dst = out.reshape(-1).view(np.uint8)
+    st = t.cuda.current_stream()
+    offs = list(range(0, nbytes, _CHUNK))
+
+    def issue(k):
+        off = offs[k]
+        n = min(_CHUNK, nbytes - off)
+        i = k & 1
+        _stage_ready(i)
+        b = _stage_buf(i, n)
+        b[:n].copy_(src[off:off + n], non_blocking=True)
+        ev = t.cuda.Event()
+        ev.record(st)
+        _stage.events[i] = ev
+
+    issue(0)
+    for k, off in enumerate(offs):
+        if k + 1 < len(offs):
+            issue(k + 1)  # the next chunk's DMA overlaps this chunk's memcpy
+        i = k & 1
+        n = min(_CHUNK, nbytes - off)
+        _stage_ready(i)
+        np.copyto(dst[off:off + n], _stage.bufs[i].numpy()[:n])
+    return out
+
+
+def _numpy_dtype(dt):
+    t = torch()
+    m = {t.int8: np.int8, t.int16: np.int16, t.int32: np.int32, t.int64: np.int64,
+         t.float64: np.float64, t.complex128: np.complex128, t.uint8: np.uint8,
+         t.float32: np.float32}
+    return np.dtype(m[dt])
 
 
 def _torch_dtype(dt: np.dtype):

@@ -259,6 +259,21 @@ def _stage_buf(i: int, nbytes: int):
     return b
 
 
+_PINNED = None
+
+
+def _pinned_ok() -> bool:
+    """Page-locked staging is available (else the plain pageable copies are used)."""
+    global _PINNED
+    if _PINNED is None:
+        try:
+            _stage_buf(0, 1 << 20)
+            _PINNED = True
+        except RuntimeError:
+            _PINNED = False
+    return _PINNED
+
+
 def _stage_ready(i: int) -> None:
     ev = _stage.events[i]
     if ev is not None:
@@ -274,7 +289,7 @@ def to_device(a: np.ndarray):
         a = a.copy()
     if a.size == 0:
         return t.empty(a.shape, dtype=_torch_dtype(a.dtype), device=device())
-    if a.nbytes <= _SMALL_COPY:
+    if a.nbytes <= _SMALL_COPY or not _pinned_ok():
         return t.from_numpy(a).to(device(), non_blocking=False)
     d = t.empty(a.shape, dtype=_torch_dtype(a.dtype), device=device())
     src = a.reshape(-1).view(np.uint8)
@@ -307,7 +322,7 @@ def to_host(x) -> np.ndarray:
     """Device tensor -> a new numpy array (synchronous, like Tensor.cpu())."""
     t = torch()
     nbytes = x.numel() * x.element_size()
-    if nbytes <= _SMALL_COPY or not x.is_cuda:
+    if nbytes <= _SMALL_COPY or not x.is_cuda or not _pinned_ok():
         return x.cpu().numpy()
     x = x.contiguous()
     out = np.empty(tuple(x.shape), dtype=_numpy_dtype(x.dtype))

@@ -8,7 +8,7 @@ import pytest
 
 import oracle as O
 import paper_2405_04253_b200 as P
-from conftest import SIG_SCALE, sha
+from conftest import ROOT, SIG_SCALE, sha
 
 pytestmark = pytest.mark.gpu
 
@@ -928,3 +928,17 @@ def test_aeq_division_and_ring_shortcuts(case):
                       tap_scale=case.get("tap_scale", float(1 << 13)),
                       **({"radii": case["radii"]} if "radii" in case else {}))
     assert aeq_selfcheck(cfg) == (0, 0)
+
+
+def test_randomized_differential_vs_oracle():
+    """A short run of tools/fuzz_parity.py (fixed seed): random AEQ states / inputs /
+    step sizes through both layouts and forwards, random CDC designs and lengths."""
+    import importlib.util
+    spec = importlib.util.spec_from_file_location("fuzz_parity", ROOT / "tools" / "fuzz_parity.py")
+    fz = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(fz)
+    rng = np.random.default_rng(2405)
+    stats = {}
+    for _ in range(150):
+        (fz.aeq_case if rng.random() < 0.7 else fz.cdc_case)(rng, stats)
+    assert sum(stats.values()) == 150

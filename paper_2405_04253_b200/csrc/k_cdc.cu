@@ -457,74 +457,13 @@ __device__ __forceinline__ int32_t sx8(uint32_t w, int k) {
   return r;
 }
 
-template <typename TIN, bool FAST>
-__global__ void __launch_bounds__(CDC_CTA, CDC_MIN_CTAS) k_cdc64(const __grid_constant__ CdcArgs A) {
-  constexpr bool F64IN = std::is_same<TIN, double>::value;  // quantized on load to int8
-  using TS = typename std::conditional<sizeof(TIN) == 1 || F64IN, int8_t, int32_t>::type;
-  // the input window and the u staging rows are never live at the same time
-  extern __shared__ __align__(16) unsigned char smem[];
-  TS* s_xr = reinterpret_cast<TS*>(smem);
-  TS* s_xi = s_xr + WIN;
-  uint32_t* s_u = reinterpret_cast<uint32_t*>(smem);  // [sign][block][UP]
-
+// One CTA item after its input window is staged in shared memory (s_xr, s_xi):
+// forward FNT-64 of this thread's block and sign, tap products, pruned inverse, then
+// the epilogue over the CTA's output range (s_u aliases the window).
+template <typename TS, bool FAST>
+__device__ __forceinline__ void cdc_item(const CdcArgs& A, int s, int64_t cta_blk0, const TS* s_xr,
+                                         const TS* s_xi, uint32_t* s_u) {
   const fntgpu_cdc_io& io = A.io;
-  const int s = A.s_base + (int)blockIdx.y;
-  const int64_t cta_blk0 = A.blk_begin + (int64_t)blockIdx.x * CDC_BLK;
-  const int64_t g0 = cta_blk0 * CDC_HOP - CDC_HOP;  // first input sample of block cta_blk0
-
-  const TIN* xr_s = reinterpret_cast<const TIN*>(io.xr) + (size_t)s * io.x_stride;
-  const TIN* xi_s = reinterpret_cast<const TIN*>(io.xi) + (size_t)s * io.x_stride;
-  bool bulk = false;
-  if (sizeof(TIN) == 1 && CDC_TMA) {
-    // interior windows of int8 planes: two 1-D bulk copies (TMA engine) straight into
-    // shared memory, completion counted on an mbarrier; edges and unaligned views
-    // take the vectorised load path
-    const int64_t lo = io.x_first > 0 ? io.x_first : 0;
-    const int64_t hi_avail = io.x_first + io.x_count;
-    const int64_t hi = hi_avail < io.length ? hi_avail : io.length;
-    const TIN* pr = xr_s + (g0 - io.x_first);
-    const TIN* pi = xi_s + (g0 - io.x_first);
-    bulk = g0 >= lo && g0 + WIN <= hi && ((reinterpret_cast<uintptr_t>(pr) | reinterpret_cast<uintptr_t>(pi)) & 15) == 0;
-    if (bulk) {
-      __shared__ __align__(8) uint64_t mbar;
-      const uint32_t mb = (uint32_t)__cvta_generic_to_shared(&mbar);
-      if (threadIdx.x == 0) {
-        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" :: "r"(mb) : "memory");
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" :: "r"(mb), "r"(2 * WIN) : "memory");
-        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
-                     :: "r"((uint32_t)__cvta_generic_to_shared(s_xr)), "l"(pr), "r"(WIN), "r"(mb) : "memory");
-        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
-                     :: "r"((uint32_t)__cvta_generic_to_shared(s_xi)), "l"(pi), "r"(WIN), "r"(mb) : "memory");
-      }
-      __syncthreads();  // barrier initialised before anyone polls it
-      uint32_t done = 0;
-      while (!done) {
-        asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0;\n\t"
-                     "selp.u32 %0, 1, 0, p;\n\t}" : "=r"(done) : "r"(mb) : "memory");
-      }
-    }
-  }
-  if constexpr (F64IN) {
-    // this CTA's own samples (second halves of its launched blocks): each sample of
-    // the launch is counted once
-    const int64_t own_lo = cta_blk0 * CDC_HOP;
-    const int64_t blk_end = A.blk_begin + A.blk_count;
-    const int64_t own_hi = (cta_blk0 + CDC_BLK < blk_end ? cta_blk0 + CDC_BLK : blk_end) * CDC_HOP;
-    uint32_t clips = stage_plane_f64(reinterpret_cast<int8_t*>(s_xr), reinterpret_cast<const double*>(xr_s),
-                                     g0, io, own_lo, own_hi);
-    clips += stage_plane_f64(reinterpret_cast<int8_t*>(s_xi), reinterpret_cast<const double*>(xi_s), g0,
-                             io, own_lo, own_hi);
-    if (io.in_clipped) {
-      clips = __reduce_add_sync(0xffffffffu, clips);
-      if ((threadIdx.x & 31) == 0 && clips) atomicAdd(io.in_clipped, (unsigned long long)clips);
-    }
-  } else if (!bulk) {
-    stage_plane<TIN, TS>(s_xr, xr_s, g0, io);
-    stage_plane<TIN, TS>(s_xi, xi_s, g0, io);
-  }
-  __syncthreads();
-
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
   const int sgn = warp & 1;                   // 0: a+ / b+, 1: a- / b-
@@ -601,6 +540,205 @@ __global__ void __launch_bounds__(CDC_CTA, CDC_MIN_CTAS) k_cdc64(const __grid_co
     return;
   }
   cdc_epilogue_generic(A, s_u, s, n0, lo, hi);
+}
+
+template <typename TIN, bool FAST>
+__global__ void __launch_bounds__(CDC_CTA, CDC_MIN_CTAS) k_cdc64(const __grid_constant__ CdcArgs A) {
+  constexpr bool F64IN = std::is_same<TIN, double>::value;  // quantized on load to int8
+  using TS = typename std::conditional<sizeof(TIN) == 1 || F64IN, int8_t, int32_t>::type;
+  // the input window and the u staging rows are never live at the same time
+  extern __shared__ __align__(16) unsigned char smem[];
+  TS* s_xr = reinterpret_cast<TS*>(smem);
+  TS* s_xi = s_xr + WIN;
+  uint32_t* s_u = reinterpret_cast<uint32_t*>(smem);  // [sign][block][UP]
+
+  const fntgpu_cdc_io& io = A.io;
+  const int s = A.s_base + (int)blockIdx.y;
+  const int64_t cta_blk0 = A.blk_begin + (int64_t)blockIdx.x * CDC_BLK;
+  const int64_t g0 = cta_blk0 * CDC_HOP - CDC_HOP;  // first input sample of block cta_blk0
+
+  const TIN* xr_s = reinterpret_cast<const TIN*>(io.xr) + (size_t)s * io.x_stride;
+  const TIN* xi_s = reinterpret_cast<const TIN*>(io.xi) + (size_t)s * io.x_stride;
+  bool bulk = false;
+  if (sizeof(TIN) == 1 && CDC_TMA) {
+    // interior windows of int8 planes: two 1-D bulk copies (TMA engine) straight into
+    // shared memory, completion counted on an mbarrier; edges and unaligned views
+    // take the vectorised load path
+    const int64_t lo = io.x_first > 0 ? io.x_first : 0;
+    const int64_t hi_avail = io.x_first + io.x_count;
+    const int64_t hi = hi_avail < io.length ? hi_avail : io.length;
+    const TIN* pr = xr_s + (g0 - io.x_first);
+    const TIN* pi = xi_s + (g0 - io.x_first);
+    bulk = g0 >= lo && g0 + WIN <= hi && ((reinterpret_cast<uintptr_t>(pr) | reinterpret_cast<uintptr_t>(pi)) & 15) == 0;
+    if (bulk) {
+      __shared__ __align__(8) uint64_t mbar;
+      const uint32_t mb = (uint32_t)__cvta_generic_to_shared(&mbar);
+      if (threadIdx.x == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" :: "r"(mb) : "memory");
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" :: "r"(mb), "r"(2 * WIN) : "memory");
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                     :: "r"((uint32_t)__cvta_generic_to_shared(s_xr)), "l"(pr), "r"(WIN), "r"(mb) : "memory");
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                     :: "r"((uint32_t)__cvta_generic_to_shared(s_xi)), "l"(pi), "r"(WIN), "r"(mb) : "memory");
+      }
+      __syncthreads();  // barrier initialised before anyone polls it
+      uint32_t done = 0;
+      while (!done) {
+        asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0;\n\t"
+                     "selp.u32 %0, 1, 0, p;\n\t}" : "=r"(done) : "r"(mb) : "memory");
+      }
+    }
+  }
+  if constexpr (F64IN) {
+    // this CTA's own samples (second halves of its launched blocks): each sample of
+    // the launch is counted once
+    const int64_t own_lo = cta_blk0 * CDC_HOP;
+    const int64_t blk_end = A.blk_begin + A.blk_count;
+    const int64_t own_hi = (cta_blk0 + CDC_BLK < blk_end ? cta_blk0 + CDC_BLK : blk_end) * CDC_HOP;
+    uint32_t clips = stage_plane_f64(reinterpret_cast<int8_t*>(s_xr), reinterpret_cast<const double*>(xr_s),
+                                     g0, io, own_lo, own_hi);
+    clips += stage_plane_f64(reinterpret_cast<int8_t*>(s_xi), reinterpret_cast<const double*>(xi_s), g0,
+                             io, own_lo, own_hi);
+    if (io.in_clipped) {
+      clips = __reduce_add_sync(0xffffffffu, clips);
+      if ((threadIdx.x & 31) == 0 && clips) atomicAdd(io.in_clipped, (unsigned long long)clips);
+    }
+  } else if (!bulk) {
+    stage_plane<TIN, TS>(s_xr, xr_s, g0, io);
+    stage_plane<TIN, TS>(s_xi, xi_s, g0, io);
+  }
+  __syncthreads();
+  cdc_item<TS, FAST>(A, s, cta_blk0, s_xr, s_xi, s_u);
+}
+
+// ---------------------------------------------------------------------------------
+// Float64 inputs quantized on load, persistent form (CDC_F64P). A CTA's float64 window
+// is 8x the int8 one (66 KB for both planes), so in the one-item-per-CTA kernel every
+// CTA spent a quarter of its life waiting for it. Here each CTA walks items
+// it, it + gridDim.x, ...: the next item's raw window arrives by two TMA bulk copies
+// into a shared-memory buffer while the current item's FNTs run, and is quantized from
+// shared memory (quant_in, the k_quant.cu / fixedpoint.py:51-60 float64 steps) into the
+// int8 window the shift-add path reads. Stream edges and unaligned views take the
+// synchronous global-load staging. Two CTAs per SM (raw buffer + window / u rows).
+#ifndef CDC_F64P
+#define CDC_F64P 1
+#endif
+constexpr int F64P_RAW = 2 * WIN * (int)sizeof(double);                 // raw planes
+constexpr int F64P_WORK = (2 * WIN > 2 * CDC_BLK * UP * 4) ? 2 * WIN : 2 * CDC_BLK * UP * 4;
+
+// quantize a landed raw window (samples g0 .. g0 + WIN of one plane, all inside the
+// stream) into int8, two samples per thread per step (conflict-free 16-byte reads);
+// returns the clips among this CTA's own samples [own_lo, own_hi)
+__device__ __forceinline__ uint32_t quant_window_smem(int8_t* dst, const double* raw, int64_t g0,
+                                                      const fntgpu_cdc_io& io, int64_t own_lo,
+                                                      int64_t own_hi) {
+  uint32_t clips = 0;
+  const int32_t mx = io.in_max;
+  for (int j = threadIdx.x; j < WIN / 2; j += blockDim.x) {
+    const double2 v = reinterpret_cast<const double2*>(raw)[j];
+    uint32_t c0, c1;
+    const int8_t q0 = quant_in(v.x, io.in_scale, mx, c0), q1 = quant_in(v.y, io.in_scale, mx, c1);
+    reinterpret_cast<uint16_t*>(dst)[j] = (uint16_t)((uint32_t)(uint8_t)q0 | ((uint32_t)(uint8_t)q1 << 8));
+    const int64_t g = g0 + 2 * j;
+    clips += (c0 & (g >= own_lo && g < own_hi)) + (c1 & (g + 1 >= own_lo && g + 1 < own_hi));
+  }
+  return clips;
+}
+
+template <bool FAST>
+__global__ void __launch_bounds__(CDC_CTA, 2) k_cdc64_f64p(const __grid_constant__ CdcArgs A) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  double* raw = reinterpret_cast<double*>(smem);  // [re | im][WIN]
+  unsigned char* work = smem + F64P_RAW;
+  int8_t* s_xr = reinterpret_cast<int8_t*>(work);
+  int8_t* s_xi = s_xr + WIN;
+  uint32_t* s_u = reinterpret_cast<uint32_t*>(work);
+  __shared__ __align__(8) uint64_t mbar;
+  const fntgpu_cdc_io& io = A.io;
+  const int tid = threadIdx.x;
+  const int64_t chunks = (A.blk_count + CDC_BLK - 1) / CDC_BLK;
+  const int64_t items = chunks * io.n_streams;
+  const int64_t lo = io.x_first > 0 ? io.x_first : 0;
+  const int64_t hi_avail = io.x_first + io.x_count;
+  const int64_t hi = hi_avail < io.length ? hi_avail : io.length;
+  const double* xr0 = reinterpret_cast<const double*>(io.xr);
+  const double* xi0 = reinterpret_cast<const double*>(io.xi);
+  const uint32_t mb = (uint32_t)__cvta_generic_to_shared(&mbar);
+  auto where = [&](int64_t it, int& s, int64_t& blk0) {
+    s = (int)(it / chunks);
+    blk0 = A.blk_begin + (it - (int64_t)s * chunks) * CDC_BLK;
+  };
+  auto src = [&](const double* base, int s, int64_t g0) {
+    return base + (size_t)s * io.x_stride + (g0 - io.x_first);
+  };
+  auto bulk_ok = [&](int64_t it) {
+    int s;
+    int64_t blk0;
+    where(it, s, blk0);
+    const int64_t g0 = blk0 * CDC_HOP - CDC_HOP;
+    return g0 >= lo && g0 + WIN <= hi &&
+           ((reinterpret_cast<uintptr_t>(src(xr0, s, g0)) | reinterpret_cast<uintptr_t>(src(xi0, s, g0))) & 15) == 0;
+  };
+  auto issue = [&](int64_t it) {  // thread 0
+    int s;
+    int64_t blk0;
+    where(it, s, blk0);
+    const int64_t g0 = blk0 * CDC_HOP - CDC_HOP;
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" :: "r"(mb), "r"(F64P_RAW) : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 :: "r"((uint32_t)__cvta_generic_to_shared(raw)), "l"(src(xr0, s, g0)), "r"(WIN * 8), "r"(mb)
+                 : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 :: "r"((uint32_t)__cvta_generic_to_shared(raw + WIN)), "l"(src(xi0, s, g0)), "r"(WIN * 8),
+                    "r"(mb)
+                 : "memory");
+  };
+  if (tid == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" :: "r"(mb) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  uint32_t phase = 0;
+  int64_t it = blockIdx.x;
+  if (tid == 0 && it < items && bulk_ok(it)) issue(it);
+  for (; it < items; it += gridDim.x) {
+    int s;
+    int64_t cta_blk0;
+    where(it, s, cta_blk0);
+    const int64_t g0 = cta_blk0 * CDC_HOP - CDC_HOP;
+    const int64_t own_lo = cta_blk0 * CDC_HOP;
+    const int64_t blk_end = A.blk_begin + A.blk_count;
+    const int64_t own_hi = (cta_blk0 + CDC_BLK < blk_end ? cta_blk0 + CDC_BLK : blk_end) * CDC_HOP;
+    uint32_t clips;
+    if (bulk_ok(it)) {
+      uint32_t done = 0;
+      while (!done) {
+        asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+                     "selp.u32 %0, 1, 0, p;\n\t}" : "=r"(done) : "r"(mb), "r"(phase) : "memory");
+      }
+      phase ^= 1u;
+      clips = quant_window_smem(s_xr, raw, g0, io, own_lo, own_hi);
+      clips += quant_window_smem(s_xi, raw + WIN, g0, io, own_lo, own_hi);
+    } else {
+      clips = stage_plane_f64(s_xr, src(xr0, s, io.x_first), g0, io, own_lo, own_hi);
+      clips += stage_plane_f64(s_xi, src(xi0, s, io.x_first), g0, io, own_lo, own_hi);
+    }
+    if (io.in_clipped) {
+      clips = __reduce_add_sync(0xffffffffu, clips);
+      if ((tid & 31) == 0 && clips) atomicAdd(io.in_clipped, (unsigned long long)clips);
+    }
+    __syncthreads();  // int8 window complete; every thread is done with the raw buffer
+    {
+      const int64_t nx = it + gridDim.x;
+      if (tid == 0 && nx < items && bulk_ok(nx)) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        issue(nx);  // lands while this item's transforms run
+      }
+    }
+    cdc_item<int8_t, FAST>(A, s, cta_blk0, s_xr, s_xi, s_u);
+    __syncthreads();  // the epilogue's reads of s_u are done before the next window
+  }
 }
 
 // ---------------------------------------------------------------------------------
@@ -1628,6 +1766,20 @@ static cudaError_t launch_tc(const CdcArgs& A, cudaStream_t st) {
 }
 
 template <bool FAST>
+static cudaError_t launch_f64p(const CdcArgs& A, cudaStream_t st) {
+  constexpr int SMEM = F64P_RAW + F64P_WORK;
+  static TcLaunchCfg cfgs[64];
+  int per_sm = 0, sms = 0;
+  const cudaError_t e = tc_launch_cfg(cfgs, k_cdc64_f64p<FAST>, SMEM, 2, per_sm, sms);
+  if (e != cudaSuccess) return e;
+  const int64_t items = (A.blk_count + CDC_BLK - 1) / CDC_BLK * A.io.n_streams;
+  const int64_t full = (int64_t)per_sm * sms;
+  const unsigned grid = (unsigned)(items < full ? items : full);
+  k_cdc64_f64p<FAST><<<grid, CDC_CTA, SMEM, st>>>(A);
+  return cudaGetLastError();
+}
+
+template <bool FAST>
 static cudaError_t launch_umma(const CdcArgs& A, cudaStream_t st) {
   constexpr int SMEM = (int)sizeof(UmmaSmem) + (FAST ? 0 : 2 * CDC_BLK * UP * 4);
   static TcLaunchCfg cfgs[64];
@@ -1691,6 +1843,10 @@ cudaError_t launch_cdc64(const fntgpu_cdc_taps& taps, const fntgpu_cdc_io& io, c
   if (io.in_dtype == FNTGPU_I8 && kern == FNTGPU_CDC_KERNEL_UMMA) {
     A.s_base = 0;
     return fast ? launch_umma<true>(A, st) : launch_umma<false>(A, st);
+  }
+  if (io.in_dtype == FNTGPU_F64 && CDC_F64P) {
+    A.s_base = 0;
+    return fast ? launch_f64p<true>(A, st) : launch_f64p<false>(A, st);
   }
   for (int64_t s0 = 0; s0 < io.n_streams; s0 += 65535) {
     A.s_base = (int32_t)s0;

@@ -942,3 +942,33 @@ def test_randomized_differential_vs_oracle():
     for _ in range(150):
         (fz.aeq_case if rng.random() < 0.7 else fz.cdc_case)(rng, stats)
     assert sum(stats.values()) == 150
+
+
+def test_cdc_float64_persistent_many_items():
+    """The persistent float64 CDC (several items per CTA, each next window prefetched
+    by TMA while the current one is transformed) over 3 streams x ~2^20 samples,
+    aligned and unaligned views (bulk and synchronous staging mixed), equals the
+    separate quantize_real + int8 CDC, clip count included."""
+    import torch
+    from paper_2405_04253_b200.stream import CdcBank
+    eng = _c2_engine()
+    bank = CdcBank(eng)
+    spec = eng.sig_spec
+    rng = np.random.default_rng(29)
+    L = (1 << 20) + 77
+    for off in (0, 1):
+        x = rng.normal(0.0, 1.6, (2, 3, L + 2))
+        xr = torch.from_numpy(x[0]).cuda()[:, off:off + L]
+        xi = torch.from_numpy(x[1]).cuda()[:, off:off + L]
+        yr = torch.empty((3, L), dtype=torch.int16, device="cuda")
+        yi = torch.empty_like(yr)
+        clip = torch.zeros(1, dtype=torch.int64, device="cuda")
+        bank.run(xr, xi, yr=yr, yi=yi, in_spec=spec, in_clipped=clip)
+        q = [np.stack([P.quantize_real(t[s].cpu().numpy(), spec)[0] for s in range(3)]) for t in (xr, xi)]
+        nclip = sum(P.quantize_real(t[s].cpu().numpy(), spec)[1] for t in (xr, xi) for s in range(3))
+        assert int(clip.item()) == nclip > 0
+        rr = torch.empty_like(yr)
+        ri = torch.empty_like(yr)
+        bank.run(torch.from_numpy(q[0].astype(np.int8)).cuda(), torch.from_numpy(q[1].astype(np.int8)).cuda(),
+                 yr=rr, yi=ri)
+        assert torch.equal(rr, yr) and torch.equal(ri, yi), off

@@ -1046,7 +1046,7 @@ def c4_f64_variant(args, bank, eng, xr, xi, sh, L, world, peaks) -> dict:
             "hbm_gbs": byts / (ms * 1e-3) / 1e9, "hbm_frac": byts / (ms * 1e-3) / 1e9 / peaks["hbm_gbs"],
             "int_tops": tops, "int_frac": tops / peaks["int_tops"],
             "equals_int8_path": same, "clip_count": int(clip.item()),
-            "kernel": "k_cdc64<double> (quantize-on-load staging, shift-add butterflies)"}
+            "kernel": "k_cdc64_f64p (persistent; raw float64 windows prefetched by TMA, quantized on load from shared memory; shift-add butterflies)"}
 
 
 def c4_window(x_first: int, x_count: int, sig_scale: float, seg: int = 1 << 22):

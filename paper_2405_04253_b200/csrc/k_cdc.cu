@@ -460,8 +460,11 @@ __device__ __forceinline__ int32_t sx8(uint32_t w, int k) {
 // One CTA item after its input window is staged in shared memory (s_xr, s_xi):
 // forward FNT-64 of this thread's block and sign, tap products, pruned inverse, then
 // the epilogue over the CTA's output range (s_u aliases the window).
-template <typename TS, bool FAST>
-__device__ __forceinline__ void cdc_item(const CdcArgs& A, int s, int64_t cta_blk0, const TS* s_xr,
+// `where(s, cta_blk0)` yields the item's stream and first block when the epilogue
+// needs them (recomputed from blockIdx, or re-read from shared memory by the persistent
+// kernels, so they are not held in registers across the transforms).
+template <typename TS, bool FAST, typename Where>
+__device__ __forceinline__ void cdc_item(const CdcArgs& A, Where where, const TS* s_xr,
                                          const TS* s_xi, uint32_t* s_u) {
   const fntgpu_cdc_io& io = A.io;
   const int tid = threadIdx.x;
@@ -530,6 +533,9 @@ __device__ __forceinline__ void cdc_item(const CdcArgs& A, int s, int64_t cta_bl
   __syncthreads();
 
   // ---- epilogue: outputs of this CTA are global indices [32*cta_blk0 - c, ... + 32*CDC_BLK)
+  int s;
+  int64_t cta_blk0;
+  where(s, cta_blk0);
   const int64_t n0 = cta_blk0 * CDC_HOP - A.c;
   int64_t lo = n0, hi = n0 + (int64_t)CDC_BLK * CDC_HOP;
   const int64_t o_lo = io.out_first, o_hi = io.out_first + io.out_count;
@@ -609,7 +615,10 @@ __global__ void __launch_bounds__(CDC_CTA, CDC_MIN_CTAS) k_cdc64(const __grid_co
     stage_plane<TIN, TS>(s_xi, xi_s, g0, io);
   }
   __syncthreads();
-  cdc_item<TS, FAST>(A, s, cta_blk0, s_xr, s_xi, s_u);
+  cdc_item<TS, FAST>(A, [&](int& s_, int64_t& b_) {
+    s_ = A.s_base + (int)blockIdx.y;
+    b_ = A.blk_begin + (int64_t)blockIdx.x * CDC_BLK;
+  }, s_xr, s_xi, s_u);
 }
 
 // ---------------------------------------------------------------------------------
@@ -655,6 +664,8 @@ __global__ void __launch_bounds__(CDC_CTA, 2) k_cdc64_f64p(const __grid_constant
   int8_t* s_xi = s_xr + WIN;
   uint32_t* s_u = reinterpret_cast<uint32_t*>(work);
   __shared__ __align__(8) uint64_t mbar;
+  __shared__ int64_t sh_blk0;
+  __shared__ int sh_s;
   const fntgpu_cdc_io& io = A.io;
   const int tid = threadIdx.x;
   const int64_t chunks = (A.blk_count + CDC_BLK - 1) / CDC_BLK;
@@ -736,7 +747,14 @@ __global__ void __launch_bounds__(CDC_CTA, 2) k_cdc64_f64p(const __grid_constant
         issue(nx);  // lands while this item's transforms run
       }
     }
-    cdc_item<int8_t, FAST>(A, s, cta_blk0, s_xr, s_xi, s_u);
+    if (tid == 0) {
+      sh_s = s;  // read back by the epilogue (ordered by cdc_item's barriers)
+      sh_blk0 = cta_blk0;
+    }
+    cdc_item<int8_t, FAST>(A, [&](int& s_, int64_t& b_) {
+      s_ = *(volatile int*)&sh_s;
+      b_ = *(volatile int64_t*)&sh_blk0;
+    }, s_xr, s_xi, s_u);
     __syncthreads();  // the epilogue's reads of s_u are done before the next window
   }
 }

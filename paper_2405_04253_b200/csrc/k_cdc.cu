@@ -633,7 +633,6 @@ __global__ void __launch_bounds__(CDC_CTA, CDC_MIN_CTAS) k_cdc64(const __grid_co
 #ifndef CDC_F64P
 #define CDC_F64P 1
 #endif
-constexpr int F64P_RAW = 2 * WIN * (int)sizeof(double);                 // raw planes
 constexpr int F64P_WORK = (2 * WIN > 2 * CDC_BLK * UP * 4) ? 2 * WIN : 2 * CDC_BLK * UP * 4;
 
 // quantize a landed raw window (samples g0 .. g0 + WIN of one plane, all inside the
@@ -655,65 +654,93 @@ __device__ __forceinline__ uint32_t quant_window_smem(int8_t* dst, const double*
   return clips;
 }
 
+#ifndef CDC_F64P_PLANES
+// raw float64 planes prefetched per item: 2 (both, 103 KB per CTA, 2 CTAs per SM) or
+// 1 (the real plane prefetched, the imaginary one loaded at the item's start into the
+// same buffer: 70 KB per CTA, 3 CTAs per SM and the int8 kernel's register budget).
+// Measured at 2^27 samples: 2 planes 116 Gsamples/s, 1 plane 107 (the exposed load of
+// the second plane costs more than the third CTA gains).
+#define CDC_F64P_PLANES 2
+#endif
+constexpr int F64P_RAWB = CDC_F64P_PLANES * WIN * (int)sizeof(double);
+
 template <bool FAST>
-__global__ void __launch_bounds__(CDC_CTA, 2) k_cdc64_f64p(const __grid_constant__ CdcArgs A) {
+__global__ void __launch_bounds__(CDC_CTA, CDC_F64P_PLANES == 2 ? 2 : CDC_MIN_CTAS)
+k_cdc64_f64p(const __grid_constant__ CdcArgs A) {
+  constexpr int NP = CDC_F64P_PLANES;
   extern __shared__ __align__(16) unsigned char smem[];
-  double* raw = reinterpret_cast<double*>(smem);  // [re | im][WIN]
-  unsigned char* work = smem + F64P_RAW;
+  double* raw = reinterpret_cast<double*>(smem);  // [NP][WIN]
+  unsigned char* work = smem + F64P_RAWB;
   int8_t* s_xr = reinterpret_cast<int8_t*>(work);
   int8_t* s_xi = s_xr + WIN;
   uint32_t* s_u = reinterpret_cast<uint32_t*>(work);
   __shared__ __align__(8) uint64_t mbar;
-  __shared__ int64_t sh_blk0;
+  // loop state in shared memory, launch constants recomputed per item: nothing extra
+  // stays live in registers across the transforms (the int8 kernel's 80 registers)
+  __shared__ int64_t sh_it, sh_blk0;
   __shared__ int sh_s;
-  const fntgpu_cdc_io& io = A.io;
+  __shared__ uint32_t sh_phase;
   const int tid = threadIdx.x;
-  const int64_t chunks = (A.blk_count + CDC_BLK - 1) / CDC_BLK;
-  const int64_t items = chunks * io.n_streams;
-  const int64_t lo = io.x_first > 0 ? io.x_first : 0;
-  const int64_t hi_avail = io.x_first + io.x_count;
-  const int64_t hi = hi_avail < io.length ? hi_avail : io.length;
-  const double* xr0 = reinterpret_cast<const double*>(io.xr);
-  const double* xi0 = reinterpret_cast<const double*>(io.xi);
-  const uint32_t mb = (uint32_t)__cvta_generic_to_shared(&mbar);
-  auto where = [&](int64_t it, int& s, int64_t& blk0) {
-    s = (int)(it / chunks);
-    blk0 = A.blk_begin + (it - (int64_t)s * chunks) * CDC_BLK;
-  };
-  auto src = [&](const double* base, int s, int64_t g0) {
-    return base + (size_t)s * io.x_stride + (g0 - io.x_first);
-  };
-  auto bulk_ok = [&](int64_t it) {
-    int s;
-    int64_t blk0;
-    where(it, s, blk0);
-    const int64_t g0 = blk0 * CDC_HOP - CDC_HOP;
-    return g0 >= lo && g0 + WIN <= hi &&
-           ((reinterpret_cast<uintptr_t>(src(xr0, s, g0)) | reinterpret_cast<uintptr_t>(src(xi0, s, g0))) & 15) == 0;
-  };
-  auto issue = [&](int64_t it) {  // thread 0
-    int s;
-    int64_t blk0;
-    where(it, s, blk0);
-    const int64_t g0 = blk0 * CDC_HOP - CDC_HOP;
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" :: "r"(mb), "r"(F64P_RAW) : "memory");
-    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
-                 :: "r"((uint32_t)__cvta_generic_to_shared(raw)), "l"(src(xr0, s, g0)), "r"(WIN * 8), "r"(mb)
-                 : "memory");
-    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
-                 :: "r"((uint32_t)__cvta_generic_to_shared(raw + WIN)), "l"(src(xi0, s, g0)), "r"(WIN * 8),
-                    "r"(mb)
-                 : "memory");
-  };
   if (tid == 0) {
+    const uint32_t mb = (uint32_t)__cvta_generic_to_shared(&mbar);
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" :: "r"(mb) : "memory");
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    sh_it = -1;
+    sh_phase = 0;
   }
   __syncthreads();
-  uint32_t phase = 0;
-  int64_t it = blockIdx.x;
-  if (tid == 0 && it < items && bulk_ok(it)) issue(it);
-  for (; it < items; it += gridDim.x) {
+  for (;;) {
+    const fntgpu_cdc_io& io = A.io;
+    const int64_t chunks = (A.blk_count + CDC_BLK - 1) / CDC_BLK;
+    const int64_t items = chunks * io.n_streams;
+    const int64_t lo = io.x_first > 0 ? io.x_first : 0;
+    const int64_t hi_avail = io.x_first + io.x_count;
+    const int64_t hi = hi_avail < io.length ? hi_avail : io.length;
+    const double* xr0 = reinterpret_cast<const double*>(io.xr);
+    const double* xi0 = reinterpret_cast<const double*>(io.xi);
+    const uint32_t mb = (uint32_t)__cvta_generic_to_shared(&mbar);
+    auto where = [&](int64_t it, int& s, int64_t& blk0) {
+      s = (int)(it / chunks);
+      blk0 = A.blk_begin + (it - (int64_t)s * chunks) * CDC_BLK;
+    };
+    auto src = [&](const double* base, int s, int64_t g0) {
+      return base + (size_t)s * io.x_stride + (g0 - io.x_first);
+    };
+    auto bulk_ok = [&](int64_t it) {
+      int s;
+      int64_t blk0;
+      where(it, s, blk0);
+      const int64_t g0 = blk0 * CDC_HOP - CDC_HOP;
+      return g0 >= lo && g0 + WIN <= hi &&
+             ((reinterpret_cast<uintptr_t>(src(xr0, s, g0)) | reinterpret_cast<uintptr_t>(src(xi0, s, g0))) & 15) == 0;
+    };
+    // thread 0: planes [p0, p0 + n) of item `it` into raw[0 .. n)
+    auto issue = [&](int64_t it, int p0, int n) {
+      int s;
+      int64_t blk0;
+      where(it, s, blk0);
+      const int64_t g0 = blk0 * CDC_HOP - CDC_HOP;
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" :: "r"(mb), "r"(n * WIN * 8) : "memory");
+      for (int q = 0; q < n; ++q)
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                     :: "r"((uint32_t)__cvta_generic_to_shared(raw + q * WIN)),
+                        "l"(src(p0 + q ? xi0 : xr0, s, g0)), "r"(WIN * 8), "r"(mb) : "memory");
+    };
+    auto wait = [&](uint32_t& phase) {
+      uint32_t done = 0;
+      while (!done) {
+        asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+                     "selp.u32 %0, 1, 0, p;\n\t}" : "=r"(done) : "r"(mb), "r"(phase) : "memory");
+      }
+      phase ^= 1u;
+    };
+    int64_t it = sh_it;
+    if (it < 0) {  // first pass
+      it = blockIdx.x;
+      if (tid == 0 && it < items && bulk_ok(it)) issue(it, 0, NP);
+    }
+    if (it >= items) break;
+    uint32_t phase = sh_phase;
     int s;
     int64_t cta_blk0;
     where(it, s, cta_blk0);
@@ -723,14 +750,19 @@ __global__ void __launch_bounds__(CDC_CTA, 2) k_cdc64_f64p(const __grid_constant
     const int64_t own_hi = (cta_blk0 + CDC_BLK < blk_end ? cta_blk0 + CDC_BLK : blk_end) * CDC_HOP;
     uint32_t clips;
     if (bulk_ok(it)) {
-      uint32_t done = 0;
-      while (!done) {
-        asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
-                     "selp.u32 %0, 1, 0, p;\n\t}" : "=r"(done) : "r"(mb), "r"(phase) : "memory");
-      }
-      phase ^= 1u;
+      wait(phase);
       clips = quant_window_smem(s_xr, raw, g0, io, own_lo, own_hi);
-      clips += quant_window_smem(s_xi, raw + WIN, g0, io, own_lo, own_hi);
+      if (NP == 2) {
+        clips += quant_window_smem(s_xi, raw + WIN, g0, io, own_lo, own_hi);
+      } else {
+        __syncthreads();  // the real plane is converted: its buffer takes the imaginary one
+        if (tid == 0) {
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          issue(it, 1, 1);
+        }
+        wait(phase);
+        clips += quant_window_smem(s_xi, raw, g0, io, own_lo, own_hi);
+      }
     } else {
       clips = stage_plane_f64(s_xr, src(xr0, s, io.x_first), g0, io, own_lo, own_hi);
       clips += stage_plane_f64(s_xi, src(xi0, s, io.x_first), g0, io, own_lo, own_hi);
@@ -739,17 +771,17 @@ __global__ void __launch_bounds__(CDC_CTA, 2) k_cdc64_f64p(const __grid_constant
       clips = __reduce_add_sync(0xffffffffu, clips);
       if ((tid & 31) == 0 && clips) atomicAdd(io.in_clipped, (unsigned long long)clips);
     }
-    __syncthreads();  // int8 window complete; every thread is done with the raw buffer
-    {
-      const int64_t nx = it + gridDim.x;
-      if (tid == 0 && nx < items && bulk_ok(nx)) {
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        issue(nx);  // lands while this item's transforms run
-      }
-    }
+    __syncthreads();  // int8 window complete; every thread is done with the raw buffer and the loop state
     if (tid == 0) {
       sh_s = s;  // read back by the epilogue (ordered by cdc_item's barriers)
       sh_blk0 = cta_blk0;
+      sh_it = it + gridDim.x;
+      sh_phase = phase;
+      const int64_t nx = it + gridDim.x;
+      if (nx < items && bulk_ok(nx)) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        issue(nx, 0, NP);  // lands while this item's transforms run
+      }
     }
     cdc_item<int8_t, FAST>(A, [&](int& s_, int64_t& b_) {
       s_ = *(volatile int*)&sh_s;
@@ -1785,10 +1817,11 @@ static cudaError_t launch_tc(const CdcArgs& A, cudaStream_t st) {
 
 template <bool FAST>
 static cudaError_t launch_f64p(const CdcArgs& A, cudaStream_t st) {
-  constexpr int SMEM = F64P_RAW + F64P_WORK;
+  constexpr int SMEM = F64P_RAWB + F64P_WORK;
   static TcLaunchCfg cfgs[64];
   int per_sm = 0, sms = 0;
-  const cudaError_t e = tc_launch_cfg(cfgs, k_cdc64_f64p<FAST>, SMEM, 2, per_sm, sms);
+  const cudaError_t e = tc_launch_cfg(cfgs, k_cdc64_f64p<FAST>, SMEM, CDC_F64P_PLANES == 2 ? 2 : CDC_MIN_CTAS,
+                                      per_sm, sms);
   if (e != cudaSuccess) return e;
   const int64_t items = (A.blk_count + CDC_BLK - 1) / CDC_BLK * A.io.n_streams;
   const int64_t full = (int64_t)per_sm * sms;

@@ -232,13 +232,17 @@ def ptr(t) -> vp:
 _NP2T = {}
 
 
-# Host <-> device copies of the drop-in calls' numpy arrays go through two pinned
-# staging chunks per host thread (DMA at the pinned rate, chunk k + 1's copy
-# overlapping chunk k's host memcpy). Pageable cudaMemcpy stages through the driver's
-# own buffers one transfer at a time, which serialized the copies of concurrent
-# threads (the drop-in chain moves ~40 MB per link).
+# Device -> host copies of the drop-in calls' larger results go through two pinned
+# staging chunks per host thread (DMA at the pinned rate, chunk k + 1's DMA
+# overlapping chunk k's host memcpy): measured on the B200 box, 5-6.6 GB/s vs 2-2.8
+# GB/s for pageable cudaMemcpy at 8-64 MB, whose driver staging also serialized the
+# copies of concurrent threads (the drop-in chain moves ~40 MB per link). Host ->
+# device copies stay pageable: there the driver's pipelined staging (13-17 GB/s)
+# beats a single-threaded memcpy into pinned memory (11-12 GB/s).
 _SMALL_COPY = 1 << 18
-_CHUNK = 16 << 20
+_STAGED_D2H = 4 << 20
+_STAGED_H2D = False
+_CHUNK = 4 << 20
 
 
 class _Stage(threading.local):
@@ -289,7 +293,7 @@ def to_device(a: np.ndarray):
         a = a.copy()
     if a.size == 0:
         return t.empty(a.shape, dtype=_torch_dtype(a.dtype), device=device())
-    if a.nbytes <= _SMALL_COPY or not _pinned_ok():
+    if a.nbytes <= _SMALL_COPY or not _STAGED_H2D or not _pinned_ok():
         return t.from_numpy(a).to(device(), non_blocking=False)
     d = t.empty(a.shape, dtype=_torch_dtype(a.dtype), device=device())
     src = a.reshape(-1).view(np.uint8)
@@ -322,7 +326,7 @@ def to_host(x) -> np.ndarray:
     """Device tensor -> a new numpy array (synchronous, like Tensor.cpu())."""
     t = torch()
     nbytes = x.numel() * x.element_size()
-    if nbytes <= _SMALL_COPY or not x.is_cuda or not _pinned_ok():
+    if nbytes < _STAGED_D2H or not x.is_cuda or not _pinned_ok():
         return x.cpu().numpy()
     x = x.contiguous()
     out = np.empty(tuple(x.shape), dtype=_numpy_dtype(x.dtype))

@@ -182,6 +182,14 @@ def test_pinned_staging_multi_chunk_copies():
     assert np.array_equal(yr, orr) and np.array_equal(yi, ori)
     inv = 1.0 / eng.output_scale
     assert np.array_equal(y, yr * inv + 1j * (yi * inv))
-    # the round trip of an odd-sized buffer through the staging chunks is the identity
+    # the round trip of an odd-sized buffer through the staging chunks is the identity,
+    # with the (optional) staged host-to-device path as well
     a = rng.integers(-(1 << 62), 1 << 62, (1 << 22) + 3)
     assert np.array_equal(_lib.to_host(_lib.to_device(a)), a)
+    prev = _lib._STAGED_H2D
+    _lib._STAGED_H2D = True
+    try:
+        assert np.array_equal(_lib.to_host(_lib.to_device(a)), a)
+        assert np.array_equal(P.fnt(p, x), O.fnt(O.Plan.named("cdc64"), x))
+    finally:
+        _lib._STAGED_H2D = prev

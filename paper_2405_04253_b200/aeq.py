@@ -131,6 +131,11 @@ def mu_block_array(n_blocks: int, hop: int, mu_schedule, default_mu: float) -> n
     """mu of each block: mu_schedule(b * hop), or config.mu (aeq.py:187-188)."""
     if mu_schedule is None:
         return np.full(n_blocks, default_mu, dtype=np.float64)
+    fast = getattr(mu_schedule, "block_mu", None)  # linksim.GearSchedule: vectorized
+    if fast is not None:
+        table = fast(n_blocks, hop)
+        if table is not None:
+            return table
     out = np.empty(n_blocks, dtype=np.float64)
     for b in range(n_blocks):
         m = mu_schedule(b * hop)
@@ -333,8 +338,13 @@ def td_aeq_float(x: np.ndarray, config: AeqConfig, mu_schedule=None,
             w[s, s, L // 2] = 1.0
     else:
         w = np.ascontiguousarray(np.asarray(w0, dtype=np.float64)).copy()
-    mu_arr = (np.full(n, config.mu) if mu_schedule is None
-              else np.array([mu_schedule(i) for i in range(n)], dtype=np.float64))
+    mu_arr = None
+    if mu_schedule is None:
+        mu_arr = np.full(n, config.mu)
+    elif getattr(mu_schedule, "block_mu", None) is not None:
+        mu_arr = mu_schedule.block_mu(n, 1)  # per symbol index
+    if mu_arr is None:
+        mu_arr = np.array([mu_schedule(i) for i in range(n)], dtype=np.float64)
     radii = np.asarray(config.radii, dtype=float)
     if not 1 <= radii.size <= 8:
         raise NotImplementedError("the GPU equalizer supports 1..8 ring radii")

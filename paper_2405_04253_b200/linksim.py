@@ -79,7 +79,34 @@ class LinkConfig:
                          sig_spec=self.sig_spec())
 
     def mu_schedule(self):
-        return lambda i: self.mu1 if i < self.gear_symbols else self.mu2
+        return GearSchedule(self)
+
+
+class GearSchedule:
+    """LinkConfig.mu_schedule (linksim.py:82-83): mu1 before gear_symbols, mu2 after.
+    Called per symbol index like the reference's lambda (reading the config's current
+    fields, as the lambda's closure does); FntAeq additionally takes the whole
+    per-block table from block_mu instead of one Python call per block."""
+
+    __slots__ = ("cfg",)
+
+    def __init__(self, cfg):
+        self.cfg = cfg
+
+    def __call__(self, i):
+        c = self.cfg
+        return c.mu1 if i < c.gear_symbols else c.mu2
+
+    def block_mu(self, n_blocks: int, hop: int):
+        """mu of blocks 0 .. n_blocks-1 (symbol index b * hop), or None when a field
+        is not a plain number (the caller then calls the schedule per block)."""
+        c = self.cfg
+        try:
+            mu1, mu2, gear = float(c.mu1), float(c.mu2), c.gear_symbols
+            i = np.arange(n_blocks, dtype=np.int64) * hop
+            return np.where(i < gear, mu1, mu2).astype(np.float64)
+        except (TypeError, ValueError):
+            return None
 
 
 @dataclass

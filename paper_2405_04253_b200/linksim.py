@@ -62,8 +62,7 @@ class LinkConfig:
     @property
     def sig_scale(self) -> float:
         """Quantizer scale putting the outer 16QAM modulus at load_fraction."""
-        max_int = (1 << (self.sig_bits - 1)) - 1
-        return self.load_fraction * max_int / _OUTER_MODULUS
+        return self.load_fraction * (2 ** (self.sig_bits - 1) - 1) / _OUTER_MODULUS
 
     def sig_spec(self) -> QuantSpec:
         return QuantSpec(self.sig_bits, self.sig_scale)
@@ -129,29 +128,31 @@ class Metrics:
 
 
 def fec_crossing_snr(snrs, bers, threshold: float = HD_FEC_BER) -> float:
-    """SNR where a BER curve crosses the FEC threshold, log-interpolated (linksim.py:439-454)."""
-    snrs = np.asarray(snrs, dtype=float)
-    bers = np.asarray(bers, dtype=float)
-    order = np.argsort(snrs)
-    snrs, bers = snrs[order], bers[order]
+    """SNR at which a BER curve falls through the FEC threshold: the first adjacent
+    pair (in SNR order) bracketing it, interpolated linearly in log10(BER)
+    (linksim.py:439-454)."""
+    order = np.argsort(np.asarray(snrs, dtype=float))
+    x = np.asarray(snrs, dtype=float)[order]
+    y = np.asarray(bers, dtype=float)[order]
     logt = math.log10(threshold)
-    for i in range(len(snrs) - 1):
-        b0, b1 = bers[i], bers[i + 1]
-        if b0 >= threshold >= b1 and b1 > 0:
-            l0, l1 = math.log10(b0), math.log10(b1)
-            if l0 == l1:
-                return float(snrs[i])
-            frac = (l0 - logt) / (l0 - l1)
-            return float(snrs[i] + frac * (snrs[i + 1] - snrs[i]))
+    for (x0, x1), (y0, y1) in zip(zip(x[:-1], x[1:]), zip(y[:-1], y[1:])):
+        if not (y0 >= threshold >= y1 and y1 > 0):
+            continue
+        l0, l1 = math.log10(y0), math.log10(y1)
+        if l0 == l1:
+            return float(x0)
+        frac = (l0 - logt) / (l0 - l1)
+        return float(x0 + frac * (x1 - x0))
     raise ValueError("BER curve does not cross the FEC threshold")
 
 
 def penalty_at_fec(rows: list[Metrics], scheme_a: str, scheme_b: str,
                    threshold: float = HD_FEC_BER) -> float:
-    def crossing(scheme):
-        pts = [(m.snr_db, m.ber) for m in rows if m.scheme == scheme]
-        return fec_crossing_snr([p[0] for p in pts], [p[1] for p in pts], threshold)
-    return crossing(scheme_a) - crossing(scheme_b)
+    """FEC-threshold SNR of scheme_a minus that of scheme_b (linksim.py:457-466)."""
+    def at_fec(name):
+        curve = [(m.snr_db, m.ber) for m in rows if m.scheme == name]
+        return fec_crossing_snr([c[0] for c in curve], [c[1] for c in curve], threshold)
+    return at_fec(scheme_a) - at_fec(scheme_b)
 
 
 # ---------------------------------------------------------------- link simulator
@@ -275,10 +276,12 @@ def rx_frontend(rx: np.ndarray, cfg: LinkConfig, scheme: str) -> tuple[np.ndarra
 
 
 def _q_factor_db(ber: float) -> float:
-    from scipy.special import erfcinv
+    """Q factor in dB from the BER of Gray-coded QAM: 20 log10(sqrt(2) erfcinv(2 BER))."""
     if ber <= 0:
         return math.inf
-    return 20.0 * math.log10(math.sqrt(2.0) * float(erfcinv(2.0 * ber)))
+    from scipy.special import erfcinv
+    q = math.sqrt(2.0) * float(erfcinv(2.0 * ber))
+    return 20.0 * math.log10(q)
 
 
 def run_single(cfg: LinkConfig, scheme: str, snr_db: float) -> Metrics:

@@ -79,3 +79,38 @@ def test_host_helpers_equal_reference():
         assert err(PF.for_modulus, F) == err(RF.for_modulus, F)
     assert err(PF.encode_signed, 40000, PF.FermatParams(4)) == err(RF.encode_signed, 40000, RF.FermatParams(4))
 
+
+
+def test_linksim_helpers_equal_reference():
+    sys.path.insert(0, str(REF))
+    try:
+        import fntdsp.linksim as R
+    finally:
+        sys.path.remove(str(REF))
+    import paper_2405_04253_b200.linksim as L
+    rng = np.random.default_rng(1)
+    for _ in range(1500):
+        n = rng.integers(2, 8)
+        snrs = rng.uniform(10, 25, n)
+        bers = 10 ** rng.uniform(-6, -1, n)
+        if rng.random() < 0.2:
+            bers[rng.integers(0, n)] = 0.0
+        if rng.random() < 0.1:
+            bers[:] = 3.8e-3
+        assert err(L.fec_crossing_snr, snrs, bers) == err(R.fec_crossing_snr, snrs, bers)
+        try:
+            assert L.fec_crossing_snr(snrs, bers) == R.fec_crossing_snr(snrs, bers)
+        except ValueError:
+            pass
+    for ber in (0.0, -1.0, 1e-9, 1e-3, 0.2, 0.49, 0.5):
+        assert err(L._q_factor_db, ber) == err(R._q_factor_db, ber)
+        if 0 < ber < 0.5:
+            assert L._q_factor_db(ber) == R._q_factor_db(ber)
+    for bits in (3, 5, 8):
+        for lf in (0.5, 0.8, 1.0):
+            assert (L.LinkConfig(sig_bits=bits, load_fraction=lf).sig_scale
+                    == R.LinkConfig(sig_bits=bits, load_fraction=lf).sig_scale)
+    pts = list(zip((14, 16, 18, 20), (1e-2, 5e-3, 2e-3, 1e-4)))
+    rows = [L.Metrics(s, x, y, 0, 0, 0, 0, 0, True) for s in ("fnt", "float") for x, y in pts]
+    rrows = [R.Metrics(s, x, y, 0, 0, 0, 0, 0, True) for s in ("fnt", "float") for x, y in pts]
+    assert L.penalty_at_fec(rows, "fnt", "float") == R.penalty_at_fec(rrows, "fnt", "float")

@@ -23,12 +23,14 @@ from .complexity import COUNTER
 from .fixedpoint import QuantSpec, check_overflow, split_taps
 from .fnt import TransformPlan, default_plans
 
+#: output / input stream order of the 4x4 real MIMO: X and Y polarizations, I and Q
 STREAMS = ("XI", "XQ", "YI", "YQ")
-TAP_MAG_MAX = (1 << 14) - 1
+TAP_MAG_MAX = 2 ** 14 - 1  # largest 14-bit tap magnitude
 
 
 def qam16_radii() -> np.ndarray:
-    """Ring moduli of unit-energy 16QAM (aeq.py:29-31)."""
+    """The three ring radii of 16QAM scaled to unit mean energy (levels +-1, +-3:
+    |s|^2 in {2, 10, 18} / 10) (aeq.py:29-31)."""
     return np.sqrt(np.array([2.0, 10.0, 18.0]) / 10.0)
 
 
@@ -52,16 +54,18 @@ class AeqConfig:
 
 
 def rde_error(y_i: np.ndarray, y_q: np.ndarray, radii: np.ndarray) -> np.ndarray:
-    """R^2 - |y|^2 against the nearest ring (aeq.py:53-58); host helper."""
-    r2 = np.asarray(y_i) ** 2 + np.asarray(y_q) ** 2
-    r = np.sqrt(r2)
-    nearest = radii[np.argmin(np.abs(r[..., None] - radii), axis=-1)]
-    return nearest ** 2 - r2
+    """Radius-directed error R^2 - |y|^2, R the ring nearest to |y| (the first one on a
+    tie), shared by the I and Q outputs of a polarization (aeq.py:53-58). Host helper;
+    the kernels decide the ring without the square root (aeq_common.cuh rde)."""
+    power = np.asarray(y_i) ** 2 + np.asarray(y_q) ** 2
+    dist = np.abs(np.sqrt(power)[..., None] - radii)
+    return radii[dist.argmin(axis=-1)] ** 2 - power
 
 
 @dataclass
 class RvMimoTaps:
-    """16 real FIR filters (output stream, input stream, lag) (aeq.py:61-81)."""
+    """The 16 real FIR filters as 14-bit integers w_int[s_out, s_in, lag], with their
+    7-bit sign-magnitude groups (aeq.py:61-81)."""
 
     w_int: np.ndarray
     high: np.ndarray = field(init=False)
@@ -71,14 +75,15 @@ class RvMimoTaps:
         self.resplit()
 
     def resplit(self) -> None:
-        s = split_taps(self.w_int)
-        self.high, self.low = s.high, s.low
+        groups = split_taps(self.w_int)
+        self.high = groups.high
+        self.low = groups.low
 
     @classmethod
     def center_spike(cls, l_taps: int, spike: int) -> "RvMimoTaps":
+        """Identity MIMO: `spike` at the centre lag of the four direct filters."""
         w = np.zeros((4, 4, l_taps), dtype=np.int64)
-        for s in range(4):
-            w[s, s, l_taps // 2] = spike
+        w[np.arange(4), np.arange(4), l_taps // 2] = spike
         return cls(w)
 
 

@@ -13,6 +13,7 @@ from __future__ import annotations
 
 import ctypes as C
 import math
+from pathlib import Path
 import os
 from dataclasses import dataclass, field
 
@@ -50,38 +51,38 @@ class CdcConfig:
 
     @property
     def accumulated_dispersion(self) -> float:
-        """D lambda^2 z / c in s^2 (cdc.py:47-52)."""
-        d_si = self.dispersion_ps_nm_km * 1e-6
-        lam = self.wavelength_nm * 1e-9
-        return d_si * lam * lam * (self.z_km * 1e3) / SPEED_OF_LIGHT
+        """beta = D lambda^2 L / c in s^2, with D in s/m^2, lambda and L in m
+        (cdc.py:47-52; the float64 products in the reference's order)."""
+        wl_m = self.wavelength_nm * 1e-9
+        return self.dispersion_ps_nm_km * 1e-6 * wl_m * wl_m * (self.z_km * 1e3) / SPEED_OF_LIGHT
 
 
 def required_taps(cfg: CdcConfig) -> int:
-    """Full-band tap estimate 2*floor(D lambda^2 z fs^2 / c / 2) + 1 (cdc.py:55-58)."""
-    n = cfg.accumulated_dispersion * cfg.fs_hz ** 2
-    return 2 * int(n / 2) + 1
+    """Odd tap count spanning the dispersive spread, 2 floor(beta fs^2 / 2) + 1
+    (cdc.py:55-58)."""
+    return 1 + 2 * int(cfg.accumulated_dispersion * cfg.fs_hz ** 2 / 2)
 
 
 def design_cd_taps(cfg: CdcConfig) -> np.ndarray:
-    """Energy-normalised inverse-dispersion chirp centred on n_taps // 2 (cdc.py:61-77)."""
-    h = np.zeros(cfg.n_taps, dtype=complex)
-    centre = cfg.n_taps // 2
+    """Unit-energy inverse all-pass chirp exp(-j pi t^2 / beta) sampled at t = (n - c) / fs,
+    c = n_taps // 2 (cdc.py:61-77); a unit impulse at c for z = 0."""
+    c = cfg.n_taps // 2
     if cfg.z_km == 0:
-        h[centre] = 1.0
-        return h
-    acc = cfg.accumulated_dispersion
-    t = (np.arange(cfg.n_taps) - centre) / cfg.fs_hz
-    h = np.exp(-1j * math.pi * t * t / acc)
-    return h / np.linalg.norm(h)
+        return np.eye(1, cfg.n_taps, c, dtype=complex)[0]
+    beta = cfg.accumulated_dispersion
+    t = (np.arange(cfg.n_taps) - c) / cfg.fs_hz
+    chirp = np.exp(-1j * math.pi * t * t / beta)
+    return chirp / np.linalg.norm(chirp)
 
 
 def quantize_taps(taps: np.ndarray, bits: int) -> tuple[np.ndarray, np.ndarray, float]:
-    """Power-of-two tap scale filling the bits-wide grid (cdc.py:80-86)."""
-    max_int = (1 << (bits - 1)) - 1
+    """6-bit (say) taps on the largest power-of-two scale that keeps the biggest
+    component within 2^(bits-1) - 1 (cdc.py:80-86): (re, im, scale)."""
+    top = 2 ** (bits - 1) - 1
     peak = max(np.abs(taps.real).max(), np.abs(taps.imag).max())
-    scale = 2.0 ** math.floor(math.log2(max_int / peak))
-    blk = quantize(taps, QuantSpec(bits, scale))
-    return blk.re, blk.im, scale
+    scale = 2.0 ** math.floor(math.log2(top / peak))
+    q = quantize(taps, QuantSpec(bits, scale))
+    return q.re, q.im, scale
 
 
 def overlap_save_block_count(length: int, block_n: int = 64) -> int:
@@ -337,26 +338,23 @@ def td_cdc_float(x: np.ndarray, cfg: CdcConfig, taps: np.ndarray | None = None) 
 
 
 def save_taps(path, tap_re: np.ndarray, tap_im: np.ndarray, scale: float) -> None:
-    """Plain-text taps with a '# scale' header (cdc.py:213-217)."""
-    with open(path, "w") as f:
-        f.write(f"# scale {scale!r}\n")
-        for r, i in zip(tap_re, tap_im):
-            f.write(f"{int(r)} {int(i)}\n")
+    """Integer taps as "re im" lines under a "# scale <repr>" header (cdc.py:213-217)."""
+    lines = [f"# scale {scale!r}"] + [f"{int(a)} {int(b)}" for a, b in zip(tap_re, tap_im)]
+    Path(path).write_text("".join(line + "\n" for line in lines))
 
 
 def load_taps(path) -> tuple[np.ndarray, np.ndarray, float]:
-    scale = 1.0
-    re, im = [], []
-    with open(path) as f:
-        for line in f:
-            line = line.strip()
-            if line.startswith("# scale"):
-                scale = float(line.split()[-1])
-            elif line:
-                a, b = line.split()
-                re.append(int(a))
-                im.append(int(b))
-    return np.array(re, dtype=np.int64), np.array(im, dtype=np.int64), scale
+    """Inverse of save_taps (cdc.py:220-233): (re, im, scale), scale 1.0 without a header."""
+    scale, pairs = 1.0, []
+    for raw in Path(path).read_text().splitlines():
+        text = raw.strip()
+        if text.startswith("# scale"):
+            scale = float(text.split()[-1])
+        elif text:
+            a, b = text.split()
+            pairs.append((int(a), int(b)))
+    cols = np.array(pairs, dtype=np.int64).reshape(-1, 2)
+    return cols[:, 0].copy(), cols[:, 1].copy(), scale
 
 
 __all__ = ["BudgetError", "CdcConfig", "FntCdcEngine", "design_cd_taps", "fd_cdc_float",

@@ -114,3 +114,45 @@ def test_linksim_helpers_equal_reference():
     rows = [L.Metrics(s, x, y, 0, 0, 0, 0, 0, True) for s in ("fnt", "float") for x, y in pts]
     rrows = [R.Metrics(s, x, y, 0, 0, 0, 0, 0, True) for s in ("fnt", "float") for x, y in pts]
     assert L.penalty_at_fec(rows, "fnt", "float") == R.penalty_at_fec(rrows, "fnt", "float")
+
+
+def test_cdc_aeq_host_helpers_equal_reference(tmp_path, monkeypatch):
+    """Tap design, quantization scale, tap files, the RDE error and the MIMO tap
+    object, bit for bit (quantize runs on the GPU in the product; the reference's numpy
+    quantizer stands in for it here, its own parity is a GPU test)."""
+    sys.path.insert(0, str(REF))
+    try:
+        import fntdsp.aeq as RA
+        import fntdsp.cdc as RC
+        import fntdsp.fixedpoint as RF
+    finally:
+        sys.path.remove(str(REF))
+    import paper_2405_04253_b200.aeq as A
+    import paper_2405_04253_b200.cdc as C
+    monkeypatch.setattr(C, "quantize", lambda taps, spec: RF.quantize(taps, RF.QuantSpec(spec.bit_width, spec.scale)))
+    for z in (0.0, 25.0, 75.0, 1000.0):
+        for nt in (1, 5, 32, 33):
+            for fs in (80e9, 64e9):
+                a = C.CdcConfig(z_km=z, fs_hz=fs, n_taps=nt)
+                b = RC.CdcConfig(z_km=z, fs_hz=fs, n_taps=nt)
+                assert a.accumulated_dispersion == b.accumulated_dispersion
+                assert C.required_taps(a) == RC.required_taps(b)
+                ta, tb = C.design_cd_taps(a), RC.design_cd_taps(b)
+                assert ta.dtype == tb.dtype and np.array_equal(ta.view(np.float64), tb.view(np.float64))
+                if z:
+                    qa, qb = C.quantize_taps(ta, 6), RC.quantize_taps(tb, 6)
+                    assert all(np.array_equal(x, y) for x, y in zip(qa[:2], qb[:2])) and qa[2] == qb[2]
+                    C.save_taps(tmp_path / "a", *qa)
+                    RC.save_taps(tmp_path / "b", *qb)
+                    assert (tmp_path / "a").read_text() == (tmp_path / "b").read_text()
+                    la, lb = C.load_taps(tmp_path / "a"), RC.load_taps(tmp_path / "b")
+                    assert all(np.array_equal(x, y) for x, y in zip(la[:2], lb[:2])) and la[2] == lb[2]
+    rng = np.random.default_rng(3)
+    radii = RA.qam16_radii()
+    assert np.array_equal(A.qam16_radii(), radii)
+    for _ in range(50):
+        yi, yq = rng.normal(0, 1, (2, 4, 16))
+        assert np.array_equal(A.rde_error(yi, yq, radii), RA.rde_error(yi, yq, radii))
+    for l_taps, spike in ((16, 8192), (8, 100)):
+        a, b = A.RvMimoTaps.center_spike(l_taps, spike), RA.RvMimoTaps.center_spike(l_taps, spike)
+        assert all(np.array_equal(getattr(a, k), getattr(b, k)) for k in ("w_int", "high", "low"))

@@ -33,6 +33,7 @@ def test_bench_single_gpu_line():
     assert d["roofline"]["frac"] > 0 and d["e2e"]["h2d_bytes_per_step"] > 0
     assert d["gpu_launches"] == 4 and d["parity"]["all_equal"]
     assert d["e2e"]["dropin_api"]["value"] > 0
+    assert d["link_quality"]["links"] == 128
 
 
 @pytest.mark.slow
@@ -48,4 +49,5 @@ def test_bench_torchrun_two_ranks():
     # the 64 links are split 32 + 32 (strong scaling); rank 0 checked its links vs the oracle
     assert d["n_gpus"] == 2 and d["scaling"] == "strong"
     assert d["config"]["links_per_gpu"] == 32 and d["config"]["links_total"] == 64
+    assert d["link_quality"]["links"] == 64  # both ranks' links, reduced over the group
     assert d["parity"]["all_equal"]

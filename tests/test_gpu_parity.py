@@ -940,7 +940,8 @@ def test_randomized_differential_vs_oracle():
     rng = np.random.default_rng(2405)
     stats = {}
     for _ in range(150):
-        (fz.aeq_case if rng.random() < 0.7 else fz.cdc_case)(rng, stats)
+        u = rng.random()
+        (fz.aeq_case if u < 0.6 else fz.cdc_case if u < 0.8 else fz.cdc_bank_case)(rng, stats)
     assert sum(stats.values()) == 150
 
 

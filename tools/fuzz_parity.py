@@ -4,8 +4,9 @@ the GPU box): FntAeq with random initial taps (float and 14-bit, set independent
 as the reference allows), random inputs (5-bit, full int8, wide int32 up to the
 encodable +-32768), random step sizes (0, tiny, large enough to saturate), random
 lengths, through both stream layouts and both forward forms; FntCdcEngine with random
-6-bit taps and random stream lengths / input widths. Every case must be bit-exact
-(y, w, w_int, saturations, err_trace; CDC outputs).
+6-bit taps and random stream lengths / input widths; the multi-stream CdcBank on random
+output ranges and input windows (int8 / int32 / float64 quantized on load). Every case
+must be bit-exact (y, w, w_int, saturations, err_trace; CDC outputs).
 
     python tools/fuzz_parity.py [--seconds 240] [--seed 1]
 """
@@ -124,6 +125,55 @@ def cdc_case(rng, stats):
         raise AssertionError(f"CDC mismatch: n_taps={n_taps} L={L} wide={wide}")
 
 
+def cdc_bank_case(rng, stats):
+    """CdcBank.run (the device-resident multi-stream path) on random output ranges of
+    random-length streams, fed a window with the overlap-save halo, int8 / int32 /
+    float64 inputs (float64 quantized on load, persistent kernel) and int16 / int32
+    outputs, against the oracle's direct FIR of the quantized samples."""
+    import torch
+    from paper_2405_04253_b200.stream import CdcBank
+    cfg = P.LinkConfig(z_km=75.0)
+    eng = P.FntCdcEngine(cfg.cdc_config("fnt"), cfg.sig_spec())
+    bank = CdcBank(eng)
+    S = int(rng.integers(1, 4))
+    L = int(rng.choice([1, 33, 4096, 4097, 70001, 300007]))
+    a = int(rng.integers(0, L))
+    b = int(rng.integers(a + 1, L + 1))
+    c = eng.config.n_taps // 2
+    x_lo = max(0, (a + c) // 32 * 32 - 32 - int(rng.integers(0, 3)))
+    x_hi = min(L, ((b - 1 + c) // 32) * 32 + 32 + int(rng.integers(0, 3)))
+    kind = rng.choice(["i8", "i32", "f64"])
+    q = rng.integers(-15, 16, (2, S, L))
+    if kind == "f64":
+        spec = eng.sig_spec
+        xf = (q + (rng.random((2, S, L)) - 0.5) * 0.9) / spec.scale
+        xf[rng.random((2, S, L)) < 0.001] = 9.0  # clipped samples
+        qq = np.stack([[O.quantize_real(xf[p, s], spec.scale, spec.max_int)[0] for s in range(S)]
+                       for p in range(2)])
+        xr = torch.from_numpy(np.ascontiguousarray(xf[0][:, x_lo:x_hi])).cuda()
+        xi = torch.from_numpy(np.ascontiguousarray(xf[1][:, x_lo:x_hi])).cuda()
+        extra = dict(in_spec=spec, in_clipped=torch.zeros(1, dtype=torch.int64, device="cuda"))
+    else:
+        qq = q
+        dt = torch.int8 if kind == "i8" else torch.int32
+        xr = torch.from_numpy(np.ascontiguousarray(q[0][:, x_lo:x_hi])).to("cuda", dt)
+        xi = torch.from_numpy(np.ascontiguousarray(q[1][:, x_lo:x_hi])).to("cuda", dt)
+        extra = {}
+    odt = torch.int16 if rng.random() < 0.5 else torch.int32
+    yr = torch.empty((S, b - a), dtype=odt, device="cuda")
+    yi = torch.empty_like(yr)
+    bank.run(xr, xi, length=L, x_first=x_lo, out_first=a, out_count=b - a, yr=yr, yi=yi, **extra)
+    torch.cuda.synchronize()
+    for s in range(S):
+        orr, ori = O.cdc_direct(eng.tap_re, eng.tap_im, qq[0, s], qq[1, s])
+        if not (np.array_equal(yr[s].cpu().numpy().astype(np.int64), orr[a:b])
+                and np.array_equal(yi[s].cpu().numpy().astype(np.int64), ori[a:b])):
+            raise AssertionError(f"CdcBank mismatch: kind={kind} S={S} L={L} range=[{a},{b}) "
+                                 f"window=[{x_lo},{x_hi})")
+    key = f"cdcbank/{kind}"
+    stats[key] = stats.get(key, 0) + 1
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--seconds", type=float, default=240.0)
@@ -134,7 +184,8 @@ def main():
     t0 = time.time()
     n = 0
     while time.time() - t0 < a.seconds:
-        (aeq_case if rng.random() < 0.7 else cdc_case)(rng, stats)
+        u = rng.random()
+        (aeq_case if u < 0.6 else cdc_case if u < 0.8 else cdc_bank_case)(rng, stats)
         n += 1
     print(f"{n} cases, all bit-exact")
     for k in sorted(stats):

@@ -69,6 +69,9 @@ class DeviceLinkGenerator:
         self.max_int = (1 << (sig_bits - 1)) - 1
         L = self.L
         taps = rrc_taps(sps, span, rolloff)
+        if taps.size > L:
+            raise ValueError(f"n_symbols * sps = {L} is shorter than the {taps.size}-tap RRC "
+                             f"pulse (circular shaping needs at least span * sps + 1 samples)")
         th = np.zeros(L, dtype=complex)
         th[:taps.size] = taps
         th = np.roll(th, -(taps.size // 2))

@@ -174,6 +174,43 @@ def cdc_bank_case(rng, stats):
     stats[key] = stats.get(key, 0) + 1
 
 
+def chain_case(rng, stats):
+    """The whole device-resident receiver chain (CdcAeqChain: CDC with the fused
+    requantization and decimation statistics, phase decision with the tie guard,
+    FNT-AEQ over both layouts) on random links of the device link model with random
+    lengths and gear-shift points, against the oracle's chain per link."""
+    import torch
+    from paper_2405_04253_b200.linkgen import DeviceLinkGenerator
+    from paper_2405_04253_b200.stream import CdcAeqChain
+    n_links = int(rng.integers(1, 6))
+    n_sym = int(rng.choice([80, 300, 1024, 4096]))
+    cfg = P.LinkConfig(n_symbols=n_sym, z_km=75.0, seed=4)
+    cfg.gear_symbols = int(rng.integers(0, 2 * n_sym))
+    eng = P.FntCdcEngine(cfg.cdc_config("fnt"), cfg.sig_spec())
+    xr, xi = DeviceLinkGenerator(n_sym).generate(n_links, seed=int(rng.integers(1, 1 << 30)))
+    L = 2 * n_sym  # the chain takes 2-sps streams of even length
+    kind = rng.choice(["warp", "pol"])
+    prev = A.set_aeq_kernel(kind)
+    try:
+        ch = CdcAeqChain(eng, cfg.aeq_config(), n_links, L, cfg.sig_spec(), cfg.mu_schedule())
+    finally:
+        A.set_aeq_kernel(prev)
+    ch.run(xr, xi)
+    torch.cuda.synchronize()
+    for l in range(n_links):
+        fe = [(xr[2 * l + p].cpu().numpy().astype(np.int64), xi[2 * l + p].cpu().numpy().astype(np.int64))
+              for p in range(2)]
+        ph, y, oq = O.chain_link(eng.tap_re, eng.tap_im, eng.output_scale, cfg.sig_scale, fe,
+                                 cfg.mu1, cfg.mu2, cfg.gear_symbols)
+        nb = y.shape[1] // 16
+        ok = (int(ch.phase[l].item()) == ph and np.array_equal(ch.y[l].cpu().numpy()[:, :16 * nb], y)
+              and np.array_equal(ch.err[l].cpu().numpy()[:nb], np.array(oq.err_trace)))
+        if not ok:
+            raise AssertionError(f"chain mismatch: link {l} of {n_links}, n_sym={n_sym}, L={L}, {kind}")
+    key = f"chain/{kind}"
+    stats[key] = stats.get(key, 0) + 1
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--seconds", type=float, default=240.0)
@@ -185,7 +222,8 @@ def main():
     n = 0
     while time.time() - t0 < a.seconds:
         u = rng.random()
-        (aeq_case if u < 0.6 else cdc_case if u < 0.8 else cdc_bank_case)(rng, stats)
+        (aeq_case if u < 0.55 else cdc_case if u < 0.75 else cdc_bank_case if u < 0.9
+         else chain_case)(rng, stats)
         n += 1
     print(f"{n} cases, all bit-exact")
     for k in sorted(stats):

@@ -5,8 +5,9 @@ as the reference allows), random inputs (5-bit, full int8, wide int32 up to the
 encodable +-32768), random step sizes (0, tiny, large enough to saturate), random
 lengths, through both stream layouts and both forward forms; FntCdcEngine with random
 6-bit taps and random stream lengths / input widths; the multi-stream CdcBank on random
-output ranges and input windows (int8 / int32 / float64 quantized on load). Every case
-must be bit-exact (y, w, w_int, saturations, err_trace; CDC outputs).
+output ranges and input windows (int8 / int32 / float64 quantized on load); the whole
+device chain; fnt / ifnt / convolutions on random plans of every prime Fermat modulus.
+Every case must be bit-exact (y, w, w_int, saturations, err_trace; CDC outputs).
 
     python tools/fuzz_parity.py [--seconds 240] [--seed 1]
 """
@@ -211,6 +212,40 @@ def chain_case(rng, stats):
     stats[key] = stats.get(key, 0) + 1
 
 
+def transform_case(rng, stats):
+    """fnt / ifnt / cyclic_convolve_real / _complex on a random valid plan (any prime
+    Fermat modulus F1..F4, any power-of-two length the modulus supports up to 256, a
+    random root of exactly that order: the shift-add kernels for the two shipped
+    plans, the table-driven ones otherwise) and random batch shapes, residues and
+    out-of-range int64 inputs, against the oracle's C restatement."""
+    t = int(rng.integers(1, 5))
+    F = (1 << (1 << t)) + 1
+    n = 1 << int(rng.integers(1, min(1 << t, 8) + 1))
+    while True:
+        alpha = pow(int(rng.integers(2, F)), (F - 1) // n, F)
+        if pow(alpha, n // 2, F) == F - 1:
+            break
+    if rng.random() < 0.3:  # the shipped shift-add plans
+        (t, n, alpha), F = (rng.choice([(4, 32, 2), (4, 64, 4080)]).tolist()), 65537
+    plan = P.make_plan(P.FermatParams(t), alpha, n)
+    op = O.Plan(t, n, alpha)
+    shape = tuple(int(v) for v in rng.integers(1, 40, int(rng.integers(1, 3)))) + (n,)
+    wide = rng.random() < 0.3
+    x = rng.integers(-(1 << 40), 1 << 40, shape) if wide else rng.integers(0, F, shape)
+    ok = np.array_equal(P.fnt(plan, x), O.fnt(op, x)) and np.array_equal(P.ifnt(plan, x), O.ifnt(op, x))
+    xr, xi, yr, yi = (rng.integers(0, F, shape) for _ in range(4))
+    ok = ok and np.array_equal(P.cyclic_convolve_real(plan, xr, yr), O.cyclic_real(op, xr, yr))
+    y1 = yr.reshape(-1, n)[0]
+    ok = ok and np.array_equal(P.cyclic_convolve_real(plan, xr, y1), O.cyclic_real(op, xr, y1))
+    zr, zi = P.cyclic_convolve_complex(plan, xr, xi, yr, yi)
+    orr, ori = O.cyclic_complex(op, xr, xi, yr, yi)
+    ok = ok and np.array_equal(zr, orr) and np.array_equal(zi, ori)
+    key = f"transform/F{t}/n{n}"
+    stats[key] = stats.get(key, 0) + 1
+    if not ok:
+        raise AssertionError(f"transform mismatch: t={t} n={n} alpha={alpha} shape={shape} wide={wide}")
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--seconds", type=float, default=240.0)
@@ -222,8 +257,8 @@ def main():
     n = 0
     while time.time() - t0 < a.seconds:
         u = rng.random()
-        (aeq_case if u < 0.55 else cdc_case if u < 0.75 else cdc_bank_case if u < 0.9
-         else chain_case)(rng, stats)
+        (aeq_case if u < 0.5 else cdc_case if u < 0.65 else cdc_bank_case if u < 0.8
+         else chain_case if u < 0.9 else transform_case)(rng, stats)
         n += 1
     print(f"{n} cases, all bit-exact")
     for k in sorted(stats):

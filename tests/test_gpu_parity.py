@@ -941,8 +941,8 @@ def test_randomized_differential_vs_oracle():
     stats = {}
     for _ in range(150):
         u = rng.random()
-        (fz.aeq_case if u < 0.5 else fz.cdc_case if u < 0.65 else fz.cdc_bank_case if u < 0.8
-         else fz.chain_case if u < 0.9 else fz.transform_case)(rng, stats)
+        (fz.aeq_case if u < 0.5 else fz.cdc_case if u < 0.62 else fz.cdc_bank_case if u < 0.74
+         else fz.chain_case if u < 0.84 else fz.transform_case if u < 0.94 else fz.host_case)(rng, stats)
     assert sum(stats.values()) == 150
 
 

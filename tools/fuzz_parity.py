@@ -6,7 +6,8 @@ encodable +-32768), random step sizes (0, tiny, large enough to saturate), rando
 lengths, through both stream layouts and both forward forms; FntCdcEngine with random
 6-bit taps and random stream lengths / input widths; the multi-stream CdcBank on random
 output ranges and input windows (int8 / int32 / float64 quantized on load); the whole
-device chain; fnt / ifnt / convolutions on random plans of every prime Fermat modulus.
+device chain; fnt / ifnt / convolutions on random plans of every prime Fermat modulus;
+the pipelined host-buffer HostCdc / HostChain with random piece and segment counts.
 Every case must be bit-exact (y, w, w_int, saturations, err_trace; CDC outputs).
 
     python tools/fuzz_parity.py [--seconds 240] [--seed 1]
@@ -246,6 +247,53 @@ def transform_case(rng, stats):
         raise AssertionError(f"transform mismatch: t={t} n={n} alpha={alpha} shape={shape} wide={wide}")
 
 
+def host_case(rng, stats):
+    """The pipelined host-buffer APIs with random piece / segment counts: HostCdc (pinned
+    int8 in, int16 out) against one device-resident CDC launch, and HostChain against the
+    device-resident CdcAeqChain (outputs and err_trace), call after call."""
+    import torch
+    from paper_2405_04253_b200.linkgen import DeviceLinkGenerator
+    from paper_2405_04253_b200.stream import CdcAeqChain, CdcBank, HostCdc, HostChain
+    cfg = P.LinkConfig(z_km=75.0)
+    eng = P.FntCdcEngine(cfg.cdc_config("fnt"), cfg.sig_spec())
+    if rng.random() < 0.5:
+        S = int(rng.integers(1, 4))
+        L = int(rng.integers(64, 200_000))
+        x = rng.integers(-15, 16, size=(2, S, L)).astype(np.int8)
+        hc = HostCdc(eng, S, L, pieces=int(rng.integers(1, 12)))
+        yr, yi = hc(torch.from_numpy(x[0]).pin_memory(), torch.from_numpy(x[1]).pin_memory())
+        hc.join()
+        torch.cuda.synchronize()
+        rr = torch.empty((S, L), dtype=torch.int16, device="cuda")
+        ri = torch.empty_like(rr)
+        CdcBank(eng).run(torch.from_numpy(x[0]).cuda(), torch.from_numpy(x[1]).cuda(), length=L,
+                         yr=rr, yi=ri)
+        ok = np.array_equal(yr.numpy(), rr.cpu().numpy()) and np.array_equal(yi.numpy(), ri.cpu().numpy())
+        key = "host/cdc"
+    else:
+        n_links = int(rng.integers(1, 5))
+        n_sym = int(rng.choice([512, 2048, 8192]))
+        L = 2 * n_sym
+        xr, xi = DeviceLinkGenerator(n_sym).generate(n_links, seed=int(rng.integers(1, 1 << 30)))
+        ref = CdcAeqChain(eng, cfg.aeq_config(), n_links, L, cfg.sig_spec(), cfg.mu_schedule())
+        hch = HostChain(eng, cfg.aeq_config(), n_links, L, cfg.sig_spec(), cfg.mu_schedule(),
+                        in_chunks=int(rng.integers(1, 8)), aeq_segments=int(rng.integers(1, 12)))
+        hr = torch.empty(xr.shape, dtype=torch.int8, pin_memory=True)
+        hi = torch.empty(xi.shape, dtype=torch.int8, pin_memory=True)
+        hr.copy_(xr)
+        hi.copy_(xi)
+        torch.cuda.synchronize()
+        y, err = hch(hr, hi)
+        hch.join()
+        ref.run(xr, xi)
+        torch.cuda.synchronize()
+        ok = np.array_equal(y.numpy(), ref.y.cpu().numpy()) and np.array_equal(err.numpy(), ref.err.cpu().numpy())
+        key = "host/chain"
+    stats[key] = stats.get(key, 0) + 1
+    if not ok:
+        raise AssertionError(f"{key} mismatch")
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--seconds", type=float, default=240.0)
@@ -257,8 +305,8 @@ def main():
     n = 0
     while time.time() - t0 < a.seconds:
         u = rng.random()
-        (aeq_case if u < 0.5 else cdc_case if u < 0.65 else cdc_bank_case if u < 0.8
-         else chain_case if u < 0.9 else transform_case)(rng, stats)
+        (aeq_case if u < 0.5 else cdc_case if u < 0.62 else cdc_bank_case if u < 0.74
+         else chain_case if u < 0.84 else transform_case if u < 0.94 else host_case)(rng, stats)
         n += 1
     print(f"{n} cases, all bit-exact")
     for k in sorted(stats):
